@@ -1,0 +1,169 @@
+/*
+ * sketchcu: C ABI of the B200 (sm_100a) hot path of preconditioned data
+ * sparsification (arXiv 1511.00152).
+ *
+ * This is the drop-in boundary. Every entry point replaces one call of the reference
+ * package `sketchpipe` (/root/reference/pkg/src/sketchpipe). Each one cites its
+ * reference file:line. The reference has no FFI of its own because it is pure Python,
+ * so these entry points are what its ctypes binding would call; see INTEGRATION.md.
+ *
+ * Conventions:
+ *  - Plain device pointers and sizes. No framework types appear in any signature.
+ *  - `stream` is a cudaStream_t passed as void*; NULL means the legacy default stream.
+ *    Every call is stream-ordered and asynchronous unless stated otherwise.
+ *  - Samples are rows. X is (n, p) row-major with row stride `ld` elements, which is
+ *    the reference's (p, n) column matrix in Fortran order. Sketch indices/values are
+ *    (n, m) row-major, the same as SparseSketch.indices/.values (sketch.py:64-77).
+ *  - Centres are (p_pad, K) row-major fp64, the same as CenterSet.centers (cluster.py:28-32).
+ *  - Return value: SKC_OK, or an error code with a message from skc_last_error().
+ *    SKC_EDIM maps to the reference's DimensionError and SKC_EPARAM to ParameterError
+ *    (errors.py:4-9). Validation runs before any work is enqueued.
+ *  - Outputs marked "+=" accumulate, so partials from several calls, chunks or ranks
+ *    add up. Outputs marked "=" are overwritten.
+ */
+#ifndef SKETCHCU_H
+#define SKETCHCU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { SKC_OK = 0, SKC_EDIM = 1, SKC_EPARAM = 2, SKC_ECUDA = 3 };
+/* transform kinds, transform.py:81-84 (DCT is outside the GPU hot path: SKC_EPARAM) */
+enum { SKC_KIND_HADAMARD = 0, SKC_KIND_DCT = 1, SKC_KIND_NONE = 2 };
+enum { SKC_F32 = 0, SKC_F64 = 1 };
+
+/* Thread-local message for the last non-OK return on this thread. */
+const char *skc_last_error(void);
+int skc_abi_version(void);
+/* Largest p_pad the kernels are instantiated for (4096). */
+int32_t skc_max_p_pad(void);
+/* Number of kernels this library has launched in the process (for launch accounting). */
+uint64_t skc_launch_count(void);
+
+/* --- L0/L1: signs and transform -------------------------------------------------- */
+
+/* D diagonal as fp64 +-1 (all ones for kind NONE) = PreconditionSpec.signs(),
+ * transform.py:132-143 -> _hash.sign_array, _hash.py:38-43. out: device[p_pad] (=). */
+int skc_signs(uint64_t sign_seed, int32_t p_pad, int32_t kind, double *out, void *stream);
+
+/* precondition_columns, transform.py:241-250, for n rows: Y = H D pad(X). Y: (n, p_pad)
+ * fp64 (=). fp64 arithmetic in the reference's butterfly order, so it is bit-exact. */
+int skc_precondition(const void *X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, int32_t p_pad,
+                     int32_t kind, uint64_t sign_seed, double *Y, void *stream);
+
+/* unprecondition_columns, transform.py:253-261: X = D^T H^T Y, keeping the first p_out
+ * columns (the [:p] truncation of estimators.py:45/129 and cluster.py:388). Y: (n, p_pad)
+ * fp64, X: (n, p_out) fp64 (=). Bit-exact. */
+int skc_unprecondition(const double *Y, int64_t n, int32_t p_pad, int32_t kind, uint64_t sign_seed, int32_t p_out,
+                       double *X, void *stream);
+
+/* Normalised WHT of n rows of length p_pad (fwht_inplace / _fwht_axis0,
+ * transform.py:153-183), fp64 in the reference stage order: bit-exact. X may alias Y. */
+int skc_fwht(const double *Y, int64_t n, int32_t p_pad, double *X, void *stream);
+
+/* --- L2: sampling plan and the fused single-pass sketch ------------------------------ */
+
+/* SamplingPlan.indices_block(col0, col0+n), sketch.py:48-56. The m smallest splitmix64
+ * keys of each column, sorted ascending (=). Bit-exact. */
+int skc_indices(uint64_t master_seed, int64_t col0, int64_t n, int32_t p_pad, int32_t m, int32_t *idx_out,
+                void *stream);
+
+/* sketch_stream body, sketch.py:196-223, for rows [0, n) of X, which are global columns
+ * [col0, col0+n). One pass: zero-pad, signs, normalised WHT, m-of-p_pad selection,
+ * gather. compute_dtype SKC_F64 reproduces the reference values bit for bit;
+ * SKC_F32 is the fast path (about 1e-7 relative). Indices are bit-exact in both.
+ * idx_out: (n, m) int32, val_out: (n, m) of val_dtype (=). */
+int skc_sketch(const void *X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, int32_t p_pad, int32_t kind,
+               uint64_t sign_seed, uint64_t master_seed, int64_t col0, int32_t m, int32_t compute_dtype,
+               int32_t *idx_out, void *val_out, int32_t val_dtype, void *stream);
+
+/* --- L3a: estimators ------------------------------------------------------------------ */
+
+/* Mean accumulation of estimate_mean, estimators.py:39-43: acc[j] += sum of values with
+ * index j (fp64, deterministic order). Also stats[0] += sum of squared values,
+ * stats[1] = max(stats[1], max |value|), and stats[2] += n, which feed
+ * skc_cov_accumulate's fixed-point scale. acc: device[p_pad], stats: device[3]. */
+size_t skc_moments_workspace(int64_t n, int32_t m, int32_t p_pad);
+int skc_moments(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m, int32_t p_pad,
+                double *acc, double *stats, void *workspace, size_t ws_bytes, void *stream);
+
+/* estimate_mean tail, estimators.py:44-45: mean = unprecondition((p_pad/m)*acc/n_total)[:p]
+ * mean: device[p] (=). */
+int skc_mean_finalize(const double *acc, int32_t p, int32_t p_pad, int32_t m, int64_t n_total, int32_t kind,
+                      uint64_t sign_seed, double *mean, void *stream);
+
+/* Raw second moment of estimate_covariance, estimators.py:59-61: the W W^T upper
+ * triangle, packed row-major (entry (a,b), a<=b, at a*p_pad - a*(a-1)/2 + (b-a)), +=
+ * into tri[p_pad*(p_pad+1)/2] fp64. Products go into int32 fixed-point shared-memory
+ * accumulators through native ATOMS.ADD. The scale comes from stats (skc_moments).
+ * Integer sums make the result deterministic; the fp64 error is about 1e-9 relative. */
+size_t skc_cov_workspace(int64_t n, int32_t m, int32_t p_pad);
+int skc_cov_accumulate(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m,
+                       int32_t p_pad, const double *stats, double *tri, void *workspace, size_t ws_bytes,
+                       void *stream);
+
+/* estimate_covariance tail, estimators.py:62-65: scale by (p(p-1)/(m(m-1)))/n_total,
+ * symmetrise, debias the diagonal. C: device[p_pad*p_pad] fp64 (=). */
+int skc_cov_finalize(const double *tri, int32_t p_pad, int32_t m, int64_t n_total, double *C, void *stream);
+
+/* --- L3b: sparsified K-means ---------------------------------------------------------- */
+
+/* _SparseOps.init_centers, cluster.py:175-179: mu[:,k] = sparse column chosen[k] (=). */
+int skc_kmeans_init(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m,
+                    const int64_t *chosen, int32_t K, int32_t p_pad, double *mu, void *stream);
+
+/* _SparseOps.assign, cluster.py:181-187, in the reference's fp64 operation order
+ * (CSR x dense axpy order, numpy pairwise row norm), so labels and d2min are bit-exact.
+ * labels (n) int32, d2min (n) fp64 (=). If prev_labels is non-NULL, out[0] = number of
+ * labels that differ from prev_labels. out[1] = first index of max d2min, which is the
+ * reseed point of cluster.py:213. d2max[0] = that max value. */
+size_t skc_kmeans_assign_workspace(int64_t n, int32_t p_pad, int32_t K);
+int skc_kmeans_assign(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m,
+                      const double *mu, int32_t p_pad, int32_t K, const int32_t *prev_labels, int32_t *labels,
+                      double *d2min, int64_t *out, double *d2max, void *workspace, size_t ws_bytes,
+                      void *stream);
+
+/* numpy pairwise summation of x[0..n) (objective = d2min.sum(), cluster.py:233). Bit-exact
+ * to ndarray.sum. out: device[1] (=). */
+size_t skc_pairwise_sum_workspace(int64_t n);
+int skc_pairwise_sum(const double *x, int64_t n, double *out, void *workspace, size_t ws_bytes, void *stream);
+
+/* _SparseOps.update partial sums, cluster.py:189-208: per (j,k) value sums (fp64) and
+ * sampling counts (int64), plus cluster sizes n_k (int64). Points are grouped by label
+ * with a stable counting sort and summed in fixed chunks, so the result is deterministic.
+ * sums/counts: (p_pad, K), sizes: (K) (=). */
+size_t skc_kmeans_partials_workspace(int64_t n, int32_t m, int32_t p_pad, int32_t K);
+int skc_kmeans_partials(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m,
+                        const int32_t *labels, int32_t p_pad, int32_t K, double *sums, int64_t *counts,
+                        int64_t *sizes, void *workspace, size_t ws_bytes, void *stream);
+
+/* cluster.py:196-210: mu_out[j,k] = sums/counts where counts > 0, else mu_prev. An empty
+ * cluster (sizes[k]==0) keeps mu_prev[:,k] and sets empty[k]=1. mu_out (=), empty (K) int32 (=). */
+int skc_kmeans_centers(const double *sums, const int64_t *counts, const int64_t *sizes, const double *mu_prev,
+                       int32_t p_pad, int32_t K, double *mu_out, int32_t *empty, void *stream);
+
+/* _SparseOps.reseed, cluster.py:212-215, for every k with empty[k]: mu[:,k] = 0 except
+ * the m sampled coordinates of the reseed point (idx_c, val_c: one sketch row). */
+int skc_kmeans_reseed(const int32_t *idx_c, const void *val_c, int32_t val_dtype, int32_t m, const int32_t *empty,
+                      int32_t p_pad, int32_t K, double *mu, void *stream);
+
+/* Row norms ||v_i||^2 of the sketch in numpy's pairwise order (the colsq of
+ * cluster.py:148). out: (n) fp64 (=). */
+int skc_row_sqnorms(const void *val, int32_t val_dtype, int64_t n, int32_t m, double *out, void *stream);
+
+/* _SparseOps.d2_to_point, cluster.py:169-173: out[i] = (p_pad/m) * max(0, colsq[i] +
+ * colsq[c] - 2 <w_i, w_c>). The inner product runs over shared coordinates in the row's
+ * index order, as scipy's sparse product does. dense: device[p_pad] scratch. out: (n)
+ * fp64 (=). */
+int skc_kmeans_d2_to_point(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m,
+                           int32_t p_pad, int64_t c, const double *colsq, double *dense, double *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SKETCHCU_H */

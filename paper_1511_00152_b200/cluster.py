@@ -1,0 +1,350 @@
+"""Sparsified K-means on a GPU sketch; the drop-in for cluster.py:28-404 (hot-path part).
+
+Per Lloyd iteration on the device:
+  K5 ``skc_kmeans_assign``    distances over each point's m sampled coordinates,
+                              bit-exact fp64 (scipy CSR x dense axpy order)
+     ``skc_pairwise_sum``     objective sum(d2min) in numpy's pairwise order
+  K6 ``skc_kmeans_partials``  per-(j,k) sums and sampling counts, deterministic
+     ``skc_kmeans_centers``   divide / keep previous / empty flags
+     ``skc_kmeans_reseed``    empty clusters take the farthest point (cluster.py:212-215)
+One small device-to-host read per iteration (changed-label count, objective, reseed
+row) drives the stopping rule of cluster.py:235-236.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import dist
+from .errors import ParameterError
+from .sketch import SparseSketch, as_source, plan_for, sketch_stream
+from .transform import PreconditionSpec, unprecondition_columns
+
+ORIGINAL = "original"
+PRECONDITIONED = "preconditioned"
+_TAG_RUN_SIGN, _TAG_RUN_SAMPLE = 0xD5, 0x5A  # cluster.py:362-363
+
+
+@dataclass
+class CenterSet:
+    K: int
+    centers: np.ndarray  # (p, K)
+    domain: str = ORIGINAL
+
+
+@dataclass
+class Assignments:
+    labels: np.ndarray  # (n,)
+
+
+@dataclass
+class CountDiagonal:
+    """Per-cluster, per-coordinate sampling counts n_k^(j), shape (p, K); cluster.py:40-59"""
+
+    counts: np.ndarray
+
+    def cluster_sizes(self, m: int) -> np.ndarray:
+        return self.counts.sum(axis=0) // m
+
+    def hk_deviations(self, m: int) -> np.ndarray:
+        p = self.counts.shape[0]
+        n_k = self.counts.sum(axis=0) / m
+        safe = np.where(n_k > 0, n_k, 1.0)
+        dev = np.abs(p * self.counts / (m * safe)[None, :] - 1.0).max(axis=0)
+        return np.where(n_k > 0, dev, np.nan)
+
+
+@dataclass
+class KMeansResult:
+    assignments: Assignments
+    centers: CenterSet
+    objective: float
+    diagnostics: dict = field(default_factory=dict)
+
+
+def derive_seed(seed: int, tag: int) -> int:
+    """_hash.py:33-35 (splitmix64 of seed ^ tag), evaluated on the host for the two run seeds."""
+    z = (int(seed) ^ int(tag)) & 0xFFFFFFFFFFFFFFFF
+    M = 0xFFFFFFFFFFFFFFFF
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+    return z ^ (z >> 31)
+
+
+class SketchKMeans:
+    """Device state of the sparsified Lloyd iteration on one sketch (the _SparseOps analogue)."""
+
+    def __init__(self, sketch: SparseSketch):
+        self.sketch = sketch
+        self.n, self.m, self.p = sketch.n, sketch.m, sketch.p
+        self.dev = sketch.indices.device
+        self.idx = sketch.indices.contiguous()
+        self.val = sketch.values.contiguous()
+        self.vcode = _lib.dtype_code(self.val)
+        self.col0 = int(getattr(sketch, "col0", 0))
+        self._ws = {}
+
+    def _workspace(self, key, nbytes):
+        w = self._ws.get(key)
+        if w is None or w.numel() < nbytes:
+            w = _lib.workspace(nbytes, self.dev)
+            self._ws[key] = w
+        return w
+
+    def _st(self):
+        return _lib.stream_ptr(self.dev)
+
+    def init_centers(self, chosen) -> torch.Tensor:
+        """cluster.py:175-179"""
+        ch = torch.as_tensor(np.asarray(chosen, dtype=np.int64), device=self.dev)
+        K = int(ch.numel())
+        mu = torch.empty((self.p, K), dtype=torch.float64, device=self.dev)
+        with torch.cuda.device(self.dev):
+            _lib.call("skc_kmeans_init", self.idx.data_ptr(), self.val.data_ptr(), self.vcode, self.n, self.m,
+                      ch.data_ptr(), K, self.p, mu.data_ptr(), self._st())
+        return mu
+
+    def assign(self, mu: torch.Tensor, prev: Optional[torch.Tensor], labels: torch.Tensor, d2min: torch.Tensor,
+               out: torch.Tensor, d2max: torch.Tensor) -> None:
+        """cluster.py:181-187 (+ changed count vs prev, first argmax of d2min)"""
+        K = mu.shape[1]
+        L = _lib.lib()
+        ws = self._workspace("assign", L.skc_kmeans_assign_workspace(self.n, self.p, K))
+        with torch.cuda.device(self.dev):
+            _lib.call("skc_kmeans_assign", self.idx.data_ptr(), self.val.data_ptr(), self.vcode, self.n, self.m,
+                      mu.data_ptr(), self.p, K, _lib.ptr(prev), labels.data_ptr(), d2min.data_ptr(),
+                      out.data_ptr(), d2max.data_ptr(), ws.data_ptr(), ws.numel(), self._st())
+
+    def objective(self, d2min: torch.Tensor, out: torch.Tensor) -> None:
+        with torch.cuda.device(self.dev):
+            _lib.call("skc_pairwise_sum", d2min.data_ptr(), self.n, out.data_ptr(), 0, 0, self._st())
+
+    def partials(self, labels: torch.Tensor, K: int):
+        """cluster.py:189-208 partial sums: (sums, counts, sizes) on the device."""
+        L = _lib.lib()
+        ws = self._workspace("partials", L.skc_kmeans_partials_workspace(self.n, self.m, self.p, K))
+        sums = torch.empty((self.p, K), dtype=torch.float64, device=self.dev)
+        counts = torch.empty((self.p, K), dtype=torch.int64, device=self.dev)
+        sizes = torch.empty(K, dtype=torch.int64, device=self.dev)
+        with torch.cuda.device(self.dev):
+            _lib.call("skc_kmeans_partials", self.idx.data_ptr(), self.val.data_ptr(), self.vcode, self.n, self.m,
+                      labels.data_ptr(), self.p, K, sums.data_ptr(), counts.data_ptr(), sizes.data_ptr(),
+                      ws.data_ptr(), ws.numel(), self._st())
+        return sums, counts, sizes
+
+    def centers(self, sums, counts, sizes, mu_prev):
+        """cluster.py:196-210 -> (mu, empty int32)"""
+        K = mu_prev.shape[1]
+        mu = torch.empty_like(mu_prev)
+        empty = torch.empty(K, dtype=torch.int32, device=self.dev)
+        with torch.cuda.device(self.dev):
+            _lib.call("skc_kmeans_centers", sums.data_ptr(), counts.data_ptr(), sizes.data_ptr(), mu_prev.data_ptr(),
+                      self.p, K, mu.data_ptr(), empty.data_ptr(), self._st())
+        return mu, empty
+
+    def reseed(self, mu, empty, idx_row: torch.Tensor, val_row: torch.Tensor) -> None:
+        """cluster.py:212-215 for every empty cluster, with the farthest point's sketch row."""
+        K = mu.shape[1]
+        with torch.cuda.device(self.dev):
+            _lib.call("skc_kmeans_reseed", idx_row.data_ptr(), val_row.data_ptr(), self.vcode, self.m,
+                      empty.data_ptr(), self.p, K, mu.data_ptr(), self._st())
+
+    def update(self, labels: torch.Tensor, mu_prev: torch.Tensor, group=None):
+        sums, counts, sizes = self.partials(labels, mu_prev.shape[1])
+        if dist.world(group) > 1:
+            for t in (sums, counts, sizes):
+                dist.allreduce_(t, group=group)
+        mu, empty = self.centers(sums, counts, sizes, mu_prev)
+        return mu, counts, empty
+
+    def lloyd(self, mu0: torch.Tensor, max_iter: int, group=None):
+        return lloyd_loop(self, mu0, max_iter, group)
+
+
+def lloyd_loop(ops, mu0: torch.Tensor, max_iter: int, group=None):
+    """The _lloyd_iterate loop body from given centres; cluster.py:230-241.
+
+    ``ops`` holds one shard (or all) of the sketch; with a process group of size > 1
+    the reductions of dist.py make every rank follow the same trajectory.
+    Returns (labels int32 on ops' device, mu, objective trajectory, iterations, seconds
+    measured with CUDA events).
+    """
+    w = dist.world(group)
+    mu = mu0.clone()
+    n, dev = ops.n, ops.dev
+    n_global = n
+    if w > 1:
+        t = torch.tensor([n], dtype=torch.int64, device=dev)
+        n_global = int(dist.allreduce_(t, group=group).item())
+    lab = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(2)]
+    d2min = torch.empty(n, dtype=torch.float64, device=dev)
+    out = torch.zeros(2, dtype=torch.int64, device=dev)
+    d2max = torch.zeros(1, dtype=torch.float64, device=dev)
+    obj = torch.zeros(1, dtype=torch.float64, device=dev)
+    stage = torch.empty(4, dtype=torch.float64, device=dev)
+    traj, iters, prev = [], 0, None
+    cur = lab[0]
+    timed = dev.type == "cuda"
+    if timed:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+    for it in range(max_iter):
+        cur = lab[it % 2]
+        ops.assign(mu, prev, cur, d2min, out, d2max)
+        ops.objective(d2min, obj)
+        stage[0:2].copy_(out)  # changed, local argmax row (exact below 2^53)
+        stage[2:3].copy_(obj)
+        stage[3:4].copy_(d2max)
+        if w > 1:
+            red = stage[0:1].clone()
+            dist.allreduce_(red, group=group)
+            obj_sum = stage[2:3].clone()
+            dist.allreduce_(obj_sum, group=group)
+            stage[0:1].copy_(red)
+            stage[2:3].copy_(obj_sum)
+        host = stage.cpu()  # the one device-to-host read of the iteration
+        changed, arg_local, objective, vmax = int(host[0]), int(host[1]), float(host[2]), float(host[3])
+        traj.append(objective)
+        iters += 1
+        if prev is not None and changed == 0:
+            break
+        prev = cur
+        mu, _, empty = ops.update(cur, mu, group)
+        # reseed point: global first argmax of d2min (cluster.py:213)
+        if w > 1:
+            g_local = ops.col0 + arg_local if arg_local >= 0 else -1
+            _, g = dist.global_first_argmax(vmax, g_local, dev, group)
+            owner = dist.owner_of(g, n_global, w)
+            row = g - ops.col0
+            mine = dist.rank(group) == owner
+            idx_row, val_row = dist.broadcast_row(ops.idx[row] if mine else None, ops.val[row] if mine else None,
+                                                  ops.m, ops.val.dtype, owner, dev, group)
+        else:
+            r = max(arg_local, 0)
+            idx_row, val_row = ops.idx[r], ops.val[r]
+        ops.reseed(mu, empty, idx_row, val_row)
+    secs = 0.0
+    if timed:
+        e1.record()
+        e1.synchronize()
+        secs = e0.elapsed_time(e1) * 1e-3
+    return cur, mu, traj, iters, secs
+
+
+def _labels_to_device(labels, dev) -> torch.Tensor:
+    if isinstance(labels, torch.Tensor):
+        return labels.to(device=dev, dtype=torch.int32).contiguous()
+    return torch.as_tensor(np.asarray(labels, dtype=np.int64), device=dev).to(torch.int32)
+
+
+def sparsified_assign(sketch: SparseSketch, i: int, mu_prime: CenterSet) -> int:
+    """Nearest centre for one column over its m sampled coordinates; cluster.py:306-311.
+
+    Uses the K5 kernel on row i: the same argmin, with ties going to the lowest index.
+    """
+    ops = SketchKMeans(sketch)
+    mu = torch.as_tensor(np.asarray(mu_prime.centers, dtype=np.float64), device=ops.dev).contiguous()
+    one = SketchKMeans(SparseSketch(sketch.spec, 1, sketch.indices[i : i + 1], sketch.values[i : i + 1]))
+    lab = torch.empty(1, dtype=torch.int32, device=ops.dev)
+    d2 = torch.empty(1, dtype=torch.float64, device=ops.dev)
+    out = torch.zeros(2, dtype=torch.int64, device=ops.dev)
+    mx = torch.zeros(1, dtype=torch.float64, device=ops.dev)
+    one.assign(mu, None, lab, d2, out, mx)
+    return int(lab.item())
+
+
+def sparsified_update_centers(sketch: SparseSketch, assignments: Assignments, K: int = None,
+                              prev_centers: CenterSet = None):
+    """Entry-wise sample means per cluster + sampling counts; cluster.py:314-339"""
+    labels = np.asarray(assignments.labels.cpu() if isinstance(assignments.labels, torch.Tensor)
+                        else assignments.labels, dtype=np.int64)
+    if K is None:
+        K = int(labels.max()) + 1
+    if labels.size and (labels.min() < 0 or labels.max() >= K):
+        raise ParameterError("labels must lie in [0, K)")
+    ops = SketchKMeans(sketch)
+    mu_prev = (torch.as_tensor(np.asarray(prev_centers.centers, dtype=np.float64), device=ops.dev).contiguous()
+               if prev_centers is not None else torch.zeros((sketch.p, K), dtype=torch.float64, device=ops.dev))
+    mu, counts, _ = ops.update(_labels_to_device(labels, ops.dev), mu_prev)
+    return (CenterSet(K=K, centers=mu.cpu().numpy(), domain=PRECONDITIONED),
+            CountDiagonal(counts=counts.cpu().numpy()))
+
+
+def _initial_centers(ops: SketchKMeans, K: int, init, restart: int, seed: int) -> torch.Tensor:
+    if init is None:
+        from .kmeanspp import kmeanspp_select
+
+        chosen = kmeanspp_select(ops, K, seed, restart)
+        return ops.init_centers(chosen)
+    if isinstance(init, CenterSet):
+        return torch.as_tensor(np.asarray(init.centers, dtype=np.float64), device=ops.dev).contiguous()
+    arr = np.asarray(init)
+    if arr.ndim == 1:  # K chosen point indices (init_centers semantics)
+        if arr.shape[0] != K:
+            raise ParameterError(f"init lists {arr.shape[0]} points, K={K}")
+        return ops.init_centers(arr.astype(np.int64))
+    if arr.ndim == 2 and arr.shape == (ops.p, K):
+        return torch.as_tensor(arr.astype(np.float64), device=ops.dev).contiguous()
+    raise ParameterError("init must be K point indices or a (p_pad, K) centre matrix")
+
+
+def _sparsified_on_sketch(sketch: SparseSketch, K: int, max_iter: int = 100, n_init: int = 20, seed: int = 0,
+                          init=None) -> KMeansResult:
+    """cluster.py:375-404. ``init`` (K point indices or centres) replaces K-means++ and
+    runs a single restart."""
+    ops = SketchKMeans(sketch)
+    restarts = 1 if init is not None else int(n_init)
+    best, iter_seconds, iters_total = None, 0.0, 0
+    for r in range(restarts):
+        mu0 = _initial_centers(ops, K, init, r, seed)
+        labels, mu, traj, iters, secs = ops.lloyd(mu0, max_iter)
+        iter_seconds += secs
+        iters_total += iters
+        if best is None or traj[-1] < best[2][-1]:
+            best = (labels.clone(), mu, traj, iters)
+    labels, mu, traj, iters = best
+    _, counts, _ = ops.update(labels, mu)
+    spec = sketch.spec
+    back = unprecondition_columns(mu, spec)[: spec.p]
+    mu_h = mu.cpu().numpy()
+    return KMeansResult(
+        assignments=Assignments(labels=labels.cpu().numpy().astype(np.int64)),
+        centers=CenterSet(K=K, centers=back.cpu().numpy(), domain=ORIGINAL),
+        objective=traj[-1],
+        diagnostics={
+            "iterations": iters,
+            "iterations_total": iters_total,
+            "objective_curve": traj,
+            "iter_seconds": iter_seconds,
+            "restarts": restarts,
+            "m": sketch.m,
+            "p_pad": sketch.p,
+            "centers_preconditioned": CenterSet(K=K, centers=mu_h, domain=PRECONDITIONED),
+            "count_diagonal": CountDiagonal(counts=counts.cpu().numpy()),
+        },
+    )
+
+
+def sparsified_kmeans(source, K: int, gamma: float, max_iter: int = 100, n_init: int = 20, seed: int = 0,
+                      kind: str = "hadamard", chunk_cols: int = 8192, *, init=None, compute: str = "f64",
+                      device=None) -> KMeansResult:
+    """One-pass sparsified K-means; cluster.py:342-372"""
+    source = as_source(source, chunk_cols=chunk_cols)
+    if K > source.n:
+        raise ParameterError(f"K={K} exceeds number of points n={source.n}")
+    spec = PreconditionSpec.create(kind, source.p, sign_seed=derive_seed(seed, _TAG_RUN_SIGN))
+    plan = plan_for(spec, gamma, master_seed=derive_seed(seed, _TAG_RUN_SAMPLE))
+    t0 = time.perf_counter()
+    sketch = sketch_stream(source, spec, plan, compute=compute, device=device)
+    torch.cuda.synchronize(sketch.indices.device)
+    sketch_seconds = time.perf_counter() - t0
+    result = _sparsified_on_sketch(sketch, K, max_iter=max_iter, n_init=n_init, seed=seed, init=init)
+    result.diagnostics.update(sketch_seconds=sketch_seconds, passes=getattr(source, "passes", None))
+    return result

@@ -1,0 +1,296 @@
+// extern "C" entry points of include/sketchcu.h: argument validation (the reference's
+// DimensionError / ParameterError cases) and dispatch to the kernels.
+#include <stdio.h>
+
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace skc {
+
+static thread_local std::string g_err;
+static std::atomic<uint64_t> g_launches{0};
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(SKC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return SKC_OK;
+}
+int sm_count() {
+  static std::mutex mu;
+  static std::vector<int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if ((int)cache.size() <= dev) cache.resize(dev + 1, 0);
+  if (cache[dev] == 0) {
+    int c = 0;
+    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = c > 0 ? c : 148;
+  }
+  return cache[dev];
+}
+
+// kernels (sketch.cu, moments.cu, kmeans.cu)
+int sketch_launch(const void*, int32_t, int64_t, int64_t, int32_t, int32_t, int32_t, uint64_t, uint64_t, int64_t,
+                  int32_t, int32_t, int32_t*, void*, int32_t, double*, cudaStream_t);
+int sketch_identity(const void*, int32_t, int64_t, int64_t, int32_t, int32_t, uint64_t, int64_t, int32_t, int32_t*,
+                    void*, int32_t, double*, cudaStream_t);
+size_t moments_ws(int64_t, int32_t);
+int moments_launch(const int32_t*, const void*, int, int64_t, int32_t, int32_t, double*, double*, void*,
+                   cudaStream_t);
+int cov_check(int32_t, int32_t);
+size_t cov_ws(int64_t, int32_t, int32_t);
+int cov_launch(const int32_t*, const void*, int, int64_t, int32_t, int32_t, const double*, double*, void*,
+               cudaStream_t);
+int cov_finalize_launch(const double*, int32_t, int32_t, int64_t, double*, cudaStream_t);
+int adjoint_launch(const double*, int64_t, int32_t, int32_t, uint64_t, int32_t, double, double, double*,
+                   cudaStream_t);
+int signs_launch(uint64_t, int32_t, int32_t, double*, cudaStream_t);
+size_t assign_ws(int64_t, int32_t, int32_t);
+int assign_launch(const int32_t*, const void*, int, int64_t, int32_t, const double*, int32_t, int32_t, const int32_t*,
+                  int32_t*, double*, int64_t*, double*, void*, cudaStream_t);
+int pairwise_launch(const double*, int64_t, double*, cudaStream_t);
+size_t partials_ws(int64_t, int32_t, int32_t);
+int partials_check(int32_t, int32_t);
+int partials_launch(const int32_t*, const void*, int, int64_t, int32_t, const int32_t*, int32_t, int32_t, double*,
+                    int64_t*, int64_t*, void*, cudaStream_t);
+int centers_launch(const double*, const int64_t*, const int64_t*, const double*, int32_t, int32_t, double*, int32_t*,
+                   cudaStream_t);
+int reseed_launch(const int32_t*, const void*, int, int32_t, const int32_t*, int32_t, int32_t, double*,
+                  cudaStream_t);
+int init_launch(const int32_t*, const void*, int, int32_t, const int64_t*, int32_t, int32_t, double*, cudaStream_t);
+int row_sqnorms_launch(const void*, int, int64_t, int32_t, double*, cudaStream_t);
+int d2_point_launch(const int32_t*, const void*, int, int64_t, int32_t, int32_t, int64_t, const double*, double*,
+                    double*, cudaStream_t);
+
+}  // namespace skc
+
+using namespace skc;
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+static inline bool pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+constexpr int32_t kMaxPad = 4096;
+
+static int check_spec(int32_t kind, int32_t p, int32_t p_pad) {
+  // PreconditionSpec.__post_init__, transform.py:105-115
+  if (kind == SKC_KIND_DCT) return fail(SKC_EPARAM, "dct preconditioner is not on the GPU hot path");
+  if (kind != SKC_KIND_HADAMARD && kind != SKC_KIND_NONE) return fail(SKC_EPARAM, "unknown transform kind");
+  if (p < 1) return fail(SKC_EDIM, "dimension must be positive");
+  if (p_pad < p) return fail(SKC_EDIM, "padded dimension smaller than original");
+  if (kind == SKC_KIND_HADAMARD && !pow2(p_pad)) return fail(SKC_EDIM, "hadamard padded dimension must be a power of two");
+  if (kind == SKC_KIND_NONE && p_pad != p) return fail(SKC_EDIM, "none transform does not pad");
+  if (p_pad > kMaxPad) return fail(SKC_EPARAM, "p_pad > 4096 is not instantiated on the GPU path");
+  return SKC_OK;
+}
+static int check_m(int32_t m, int32_t p_pad) {
+  // SamplingPlan.__post_init__, sketch.py:36-38
+  if (m < 1 || m > p_pad) {
+    char b[96];
+    snprintf(b, sizeof b, "need 1 <= m <= p, got m=%d, p=%d", m, p_pad);
+    return fail(SKC_EPARAM, b);
+  }
+  return SKC_OK;
+}
+static int check_dtype(int32_t d) {
+  return (d == SKC_F32 || d == SKC_F64) ? SKC_OK : fail(SKC_EPARAM, "dtype must be SKC_F32 or SKC_F64");
+}
+
+extern "C" {
+
+const char* skc_last_error(void) { return g_err.c_str(); }
+int skc_abi_version(void) { return 1; }
+int32_t skc_max_p_pad(void) { return kMaxPad; }
+uint64_t skc_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int skc_signs(uint64_t sign_seed, int32_t p_pad, int32_t kind, double* out, void* stream) {
+  int rc = check_spec(kind, p_pad, p_pad);
+  if (rc) return rc;
+  return signs_launch(sign_seed, p_pad, kind, out, S(stream));
+}
+
+int skc_precondition(const void* X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, int32_t p_pad, int32_t kind,
+                     uint64_t sign_seed, double* Y, void* stream) {
+  int rc;
+  if ((rc = check_spec(kind, p, p_pad)) || (rc = check_dtype(x_dtype))) return rc;
+  if (n < 0 || ld < p) return fail(SKC_EDIM, "expected a (n, p) row block with ld >= p");
+  if (n == 0) return SKC_OK;
+  if (kind == SKC_KIND_NONE)
+    return sketch_identity(X, x_dtype, ld, n, p, p_pad, 0, 0, 1, nullptr, nullptr, SKC_F64, Y, S(stream));
+  return sketch_launch(X, x_dtype, ld, n, p, p_pad, kind, sign_seed, 0, 0, 1, SKC_F64, nullptr, nullptr, SKC_F64, Y,
+                       S(stream));
+}
+
+int skc_unprecondition(const double* Y, int64_t n, int32_t p_pad, int32_t kind, uint64_t sign_seed, int32_t p_out,
+                       double* X, void* stream) {
+  int rc = check_spec(kind, p_pad, p_pad);
+  if (rc) return rc;
+  if (p_out < 1 || p_out > p_pad) return fail(SKC_EDIM, "p_out must be in [1, p_pad]");
+  return adjoint_launch(Y, n, p_pad, kind, sign_seed, p_out, 0.0, 1.0, X, S(stream));
+}
+
+int skc_fwht(const double* Y, int64_t n, int32_t p_pad, double* X, void* stream) {
+  if (!pow2(p_pad)) return fail(SKC_EDIM, "length is not a power of two");
+  if (p_pad > kMaxPad) return fail(SKC_EPARAM, "p_pad > 4096 is not instantiated on the GPU path");
+  return adjoint_launch(Y, n, p_pad, -1, 0, p_pad, 0.0, 1.0, X, S(stream));
+}
+
+int skc_indices(uint64_t master_seed, int64_t col0, int64_t n, int32_t p_pad, int32_t m, int32_t* idx_out,
+                void* stream) {
+  int rc;
+  if ((rc = check_m(m, p_pad))) return rc;
+  if (p_pad < 1 || p_pad > kMaxPad) return fail(SKC_EPARAM, "p_pad out of range for the GPU sampler");
+  if (n <= 0) return SKC_OK;
+  return sketch_launch(nullptr, SKC_F32, 0, n, p_pad, p_pad, SKC_KIND_HADAMARD, 0, master_seed, col0, m, SKC_F32,
+                       idx_out, nullptr, SKC_F32, nullptr, S(stream));
+}
+
+int skc_sketch(const void* X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, int32_t p_pad, int32_t kind,
+               uint64_t sign_seed, uint64_t master_seed, int64_t col0, int32_t m, int32_t compute_dtype,
+               int32_t* idx_out, void* val_out, int32_t val_dtype, void* stream) {
+  int rc;
+  if ((rc = check_spec(kind, p, p_pad)) || (rc = check_m(m, p_pad)) || (rc = check_dtype(x_dtype)) ||
+      (rc = check_dtype(compute_dtype)) || (rc = check_dtype(val_dtype)))
+    return rc;
+  if (n < 0 || ld < p) return fail(SKC_EDIM, "expected a (n, p) row block with ld >= p");
+  if (n == 0) return SKC_OK;
+  if (kind == SKC_KIND_NONE) {
+    return sketch_identity(X, x_dtype, ld, n, p, p_pad, master_seed, col0, m, idx_out, val_out, val_dtype, nullptr,
+                           S(stream));
+  }
+  return sketch_launch(X, x_dtype, ld, n, p, p_pad, kind, sign_seed, master_seed, col0, m, compute_dtype, idx_out,
+                       val_out, val_dtype, nullptr, S(stream));
+}
+
+size_t skc_moments_workspace(int64_t n, int32_t m, int32_t p_pad) {
+  (void)m;
+  return moments_ws(n, p_pad);
+}
+
+int skc_moments(const int32_t* idx, const void* val, int32_t val_dtype, int64_t n, int32_t m, int32_t p_pad,
+                double* acc, double* stats, void* workspace, size_t ws_bytes, void* stream) {
+  int rc;
+  if ((rc = check_dtype(val_dtype))) return rc;
+  if (p_pad < 1 || p_pad > kMaxPad || m < 1 || m > p_pad) return fail(SKC_EDIM, "bad (m, p_pad)");
+  if (ws_bytes < moments_ws(n, p_pad)) return fail(SKC_EPARAM, "workspace too small");
+  return moments_launch(idx, val, val_dtype == SKC_F64, n, m, p_pad, acc, stats, workspace, S(stream));
+}
+
+int skc_mean_finalize(const double* acc, int32_t p, int32_t p_pad, int32_t m, int64_t n_total, int32_t kind,
+                      uint64_t sign_seed, double* mean, void* stream) {
+  int rc;
+  if ((rc = check_spec(kind, p, p_pad))) return rc;
+  if (n_total < 1) return fail(SKC_EPARAM, "empty sketch");
+  // (p / m) * acc / n, estimators.py:44
+  return adjoint_launch(acc, 1, p_pad, kind, sign_seed, p, (double)p_pad / (double)m, (double)n_total, mean,
+                        S(stream));
+}
+
+size_t skc_cov_workspace(int64_t n, int32_t m, int32_t p_pad) { return cov_ws(n, m, p_pad); }
+
+int skc_cov_accumulate(const int32_t* idx, const void* val, int32_t val_dtype, int64_t n, int32_t m, int32_t p_pad,
+                       const double* stats, double* tri, void* workspace, size_t ws_bytes, void* stream) {
+  int rc;
+  if ((rc = check_dtype(val_dtype))) return rc;
+  if (m < 2) return fail(SKC_EPARAM, "covariance estimation needs m >= 2");
+  if (p_pad < 1 || p_pad > kMaxPad || m > p_pad) return fail(SKC_EDIM, "bad (m, p_pad)");
+  if ((rc = cov_check(p_pad, m))) return rc;
+  if (ws_bytes < cov_ws(n, m, p_pad)) return fail(SKC_EPARAM, "workspace too small");
+  return cov_launch(idx, val, val_dtype == SKC_F64, n, m, p_pad, stats, tri, workspace, S(stream));
+}
+
+int skc_cov_finalize(const double* tri, int32_t p_pad, int32_t m, int64_t n_total, double* C, void* stream) {
+  if (m < 2) return fail(SKC_EPARAM, "covariance estimation needs m >= 2");
+  if (n_total < 1) return fail(SKC_EPARAM, "empty sketch");
+  return cov_finalize_launch(tri, p_pad, m, n_total, C, S(stream));
+}
+
+int skc_kmeans_init(const int32_t* idx, const void* val, int32_t val_dtype, int64_t n, int32_t m,
+                    const int64_t* chosen, int32_t K, int32_t p_pad, double* mu, void* stream) {
+  int rc;
+  if ((rc = check_dtype(val_dtype))) return rc;
+  if (K < 1) return fail(SKC_EPARAM, "K must be >= 1");
+  if (K > n) return fail(SKC_EPARAM, "K exceeds number of points n");
+  return init_launch(idx, val, val_dtype == SKC_F64, m, chosen, K, p_pad, mu, S(stream));
+}
+
+size_t skc_kmeans_assign_workspace(int64_t n, int32_t p_pad, int32_t K) { return assign_ws(n, p_pad, K); }
+
+int skc_kmeans_assign(const int32_t* idx, const void* val, int32_t val_dtype, int64_t n, int32_t m, const double* mu,
+                      int32_t p_pad, int32_t K, const int32_t* prev_labels, int32_t* labels, double* d2min,
+                      int64_t* out, double* d2max, void* workspace, size_t ws_bytes, void* stream) {
+  int rc;
+  if ((rc = check_dtype(val_dtype))) return rc;
+  if (K < 1) return fail(SKC_EPARAM, "K must be >= 1");
+  if (m < 1 || m > p_pad) return fail(SKC_EDIM, "bad (m, p_pad)");
+  if ((size_t)8 * m * 20 > 227 * 1024) return fail(SKC_EPARAM, "m too large for the assignment kernel");
+  if (ws_bytes < assign_ws(n, p_pad, K)) return fail(SKC_EPARAM, "workspace too small");
+  return assign_launch(idx, val, val_dtype == SKC_F64, n, m, mu, p_pad, K, prev_labels, labels, d2min, out, d2max,
+                       workspace, S(stream));
+}
+
+size_t skc_pairwise_sum_workspace(int64_t n) {
+  (void)n;
+  return 0;
+}
+
+int skc_pairwise_sum(const double* x, int64_t n, double* out, void* workspace, size_t ws_bytes, void* stream) {
+  (void)workspace;
+  (void)ws_bytes;
+  if (n < 0) return fail(SKC_EDIM, "negative length");
+  return pairwise_launch(x, n, out, S(stream));
+}
+
+size_t skc_kmeans_partials_workspace(int64_t n, int32_t m, int32_t p_pad, int32_t K) {
+  (void)m;
+  return partials_ws(n, p_pad, K);
+}
+
+int skc_kmeans_partials(const int32_t* idx, const void* val, int32_t val_dtype, int64_t n, int32_t m,
+                        const int32_t* labels, int32_t p_pad, int32_t K, double* sums, int64_t* counts,
+                        int64_t* sizes, void* workspace, size_t ws_bytes, void* stream) {
+  int rc;
+  if ((rc = check_dtype(val_dtype))) return rc;
+  if (K < 1) return fail(SKC_EPARAM, "K must be >= 1");
+  if ((rc = partials_check(p_pad, K))) return rc;
+  if (ws_bytes < partials_ws(n, p_pad, K)) return fail(SKC_EPARAM, "workspace too small");
+  return partials_launch(idx, val, val_dtype == SKC_F64, n, m, labels, p_pad, K, sums, counts, sizes, workspace,
+                         S(stream));
+}
+
+int skc_kmeans_centers(const double* sums, const int64_t* counts, const int64_t* sizes, const double* mu_prev,
+                       int32_t p_pad, int32_t K, double* mu_out, int32_t* empty, void* stream) {
+  if (K < 1) return fail(SKC_EPARAM, "K must be >= 1");
+  return centers_launch(sums, counts, sizes, mu_prev, p_pad, K, mu_out, empty, S(stream));
+}
+
+int skc_kmeans_reseed(const int32_t* idx_c, const void* val_c, int32_t val_dtype, int32_t m, const int32_t* empty,
+                      int32_t p_pad, int32_t K, double* mu, void* stream) {
+  int rc;
+  if ((rc = check_dtype(val_dtype))) return rc;
+  return reseed_launch(idx_c, val_c, val_dtype == SKC_F64, m, empty, p_pad, K, mu, S(stream));
+}
+
+int skc_row_sqnorms(const void* val, int32_t val_dtype, int64_t n, int32_t m, double* out, void* stream) {
+  int rc;
+  if ((rc = check_dtype(val_dtype))) return rc;
+  return row_sqnorms_launch(val, val_dtype == SKC_F64, n, m, out, S(stream));
+}
+
+int skc_kmeans_d2_to_point(const int32_t* idx, const void* val, int32_t val_dtype, int64_t n, int32_t m,
+                           int32_t p_pad, int64_t c, const double* colsq, double* dense, double* out, void* stream) {
+  int rc;
+  if ((rc = check_dtype(val_dtype))) return rc;
+  if (c < 0 || c >= n) return fail(SKC_EPARAM, "point index out of range");
+  return d2_point_launch(idx, val, val_dtype == SKC_F64, n, m, p_pad, c, colsq, dense, out, S(stream));
+}
+
+}  // extern "C"

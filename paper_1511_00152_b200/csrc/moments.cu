@@ -1,0 +1,484 @@
+// K2 moments (mean accumulation + value statistics), K3 covariance band accumulation,
+// K4 covariance finalize, K7 adjoint transform (mean / PCs / centres).
+// Reference: estimators.py:30-66, transform.py:153-200.
+#include <math.h>
+
+#include "common.cuh"
+
+namespace skc {
+
+constexpr uint32_t kFullMask = 0xFFFFFFFFu;
+
+// ======================================================================================
+// K2: acc[j] += sum of values with index j (estimators.py:39-43), plus sum of squares and
+// max |v| for K3's fixed-point scale. Each warp owns a private fp64 p-vector in smem and
+// walks a fixed contiguous range of rows. Indices are distinct within a row, so lanes
+// never collide. Warps combine in order, then CTAs combine in order, so the result is
+// deterministic.
+// ======================================================================================
+int moments_grid(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  const int64_t cap = 2 * (int64_t)sm_count();
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+static int moments_warps(int32_t p_pad) {
+  int w = 8;
+  while (w > 1 && (size_t)w * p_pad * 8 > 128 * 1024) w >>= 1;
+  return w;
+}
+
+template <typename V>
+__global__ void moments_kernel(const int32_t* __restrict__ idx, const V* __restrict__ val, int64_t n, int32_t m,
+                               int32_t p_pad, double* __restrict__ part) {
+  extern __shared__ double wvec[];  // [warps][p_pad]
+  const int warps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* mine = wvec + (size_t)warp * p_pad;
+  for (int j = lane; j < p_pad; j += 32) mine[j] = 0.0;
+  __syncwarp();
+  const int64_t c0 = n * blockIdx.x / gridDim.x, c1 = n * (blockIdx.x + 1) / gridDim.x;
+  const int64_t r0 = c0 + (c1 - c0) * warp / warps, r1 = c0 + (c1 - c0) * (warp + 1) / warps;
+  double sq = 0.0, mx = 0.0;
+  for (int64_t r = r0; r < r1; ++r) {
+    for (int t = lane; t < m; t += 32) {
+      const int j = __ldg(idx + r * m + t);
+      const double v = (double)__ldg(val + r * m + t);
+      mine[j] = dadd(mine[j], v);
+      sq = dadd(sq, dmul(v, v));
+      mx = fmax(mx, fabs(v));
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sq = dadd(sq, __shfl_xor_sync(kFullMask, sq, o));
+    mx = fmax(mx, __shfl_xor_sync(kFullMask, mx, o));
+  }
+  __shared__ double wsq[32], wmx[32];
+  if (lane == 0) {
+    wsq[warp] = sq;
+    wmx[warp] = mx;
+  }
+  __syncthreads();
+  double* out = part + (size_t)blockIdx.x * (p_pad + 2);
+  for (int j = threadIdx.x; j < p_pad; j += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < warps; ++w) s = dadd(s, wvec[(size_t)w * p_pad + j]);
+    out[j] = s;
+  }
+  if (threadIdx.x == 0) {
+    double s = 0.0, x = 0.0;
+    for (int w = 0; w < warps; ++w) {
+      s = dadd(s, wsq[w]);
+      x = fmax(x, wmx[w]);
+    }
+    out[p_pad] = s;
+    out[p_pad + 1] = x;
+  }
+}
+
+__global__ void moments_reduce_kernel(const double* __restrict__ part, int G, int32_t p_pad, int64_t n,
+                                      double* __restrict__ acc, double* __restrict__ stats) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < p_pad) {
+    double s = 0.0;
+    for (int g = 0; g < G; ++g) s = dadd(s, part[(size_t)g * (p_pad + 2) + j]);
+    acc[j] = dadd(acc[j], s);
+  } else if (j == p_pad && stats != nullptr) {
+    double s = 0.0, x = 0.0;
+    for (int g = 0; g < G; ++g) {
+      s = dadd(s, part[(size_t)g * (p_pad + 2) + p_pad]);
+      x = fmax(x, part[(size_t)g * (p_pad + 2) + p_pad + 1]);
+    }
+    stats[0] = dadd(stats[0], s);
+    stats[1] = fmax(stats[1], x);
+    stats[2] = dadd(stats[2], (double)n);
+  }
+}
+
+size_t moments_ws(int64_t n, int32_t p_pad) { return (size_t)moments_grid(n) * (p_pad + 2) * sizeof(double); }
+
+int moments_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, int32_t p_pad,
+                   double* acc, double* stats, void* ws, cudaStream_t st) {
+  const int G = moments_grid(n);
+  const int W = moments_warps(p_pad);
+  const size_t smem = (size_t)W * p_pad * sizeof(double);
+  double* part = reinterpret_cast<double*>(ws);
+  if (n > 0) {
+    if (val_f64) {
+      cudaFuncSetAttribute(moments_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      moments_kernel<double><<<G, W * 32, smem, st>>>(idx, (const double*)val, n, m, p_pad, part);
+    } else {
+      cudaFuncSetAttribute(moments_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      moments_kernel<float><<<G, W * 32, smem, st>>>(idx, (const float*)val, n, m, p_pad, part);
+    }
+    int rc = check_launch("moments_kernel");
+    if (rc) return rc;
+    moments_reduce_kernel<<<(p_pad + 1 + 255) / 256, 256, 0, st>>>(part, G, p_pad, n, acc, stats);
+    return check_launch("moments_reduce_kernel");
+  }
+  return SKC_OK;
+}
+
+// ======================================================================================
+// K3: raw W W^T upper triangle (estimators.py:59-61), in row bands that fit shared memory.
+// CTA (band b, group g) holds band b as 64-bit fixed point split into two int32 words.
+// Each product w_a*w_b is scaled by 2^S (|q| <= 2^30 for |w| <= tau) and added to `lo`
+// with a native ATOMS.ADD; the returned old value gives the carry, and the rare nonzero
+// carry/borrow goes into `hi` with a second ATOMS.ADD. The sum is exact and independent
+// of order, so the result is deterministic. tau = 8 * rms(values) from K2's statistics.
+// A row that holds a value above tau is queued and added in fp64, in ascending row
+// order, at the end of its window. At the end each CTA writes its band to a private fp64
+// partial, and a reduce kernel sums the groups in fixed order. Error vs exact fp64:
+// ~6e-8 of tau^2 per product (quantum + fp32 product), random, so ~1e-7 relative.
+// ======================================================================================
+constexpr int kSmemBudget = 220 * 1024;  // dynamic smem per CTA: band + row staging
+constexpr int kWindow = 4096;            // rows between outlier-queue drains
+constexpr int kQueue = 512;              // outlier rows per window
+constexpr int kCovWarps = 8;
+constexpr int kMaxBands = 511;
+
+__host__ __device__ inline int64_t tri_off(int64_t a, int64_t p) { return a * p - a * (a - 1) / 2; }
+
+static int band_capacity(int32_t m) {
+  return (kSmemBudget - kCovWarps * m * 8) / 8;  // (lo, hi) entries left after row staging
+}
+// greedy row bands of <= cap entries; returns the count, fills out[0..count] if given
+static int make_bands(int32_t p_pad, int cap, int* out) {
+  int nb = 0, a = 0;
+  while (a < p_pad) {
+    int64_t e = 0;
+    int r = a;
+    while (r < p_pad && e + (p_pad - r) <= cap) {
+      e += p_pad - r;
+      ++r;
+    }
+    if (r == a) r = a + 1;
+    if (out && nb < kMaxBands) out[nb] = a;
+    ++nb;
+    a = r;
+  }
+  if (out && nb <= kMaxBands) out[nb] = p_pad;
+  return nb;
+}
+
+struct CovParams {
+  const int32_t* idx;
+  const void* val;
+  int64_t n;
+  int32_t m, p_pad;
+  const double* stats;
+  double* part;  // [groups][tri_total] fp64 partials, each CTA owns its band slice
+  int nbands, groups;
+  int band_rows[kMaxBands + 1];
+};
+
+template <typename V>
+__device__ __forceinline__ float ldv32(const void* p, int64_t i) {
+  return (float)__ldg(reinterpret_cast<const V*>(p) + i);
+}
+template <typename V>
+__device__ __forceinline__ double ldv64(const void* p, int64_t i) {
+  return (double)__ldg(reinterpret_cast<const V*>(p) + i);
+}
+
+__device__ __forceinline__ void fx_add(uint32_t* lo, int* hi, int e, int q) {
+  const uint32_t uq = (uint32_t)q;
+  const uint32_t old = atomicAdd(lo + e, uq);
+  const int delta = (int)(old + uq < old) - (int)(q < 0);
+  if (delta != 0) atomicAdd(hi + e, delta);
+}
+
+template <typename V>
+__global__ void __launch_bounds__(kCovWarps * 32) cov_band_kernel(const __grid_constant__ CovParams P) {
+  extern __shared__ int smem_i[];
+  __shared__ int qcount;
+  __shared__ int64_t queue[kQueue];
+  const int m = P.m;
+  const int band = blockIdx.x % P.nbands, group = blockIdx.x / P.nbands;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = P.band_rows[band], r1 = P.band_rows[band + 1];
+  const int64_t e0 = tri_off(r0, P.p_pad), e1 = tri_off(r1, P.p_pad);
+  const int ne = (int)(e1 - e0);
+  uint32_t* lo = reinterpret_cast<uint32_t*>(smem_i);
+  int* hi = smem_i + ne;
+  float* sval = reinterpret_cast<float*>(smem_i + 2 * ne) + (size_t)warp * m;
+  int* sidx = smem_i + 2 * ne + (size_t)kCovWarps * m + (size_t)warp * m;
+  double* part = P.part + (size_t)group * tri_off(P.p_pad, P.p_pad) + e0;
+
+  // scale: |w| <= tau -> |q| <= 2^30
+  const double cnt = P.stats[2] * (double)m;
+  const double rms = cnt > 0 ? sqrt(P.stats[0] / cnt) : 0.0;
+  double tau = 8.0 * rms;
+  if (!(tau > 0.0)) tau = 1.0;
+  int S = (int)floor(log2(1073741824.0 / (tau * tau)));
+  S &= ~1;  // even, so each factor carries 2^(S/2)
+  const float half = (float)ldexp(1.0, S / 2);
+  const double inv = ldexp(1.0, -S);
+  const float ftau = (float)tau;
+
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+    lo[e] = 0u;
+    hi[e] = 0;
+    part[e] = 0.0;
+  }
+  if (threadIdx.x == 0) qcount = 0;
+  __syncthreads();
+
+  const int64_t g0 = P.n * group / P.groups, g1 = P.n * (group + 1) / P.groups;
+  for (int64_t w0 = g0; w0 < g1; w0 += kWindow) {
+    const int64_t w1 = min(w0 + (int64_t)kWindow, g1);
+    for (int64_t r = w0 + warp; r < w1; r += kCovWarps) {
+      bool big = false;
+      int nlo = 0, nhi = 0;  // # indices < r0 and < r1 (rows are sorted)
+      for (int t = lane; t < m; t += 32) {
+        const int j = __ldg(P.idx + r * m + t);
+        const float v = ldv32<V>(P.val, r * m + t);
+        sidx[t] = j;
+        sval[t] = v * half;
+        big |= fabsf(v) > ftau;
+        nlo += j < r0;
+        nhi += j < r1;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        nlo += __shfl_xor_sync(kFullMask, nlo, o);
+        nhi += __shfl_xor_sync(kFullMask, nhi, o);
+      }
+      big = __any_sync(kFullMask, big);
+      __syncwarp();
+      if (nlo == nhi) continue;  // none of this row's indices fall in the band
+      if (big) {
+        int q = 0;
+        if (lane == 0) q = atomicAdd(&qcount, 1);
+        q = __shfl_sync(kFullMask, q, 0);
+        if (q < kQueue) {
+          if (lane == 0) queue[q] = r;
+        } else {
+          // queue full (pathological scale): add in fp64 right away (order not fixed)
+          for (int t = nlo; t < nhi; ++t) {
+            const int a = sidx[t];
+            const double va = ldv64<V>(P.val, r * m + t);
+            const int64_t base = tri_off(a, P.p_pad) - e0 - a;
+            for (int u = t + lane; u < m; u += 32)
+              atomicAdd(&part[base + sidx[u]], dmul(va, ldv64<V>(P.val, r * m + u)));
+          }
+        }
+        __syncwarp();
+        continue;
+      }
+      for (int t = nlo; t < nhi; ++t) {
+        const int a = sidx[t];
+        const float va = sval[t];
+        const int base = (int)(tri_off(a, P.p_pad) - e0) - a;
+        for (int u = t + lane; u < m; u += 32) fx_add(lo, hi, base + sidx[u], __float2int_rn(va * sval[u]));
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    // queued rows with a value above tau: fp64 products, ascending row order, warp 0
+    const int nq = min(qcount, kQueue);
+    if (warp == 0 && nq > 0) {
+      if (lane == 0) {
+        for (int i = 1; i < nq; ++i) {
+          const int64_t x = queue[i];
+          int k = i - 1;
+          while (k >= 0 && queue[k] > x) {
+            queue[k + 1] = queue[k];
+            --k;
+          }
+          queue[k + 1] = x;
+        }
+      }
+      __syncwarp();
+      for (int qi = 0; qi < nq; ++qi) {
+        const int64_t r = queue[qi];
+        for (int t = 0; t < m; ++t) {
+          const int a = __ldg(P.idx + r * m + t);
+          if (a < r0 || a >= r1) continue;
+          const double va = ldv64<V>(P.val, r * m + t);
+          const int64_t base = tri_off(a, P.p_pad) - e0 - a;
+          for (int u = t + lane; u < m; u += 32) {
+            const int b = __ldg(P.idx + r * m + u);
+            part[base + b] = dadd(part[base + b], dmul(va, ldv64<V>(P.val, r * m + u)));
+          }
+          __syncwarp();
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) qcount = 0;
+    __syncthreads();
+  }
+  // fixed-point total -> fp64 partial
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+    const int64_t q = ((int64_t)hi[e] << 32) + (int64_t)lo[e];
+    if (q != 0) part[e] = dadd(part[e], (double)q * inv);
+  }
+}
+
+__global__ void cov_reduce_kernel(const double* __restrict__ part, int groups, int64_t total,
+                                  double* __restrict__ tri) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  double s = 0.0;
+  for (int g = 0; g < groups; ++g) s = dadd(s, part[(size_t)g * total + e]);
+  tri[e] = dadd(tri[e], s);
+}
+
+static int cov_groups(int nbands, int64_t n) {
+  int g = sm_count() / nbands;
+  if (g < 1) g = 1;
+  const int64_t maxg = (n + 1023) / 1024;
+  if (g > maxg) g = (int)(maxg < 1 ? 1 : maxg);
+  return g;
+}
+
+int cov_check(int32_t p_pad, int32_t m) {
+  if (band_capacity(m) < p_pad) return fail(SKC_EPARAM, "m too large for the shared-memory covariance bands");
+  if (make_bands(p_pad, band_capacity(m), nullptr) > kMaxBands)
+    return fail(SKC_EPARAM, "too many covariance bands for p_pad");
+  return SKC_OK;
+}
+
+size_t cov_ws(int64_t n, int32_t m, int32_t p_pad) {
+  const int nb = make_bands(p_pad, band_capacity(m), nullptr);
+  const int g = cov_groups(nb, n);
+  return (size_t)g * tri_off(p_pad, p_pad) * sizeof(double);
+}
+
+int cov_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, int32_t p_pad,
+               const double* stats, double* tri, void* ws, cudaStream_t st) {
+  if (n == 0) return SKC_OK;
+  CovParams H;
+  const int cap = band_capacity(m);
+  H.nbands = make_bands(p_pad, cap, H.band_rows);
+  H.groups = cov_groups(H.nbands, n);
+  H.idx = idx;
+  H.val = val;
+  H.n = n;
+  H.m = m;
+  H.p_pad = p_pad;
+  H.stats = stats;
+  H.part = reinterpret_cast<double*>(ws);
+  int maxe = 0;
+  for (int b = 0; b < H.nbands; ++b) {
+    const int e = (int)(tri_off(H.band_rows[b + 1], p_pad) - tri_off(H.band_rows[b], p_pad));
+    if (e > maxe) maxe = e;
+  }
+  const size_t smem = (size_t)maxe * 8 + (size_t)kCovWarps * m * 8;
+  auto k = val_f64 ? cov_band_kernel<double> : cov_band_kernel<float>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k<<<H.nbands * H.groups, kCovWarps * 32, smem, st>>>(H);
+  int rc = check_launch("cov_band_kernel");
+  if (rc) return rc;
+  const int64_t total = tri_off(p_pad, p_pad);
+  cov_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(H.part, H.groups, total, tri);
+  return check_launch("cov_reduce_kernel");
+}
+
+// ======================================================================================
+// K4: estimators.py:62-65 on the packed triangle
+// ======================================================================================
+__global__ void cov_finalize_kernel(const double* __restrict__ tri, int32_t p, double f, double dfac,
+                                    double* __restrict__ C) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)p * p) return;
+  const int a = (int)(e / p), b = (int)(e % p);
+  const int lo = min(a, b), hi = max(a, b);
+  const double c = dmul(tri[tri_off(lo, p) + (hi - lo)], f);
+  C[e] = (a == b) ? dmul(c, dfac) : c;
+}
+
+int cov_finalize_launch(const double* tri, int32_t p_pad, int32_t m, int64_t n_total, double* C, cudaStream_t st) {
+  // (p * (p - 1)) / (m * (m - 1)) / n  and  1.0 - (p - m) / (p - 1), evaluated as Python does
+  const double f = ((double)((int64_t)p_pad * (p_pad - 1)) / (double)((int64_t)m * (m - 1))) / (double)n_total;
+  const double dfac = 1.0 - (double)(p_pad - m) / (double)(p_pad - 1);
+  const int64_t total = (int64_t)p_pad * p_pad;
+  cov_finalize_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(tri, p_pad, f, dfac, C);
+  return check_launch("cov_finalize_kernel");
+}
+
+// ======================================================================================
+// K7: adjoint D^T H^T per row, fp64, reference stage order (transform.py:153-171, 253-261).
+// One CTA per row, the row staged in shared memory. pre_scale != 0 first maps
+// y <- (pre_scale * y) / pre_div (the estimate_mean scaling, estimators.py:44).
+// ======================================================================================
+__global__ void adjoint_kernel(const double* __restrict__ Y, int32_t p_pad, int use_signs, uint64_t sign_state,
+                               int32_t p_out, double pre_scale, double pre_div, double* __restrict__ X) {
+  extern __shared__ double b[];
+  const int64_t row = blockIdx.x;
+  for (int j = threadIdx.x; j < p_pad; j += blockDim.x) {
+    double v = Y[row * p_pad + j];
+    if (pre_scale != 0.0) v = __ddiv_rn(dmul(pre_scale, v), pre_div);
+    b[j] = v;
+  }
+  __syncthreads();
+  for (int h = 1; h < p_pad; h <<= 1) {
+    for (int q = threadIdx.x; q < p_pad / 2; q += blockDim.x) {
+      const int i = (q / h) * 2 * h + (q % h);
+      const double u = b[i], v = b[i + h];
+      b[i] = dadd(u, v);
+      b[i + h] = dsub(u, v);
+    }
+    __syncthreads();
+  }
+  const double c = 1.0 / sqrt((double)p_pad);
+  for (int j = threadIdx.x; j < p_out; j += blockDim.x) {
+    double v = dmul(b[j], c);
+    if (use_signs) {
+      const uint64_t bit = mix64(sign_state + kGamma * (uint64_t)(j + 1)) >> 63;
+      v = dmul(v, 1.0 - 2.0 * (double)bit);
+    }
+    X[row * p_out + j] = v;
+  }
+}
+
+// identity kind: copy with truncation and optional pre-scaling
+__global__ void copy_rows_kernel(const double* __restrict__ Y, int64_t n, int32_t p_pad, int32_t p_out,
+                                 double pre_scale, double pre_div, double* __restrict__ X) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n * p_out) return;
+  const int64_t r = e / p_out;
+  const int j = (int)(e % p_out);
+  double v = Y[r * p_pad + j];
+  if (pre_scale != 0.0) v = __ddiv_rn(dmul(pre_scale, v), pre_div);
+  X[e] = v;
+}
+
+int adjoint_launch(const double* Y, int64_t n, int32_t p_pad, int32_t kind, uint64_t sign_seed, int32_t p_out,
+                   double pre_scale, double pre_div, double* X, cudaStream_t st) {
+  if (n == 0) return SKC_OK;
+  if (kind < 0) {  // plain WHT, no signs
+    const size_t smem = (size_t)p_pad * sizeof(double);
+    cudaFuncSetAttribute(adjoint_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    adjoint_kernel<<<(unsigned)n, 256, smem, st>>>(Y, p_pad, 0, 0, p_out, 0.0, 1.0, X);
+    return check_launch("adjoint_kernel");
+  }
+  if (kind == SKC_KIND_NONE) {
+    const int64_t tot = n * p_out;
+    copy_rows_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(Y, n, p_pad, p_out, pre_scale, pre_div, X);
+    return check_launch("copy_rows_kernel");
+  }
+  const size_t smem = (size_t)p_pad * sizeof(double);
+  cudaFuncSetAttribute(adjoint_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  adjoint_kernel<<<(unsigned)n, 256, smem, st>>>(Y, p_pad, 1, mix64(sign_seed ^ kTagSign), p_out, pre_scale,
+                                                 pre_div, X);
+  return check_launch("adjoint_kernel");
+}
+
+// D diagonal as fp64 (transform.py:132-143)
+__global__ void signs_kernel(uint64_t sign_state, int32_t p_pad, int use_signs, double* out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= p_pad) return;
+  out[j] = use_signs ? 1.0 - 2.0 * (double)(mix64(sign_state + kGamma * (uint64_t)(j + 1)) >> 63) : 1.0;
+}
+
+int signs_launch(uint64_t sign_seed, int32_t p_pad, int32_t kind, double* out, cudaStream_t st) {
+  signs_kernel<<<(p_pad + 255) / 256, 256, 0, st>>>(mix64(sign_seed ^ kTagSign), p_pad, kind == SKC_KIND_HADAMARD,
+                                                   out);
+  return check_launch("signs_kernel");
+}
+
+}  // namespace skc

@@ -1,0 +1,145 @@
+"""Unbiased mean / covariance estimators and PCA on a GPU sketch; estimators.py:1-129.
+
+Device work per estimate:
+  K2 ``skc_moments``         mean accumulation + value statistics
+  K3 ``skc_cov_accumulate``  raw W W^T upper triangle (fixed-point smem bands)
+  K4 ``skc_cov_finalize``    scale, symmetrise, diagonal debias
+  K7 ``skc_mean_finalize`` / ``skc_unprecondition``  adjoint transforms
+The top-k eigensolve is handed back to the host (numpy LAPACK ``eigh``), as the
+north star specifies. Partial sums (acc, stats, triangle) are plain device tensors, so
+a sharded run allreduces them between accumulate and finalize (``dist.py``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ParameterError
+from .sketch import SparseSketch
+from .transform import u64, unprecondition
+
+SYMMETRY_RTOL = 1e-9
+
+
+@dataclass
+class CovarianceEstimate:
+    """Symmetric p_pad x p_pad estimate; estimators.py:21-27. ``matrix`` is host numpy,
+    ``device_matrix`` the same values on the GPU."""
+
+    matrix: np.ndarray
+    n_used: int
+    domain: str = "preconditioned"
+    device_matrix: Optional[torch.Tensor] = field(default=None, repr=False)
+
+
+@dataclass
+class Moments:
+    """Device partial sums of one sketch (or one shard): mean accumulator, stats, triangle."""
+
+    acc: torch.Tensor    # (p_pad,) fp64
+    stats: torch.Tensor  # (3,) fp64: sum v^2, max |v|, rows
+    tri: Optional[torch.Tensor]  # (p_pad (p_pad+1)/2,) fp64 or None
+    n: int
+
+
+def accumulate_moments(sketch: SparseSketch, covariance: bool = True, into: Optional[Moments] = None) -> Moments:
+    """K2 (+ K3) over one sketch; adds into ``into`` when given (chunked / sharded use)."""
+    dev = sketch.indices.device
+    p, m, n = sketch.p, sketch.m, sketch.n
+    if into is None:
+        tri_len = p * (p + 1) // 2
+        into = Moments(
+            acc=torch.zeros(p, dtype=torch.float64, device=dev),
+            stats=torch.zeros(3, dtype=torch.float64, device=dev),
+            tri=torch.zeros(tri_len, dtype=torch.float64, device=dev) if covariance else None,
+            n=0,
+        )
+    L = _lib.lib()
+    st = _lib.stream_ptr(dev)
+    vcode = _lib.dtype_code(sketch.values)
+    idx, val = sketch.indices.contiguous(), sketch.values.contiguous()
+    with torch.cuda.device(dev):
+        ws = _lib.workspace(L.skc_moments_workspace(n, m, p), dev)
+        _lib.call("skc_moments", idx.data_ptr(), val.data_ptr(), vcode, n, m, p, into.acc.data_ptr(),
+                  into.stats.data_ptr(), ws.data_ptr(), ws.numel(), st)
+        if covariance:
+            ws2 = _lib.workspace(L.skc_cov_workspace(n, m, p), dev)
+            _lib.call("skc_cov_accumulate", idx.data_ptr(), val.data_ptr(), vcode, n, m, p, into.stats.data_ptr(),
+                      into.tri.data_ptr(), ws2.data_ptr(), ws2.numel(), st)
+    into.n += n
+    return into
+
+
+def mean_from_moments(mom: Moments, spec, m: int, n_total: int) -> torch.Tensor:
+    out = torch.empty(spec.p, dtype=torch.float64, device=mom.acc.device)
+    with torch.cuda.device(out.device):
+        _lib.call("skc_mean_finalize", mom.acc.data_ptr(), spec.p, spec.p_pad, m, int(n_total), spec.gpu_kind(),
+                  u64(spec.sign_seed), out.data_ptr(), _lib.stream_ptr(out.device))
+    return out
+
+
+def covariance_from_moments(mom: Moments, p_pad: int, m: int, n_total: int) -> torch.Tensor:
+    C = torch.empty((p_pad, p_pad), dtype=torch.float64, device=mom.tri.device)
+    with torch.cuda.device(C.device):
+        _lib.call("skc_cov_finalize", mom.tri.data_ptr(), p_pad, m, int(n_total), C.data_ptr(),
+                  _lib.stream_ptr(C.device))
+    return C
+
+
+def estimate_mean(sketch: SparseSketch) -> np.ndarray:
+    """(p/m)(1/n) sum of sketch columns, adjoint, truncate; estimators.py:30-45"""
+    if sketch.n < 1:
+        raise ParameterError("empty sketch")
+    mom = accumulate_moments(sketch, covariance=False)
+    return mean_from_moments(mom, sketch.spec, sketch.m, sketch.n).cpu().numpy()
+
+
+def estimate_covariance(sketch: SparseSketch) -> CovarianceEstimate:
+    """Unbiased covariance of the preconditioned data; estimators.py:48-66"""
+    if sketch.m < 2:
+        raise ParameterError("covariance estimation needs m >= 2")
+    if sketch.n < 1:
+        raise ParameterError("empty sketch")
+    mom = accumulate_moments(sketch, covariance=True)
+    C = covariance_from_moments(mom, sketch.p, sketch.m, sketch.n)
+    return CovarianceEstimate(matrix=C.cpu().numpy(), n_used=sketch.n, device_matrix=C)
+
+
+def top_eigenvectors(C, k: int) -> np.ndarray:
+    """Host eigensolve (north star: the top-k eigensolve stays on the host); estimators.py:69-81"""
+    C = C.cpu().numpy() if isinstance(C, torch.Tensor) else np.asarray(C, dtype=np.float64)
+    if C.ndim != 2 or C.shape[0] != C.shape[1]:
+        raise ParameterError("expected a square matrix")
+    p = C.shape[0]
+    if not 1 <= k <= p:
+        raise ParameterError(f"need 1 <= k <= {p}, got {k}")
+    scale = max(float(np.abs(C).max()), 1e-300)
+    if np.abs(C - C.T).max() > SYMMETRY_RTOL * scale:
+        raise ParameterError("matrix is not symmetric within tolerance")
+    w, V = np.linalg.eigh(0.5 * (C + C.T))
+    return V[:, ::-1][:, :k]
+
+
+def principal_components(sketch: SparseSketch, k: int) -> np.ndarray:
+    """Top-k PCs mapped back to the original domain; estimators.py:116-129"""
+    est = estimate_covariance(sketch)
+    V = top_eigenvectors(est.matrix, k)
+    spec = sketch.spec
+    Vd = torch.as_tensor(np.ascontiguousarray(V.T), device=sketch.indices.device)
+    U = torch.empty((k, spec.p), dtype=torch.float64, device=Vd.device)
+    with torch.cuda.device(Vd.device):
+        _lib.call("skc_unprecondition", Vd.data_ptr(), k, spec.p_pad, spec.gpu_kind(), u64(spec.sign_seed), spec.p,
+                  U.data_ptr(), _lib.stream_ptr(Vd.device))
+    return U.T.contiguous().cpu().numpy()
+
+
+__all__ = [
+    "CovarianceEstimate", "Moments", "SYMMETRY_RTOL", "accumulate_moments", "covariance_from_moments",
+    "estimate_covariance", "estimate_mean", "mean_from_moments", "principal_components", "top_eigenvectors",
+    "unprecondition",
+]
