@@ -153,7 +153,7 @@ class ClockSampler:
         busy = [r for r in rows if r[7].strip().isdigit() and int(r[7]) > 0] or rows
         sm = [float(r[0]) for r in busy if r[0].strip().replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in busy for i in range(4) if "Active" in r[3 + i]})
+        reasons = sorted({names[i] for r in busy for i in range(4) if r[3 + i].strip() == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": float(rows[0][1]) if rows[0][1].strip().replace(".", "").isdigit() else None,
                 "reasons": reasons, "samples": len(busy)}

@@ -123,26 +123,24 @@ int moments_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, 
 
 // ======================================================================================
 // K3: raw W W^T upper triangle (estimators.py:59-61), in row bands that fit shared memory.
-// CTA (band b, group g) holds band b as 64-bit fixed point split into two int32 words.
-// Each product w_a*w_b is scaled by 2^S (|q| <= 2^30 for |w| <= tau) and added to `lo`
-// with a native ATOMS.ADD; the returned old value gives the carry, and the rare nonzero
-// carry/borrow goes into `hi` with a second ATOMS.ADD. The sum is exact and independent
-// of order, so the result is deterministic. tau = 8 * rms(values) from K2's statistics.
-// A row that holds a value above tau is queued and added in fp64, in ascending row
-// order, at the end of its window. At the end each CTA writes its band to a private fp64
-// partial, and a reduce kernel sums the groups in fixed order. Error vs exact fp64:
-// ~6e-8 of tau^2 per product (quantum + fp32 product), random, so ~1e-7 relative.
+// CTA (band b, group g) with 32 warps holds band b as an int32 "low word" per entry. Each
+// product w_a*w_b is scaled by 2^S (|q| <= 2^30 for |w| <= tau) and added with a native
+// ATOMS.ADD whose returned old value yields the carry. A nonzero carry/borrow (~1 in 2^8
+// adds) goes to the group's int64 partial in global memory with a native REDG.ADD.64.
+// A row holding a value above tau sends its products (fp64, then scaled to int64)
+// straight to that REDG path. Every sum is integer, so the result is exact in the fixed
+// point and independent of order (deterministic). At the end the CTA adds its low words
+// into the same int64 partial. A reduce kernel sums the groups in int64 and scales to fp64.
+// tau = 8 * rms(values), from K2's statistics. Quantum 2^-S ~ 6e-8 * tau^2.
 // ======================================================================================
-constexpr int kSmemBudget = 220 * 1024;  // dynamic smem per CTA: band + row staging
-constexpr int kWindow = 4096;            // rows between outlier-queue drains
-constexpr int kQueue = 512;              // outlier rows per window
-constexpr int kCovWarps = 8;
+constexpr int kSmemBudget = 220 * 1024;  // dynamic smem per CTA
+constexpr int kCovWarps = 32;
 constexpr int kMaxBands = 511;
 
 __host__ __device__ inline int64_t tri_off(int64_t a, int64_t p) { return a * p - a * (a - 1) / 2; }
 
-static int band_capacity(int32_t m) {
-  return (kSmemBudget - kCovWarps * m * 8) / 8;  // (lo, hi) entries left after row staging
+static int band_capacity(int32_t m, int32_t p_pad) {
+  return (kSmemBudget - kCovWarps * m * 8 - 4 * p_pad) / 4;  // int32 entries after staging + row table
 }
 // greedy row bands of <= cap entries; returns the count, fills out[0..count] if given
 static int make_bands(int32_t p_pad, int cap, int* out) {
@@ -169,32 +167,38 @@ struct CovParams {
   int64_t n;
   int32_t m, p_pad;
   const double* stats;
-  double* part;  // [groups][tri_total] fp64 partials, each CTA owns its band slice
+  unsigned long long* part;  // [groups][tri_total] int64 fixed-point partials
   int nbands, groups;
   int band_rows[kMaxBands + 1];
 };
 
 template <typename V>
-__device__ __forceinline__ float ldv32(const void* p, int64_t i) {
-  return (float)__ldg(reinterpret_cast<const V*>(p) + i);
-}
-template <typename V>
 __device__ __forceinline__ double ldv64(const void* p, int64_t i) {
   return (double)__ldg(reinterpret_cast<const V*>(p) + i);
 }
 
-__device__ __forceinline__ void fx_add(uint32_t* lo, int* hi, int e, int q) {
-  const uint32_t uq = (uint32_t)q;
-  const uint32_t old = atomicAdd(lo + e, uq);
-  const int delta = (int)(old + uq < old) - (int)(q < 0);
-  if (delta != 0) atomicAdd(hi + e, delta);
+// predicated 64-bit global reduction without a branch (the carry path is rare)
+__device__ __forceinline__ void red_if(bool p, unsigned long long* addr, unsigned long long v) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q red.global.add.u64 [%1], %2;\n\t}" ::"r"((unsigned)p),
+      "l"(addr), "l"(v)
+      : "memory");
+}
+
+// S from the value statistics; identical in every CTA and in the reduce kernel
+__device__ __forceinline__ int cov_scale(const double* stats, int m, double* tau_out) {
+  const double cnt = stats[2] * (double)m;
+  const double rms = cnt > 0 ? sqrt(stats[0] / cnt) : 0.0;
+  double tau = 8.0 * rms;
+  if (!(tau > 0.0)) tau = 1.0;
+  *tau_out = tau;
+  int S = (int)floor(log2(1073741824.0 / (tau * tau)));
+  return S & ~1;  // even, so each factor carries 2^(S/2)
 }
 
 template <typename V>
-__global__ void __launch_bounds__(kCovWarps * 32) cov_band_kernel(const __grid_constant__ CovParams P) {
+__global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __grid_constant__ CovParams P) {
   extern __shared__ int smem_i[];
-  __shared__ int qcount;
-  __shared__ int64_t queue[kQueue];
   const int m = P.m;
   const int band = blockIdx.x % P.nbands, group = blockIdx.x / P.nbands;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -202,157 +206,110 @@ __global__ void __launch_bounds__(kCovWarps * 32) cov_band_kernel(const __grid_c
   const int64_t e0 = tri_off(r0, P.p_pad), e1 = tri_off(r1, P.p_pad);
   const int ne = (int)(e1 - e0);
   uint32_t* lo = reinterpret_cast<uint32_t*>(smem_i);
-  int* hi = smem_i + ne;
-  float* sval = reinterpret_cast<float*>(smem_i + 2 * ne) + (size_t)warp * m;
-  int* sidx = smem_i + 2 * ne + (size_t)kCovWarps * m + (size_t)warp * m;
-  double* part = P.part + (size_t)group * tri_off(P.p_pad, P.p_pad) + e0;
+  int* rowbase = smem_i + ne;                 // [r1 - r0]: entry (a, b) sits at rowbase[a - r0] + b
+  float* sval = reinterpret_cast<float*>(rowbase + (r1 - r0)) + (size_t)warp * m;
+  int* sidx = rowbase + (r1 - r0) + (size_t)kCovWarps * m + (size_t)warp * m;
+  unsigned long long* part = P.part + (size_t)group * tri_off(P.p_pad, P.p_pad) + e0;
 
-  // scale: |w| <= tau -> |q| <= 2^30
-  const double cnt = P.stats[2] * (double)m;
-  const double rms = cnt > 0 ? sqrt(P.stats[0] / cnt) : 0.0;
-  double tau = 8.0 * rms;
-  if (!(tau > 0.0)) tau = 1.0;
-  int S = (int)floor(log2(1073741824.0 / (tau * tau)));
-  S &= ~1;  // even, so each factor carries 2^(S/2)
+  double tau;
+  const int S = cov_scale(P.stats, m, &tau);
   const float half = (float)ldexp(1.0, S / 2);
-  const double inv = ldexp(1.0, -S);
+  const double full = ldexp(1.0, S);
   const float ftau = (float)tau;
 
-  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
-    lo[e] = 0u;
-    hi[e] = 0;
-    part[e] = 0.0;
-  }
-  if (threadIdx.x == 0) qcount = 0;
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) lo[e] = 0u;
+  for (int a = r0 + threadIdx.x; a < r1; a += blockDim.x) rowbase[a - r0] = (int)(tri_off(a, P.p_pad) - e0) - a;
   __syncthreads();
 
   const int64_t g0 = P.n * group / P.groups, g1 = P.n * (group + 1) / P.groups;
-  for (int64_t w0 = g0; w0 < g1; w0 += kWindow) {
-    const int64_t w1 = min(w0 + (int64_t)kWindow, g1);
-    for (int64_t r = w0 + warp; r < w1; r += kCovWarps) {
-      bool big = false;
-      int nlo = 0, nhi = 0;  // # indices < r0 and < r1 (rows are sorted)
-      for (int t = lane; t < m; t += 32) {
-        const int j = __ldg(P.idx + r * m + t);
-        const float v = ldv32<V>(P.val, r * m + t);
+  for (int64_t r = g0 + warp; r < g1; r += kCovWarps) {
+    bool big = false;
+    int nlo = 0, nhi = 0;  // # indices < r0 and < r1 (rows are sorted)
+    for (int t0 = 0; t0 < m; t0 += 32) {
+      const int t = t0 + lane;
+      int j = 0x7FFFFFFF;
+      if (t < m) {
+        j = __ldg(P.idx + r * m + t);
+        const float v = (float)__ldg(reinterpret_cast<const V*>(P.val) + r * m + t);
         sidx[t] = j;
         sval[t] = v * half;
         big |= fabsf(v) > ftau;
-        nlo += j < r0;
-        nhi += j < r1;
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        nlo += __shfl_xor_sync(kFullMask, nlo, o);
-        nhi += __shfl_xor_sync(kFullMask, nhi, o);
-      }
-      big = __any_sync(kFullMask, big);
-      __syncwarp();
-      if (nlo == nhi) continue;  // none of this row's indices fall in the band
-      if (big) {
-        int q = 0;
-        if (lane == 0) q = atomicAdd(&qcount, 1);
-        q = __shfl_sync(kFullMask, q, 0);
-        if (q < kQueue) {
-          if (lane == 0) queue[q] = r;
-        } else {
-          // queue full (pathological scale): add in fp64 right away (order not fixed)
-          for (int t = nlo; t < nhi; ++t) {
-            const int a = sidx[t];
-            const double va = ldv64<V>(P.val, r * m + t);
-            const int64_t base = tri_off(a, P.p_pad) - e0 - a;
-            for (int u = t + lane; u < m; u += 32)
-              atomicAdd(&part[base + sidx[u]], dmul(va, ldv64<V>(P.val, r * m + u)));
-          }
-        }
-        __syncwarp();
-        continue;
-      }
+      nlo += __popc(__ballot_sync(kFullMask, j < r0));
+      nhi += __popc(__ballot_sync(kFullMask, j < r1));
+    }
+    if (nlo == nhi) continue;  // none of this row's indices fall in the band
+    big = __any_sync(kFullMask, big);
+    __syncwarp();
+    if (!big) {
       for (int t = nlo; t < nhi; ++t) {
-        const int a = sidx[t];
         const float va = sval[t];
-        const int base = (int)(tri_off(a, P.p_pad) - e0) - a;
-        for (int u = t + lane; u < m; u += 32) fx_add(lo, hi, base + sidx[u], __float2int_rn(va * sval[u]));
-      }
-      __syncwarp();
-    }
-    __syncthreads();
-    // queued rows with a value above tau: fp64 products, ascending row order, warp 0
-    const int nq = min(qcount, kQueue);
-    if (warp == 0 && nq > 0) {
-      if (lane == 0) {
-        for (int i = 1; i < nq; ++i) {
-          const int64_t x = queue[i];
-          int k = i - 1;
-          while (k >= 0 && queue[k] > x) {
-            queue[k + 1] = queue[k];
-            --k;
-          }
-          queue[k + 1] = x;
+        const int base = rowbase[sidx[t] - r0];
+        for (int u = t + lane; u < m; u += 32) {
+          const int q = __float2int_rn(va * sval[u]);
+          const int e = base + sidx[u];
+          const uint32_t old = atomicAdd(lo + e, (uint32_t)q);
+          const int delta = (int)(old + (uint32_t)q < old) - (int)(q < 0);
+          red_if(delta != 0, part + e, (unsigned long long)((long long)delta << 32));
         }
       }
-      __syncwarp();
-      for (int qi = 0; qi < nq; ++qi) {
-        const int64_t r = queue[qi];
-        for (int t = 0; t < m; ++t) {
-          const int a = __ldg(P.idx + r * m + t);
-          if (a < r0 || a >= r1) continue;
-          const double va = ldv64<V>(P.val, r * m + t);
-          const int64_t base = tri_off(a, P.p_pad) - e0 - a;
-          for (int u = t + lane; u < m; u += 32) {
-            const int b = __ldg(P.idx + r * m + u);
-            part[base + b] = dadd(part[base + b], dmul(va, ldv64<V>(P.val, r * m + u)));
-          }
-          __syncwarp();
+    } else {
+      // a value above tau: exact fp64 product, scaled, straight to the int64 partial
+      for (int t = nlo; t < nhi; ++t) {
+        const double va = ldv64<V>(P.val, r * m + t);
+        const int base = rowbase[sidx[t] - r0];
+        for (int u = t + lane; u < m; u += 32) {
+          const long long q = __double2ll_rn(dmul(dmul(va, ldv64<V>(P.val, r * m + u)), full));
+          atomicAdd(part + base + sidx[u], (unsigned long long)q);
         }
       }
     }
-    __syncthreads();
-    if (threadIdx.x == 0) qcount = 0;
-    __syncthreads();
+    __syncwarp();
   }
-  // fixed-point total -> fp64 partial
+  __syncthreads();
   for (int e = threadIdx.x; e < ne; e += blockDim.x) {
-    const int64_t q = ((int64_t)hi[e] << 32) + (int64_t)lo[e];
-    if (q != 0) part[e] = dadd(part[e], (double)q * inv);
+    const uint32_t q = lo[e];
+    if (q != 0u) atomicAdd(part + e, (unsigned long long)q);
   }
 }
 
-__global__ void cov_reduce_kernel(const double* __restrict__ part, int groups, int64_t total,
-                                  double* __restrict__ tri) {
+__global__ void cov_reduce_kernel(const unsigned long long* __restrict__ part, int groups, int64_t total, int m,
+                                  const double* __restrict__ stats, double* __restrict__ tri) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= total) return;
-  double s = 0.0;
-  for (int g = 0; g < groups; ++g) s = dadd(s, part[(size_t)g * total + e]);
-  tri[e] = dadd(tri[e], s);
+  double tau;
+  const int S = cov_scale(stats, m, &tau);
+  long long s = 0;
+  for (int g = 0; g < groups; ++g) s += (long long)part[(size_t)g * total + e];
+  tri[e] = dadd(tri[e], (double)s * ldexp(1.0, -S));
 }
 
 static int cov_groups(int nbands, int64_t n) {
   int g = sm_count() / nbands;
   if (g < 1) g = 1;
-  const int64_t maxg = (n + 1023) / 1024;
+  const int64_t maxg = (n + 4095) / 4096;
   if (g > maxg) g = (int)(maxg < 1 ? 1 : maxg);
   return g;
 }
 
 int cov_check(int32_t p_pad, int32_t m) {
-  if (band_capacity(m) < p_pad) return fail(SKC_EPARAM, "m too large for the shared-memory covariance bands");
-  if (make_bands(p_pad, band_capacity(m), nullptr) > kMaxBands)
+  if (band_capacity(m, p_pad) < p_pad) return fail(SKC_EPARAM, "m too large for the shared-memory covariance bands");
+  if (make_bands(p_pad, band_capacity(m, p_pad), nullptr) > kMaxBands)
     return fail(SKC_EPARAM, "too many covariance bands for p_pad");
   return SKC_OK;
 }
 
 size_t cov_ws(int64_t n, int32_t m, int32_t p_pad) {
-  const int nb = make_bands(p_pad, band_capacity(m), nullptr);
+  const int nb = make_bands(p_pad, band_capacity(m, p_pad), nullptr);
   const int g = cov_groups(nb, n);
-  return (size_t)g * tri_off(p_pad, p_pad) * sizeof(double);
+  return (size_t)g * tri_off(p_pad, p_pad) * sizeof(unsigned long long);
 }
 
 int cov_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, int32_t p_pad,
                const double* stats, double* tri, void* ws, cudaStream_t st) {
   if (n == 0) return SKC_OK;
   CovParams H;
-  const int cap = band_capacity(m);
+  const int cap = band_capacity(m, p_pad);
   H.nbands = make_bands(p_pad, cap, H.band_rows);
   H.groups = cov_groups(H.nbands, n);
   H.idx = idx;
@@ -361,20 +318,22 @@ int cov_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int3
   H.m = m;
   H.p_pad = p_pad;
   H.stats = stats;
-  H.part = reinterpret_cast<double*>(ws);
-  int maxe = 0;
+  H.part = reinterpret_cast<unsigned long long*>(ws);
+  const int64_t total = tri_off(p_pad, p_pad);
+  cudaMemsetAsync(ws, 0, (size_t)H.groups * total * 8, st);
+  int maxe = 0, maxr = 0;
   for (int b = 0; b < H.nbands; ++b) {
     const int e = (int)(tri_off(H.band_rows[b + 1], p_pad) - tri_off(H.band_rows[b], p_pad));
     if (e > maxe) maxe = e;
+    if (H.band_rows[b + 1] - H.band_rows[b] > maxr) maxr = H.band_rows[b + 1] - H.band_rows[b];
   }
-  const size_t smem = (size_t)maxe * 8 + (size_t)kCovWarps * m * 8;
+  const size_t smem = (size_t)maxe * 4 + (size_t)maxr * 4 + (size_t)kCovWarps * m * 8;
   auto k = val_f64 ? cov_band_kernel<double> : cov_band_kernel<float>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<H.nbands * H.groups, kCovWarps * 32, smem, st>>>(H);
   int rc = check_launch("cov_band_kernel");
   if (rc) return rc;
-  const int64_t total = tri_off(p_pad, p_pad);
-  cov_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(H.part, H.groups, total, tri);
+  cov_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(H.part, H.groups, total, m, stats, tri);
   return check_launch("cov_reduce_kernel");
 }
 

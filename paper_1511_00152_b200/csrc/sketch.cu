@@ -1,17 +1,21 @@
 // K1: fused single-pass precondition + sparsify (sketch.py:196-223) for sm_100a.
 //
-// One CTA (8 warps) streams tiles of S = 8192 / p_pad samples:
-//   phase 1  coalesced vector loads of the tile -> XOR-swizzled shared memory (zero pad)
-//   phase 2  signs + normalised WHT. Each thread owns E = 32 elements of one sample
-//            (L = p_pad/32 threads per sample). Butterfly stages run in registers
-//            inside a 5-bit "window" of the element index. Windows are changed by a
-//            conflict-free transpose through the swizzled tile. Stages run in the
-//            reference order h = 1, 2, 4, ... (transform.py:162-169), so the fp64
-//            instantiation is bit-exact.
-//   phase 3  one warp per sample: splitmix64 keys of all p_pad coordinates, a
-//            threshold prefilter into a per-warp candidate list, then an exact bucket
-//            select of the m smallest keys (sketch.py:53-56). Kept (index, value) pairs
-//            are written in ascending index order with coalesced stores.
+// A CTA (8 warps) streams tiles of S = 8192 / P samples (P = 2^LOGP = p_pad):
+//   phase 1  coalesced 16-byte loads of the tile into a padded shared-memory layout:
+//            element i of sample s sits at word  s*SP + (i>>5)*33 + (i&31),  SP=(P/32)*33.
+//            That address is linear over disjoint index bits, so every register of a
+//            window below is "thread base + immediate". The 33-word rows make every
+//            window conflict-free, including windows whose lanes span several samples.
+//   phase 2  signs + normalised WHT. A thread owns E = 32 elements of one sample (a
+//            5-bit "window" of the index bits); butterfly stages run in registers;
+//            windows change through the tile. Stages run in the reference order
+//            h = 1, 2, 4, ... (transform.py:162-169), so the fp64 instantiation is
+//            bit-exact.
+//   phase 3  one warp per sample. Pass 1 hashes all keys of the plan (splitmix64,
+//            _hash.py:46-56) and keeps the high word only for a threshold test, as a
+//            per-lane bitmask. Pass 2 re-hashes the ~m+5sqrt(m) candidates in full into
+//            a per-warp list. An exact bucket select finds the m smallest keys
+//            (sketch.py:53-56), and a row-ballot loop emits them in ascending index order.
 #include <math.h>
 
 #include "common.cuh"
@@ -31,7 +35,7 @@ struct SketchParams {
   int32_t p, m;
   int32_t pk;          // key range of the sampling plan (plan.p; = p_pad except kind none)
   int32_t x_f64;       // input dtype
-  int32_t vec;         // 1: rows allow aligned vector loads
+  int32_t vec;         // 1: rows allow aligned 16-byte loads
   uint64_t sign_state; // mix64(sign_seed ^ TAG_SIGN), used when use_signs
   int32_t use_signs;
   uint64_t s_tag;      // mix64(master ^ TAG_SAMPLE)
@@ -40,7 +44,8 @@ struct SketchParams {
   void* val_out;
   int32_t val_f64;
   double* y_out;       // optional full transformed rows (n, p_pad) fp64
-  uint32_t t_lim;      // candidate iff (key >> 32) <= t_lim
+  uint32_t t_hi;       // candidate iff (key >> 32) < t_hi  (t_all: every key)
+  int32_t t_all;
   int32_t cap;         // per-warp candidate capacity (multiple of 32)
   int32_t mode;        // SampleMode
   int64_t num_tiles;
@@ -54,38 +59,36 @@ struct Geo {
   static constexpr int L = P / E;  // threads per sample
   static constexpr int S = kTileElems / P;
   static constexpr int NWIN = LOGE == 0 ? 1 : (LOGP + LOGE - 1) / LOGE;
-  static constexpr int ITEMS = S * L;  // (sample, thread) work items per tile
-  // conflict-free XOR swizzle inside each 32-element block ("K1 layout")
-  static __device__ __forceinline__ int phys(int s, int i) {
-    if constexpr (LOGP < 5) {
-      return s * P + i;
-    } else {
-      return s * P + (i ^ (((i >> 5) ^ (s * L)) & 31));
-    }
-  }
-  static __device__ __forceinline__ int elem(int k, int u, int e) {
-    const int bk = (k * LOGE < LOGP - LOGE) ? k * LOGE : LOGP - LOGE;
-    const int low = (1 << bk) - 1;
-    return (u & low) | (e << bk) | ((u >> bk) << (bk + LOGE));
+  static constexpr int ITEMS = S * L;
+  static constexpr int SP = LOGP < 5 ? P : (P / 32) * 33;  // words per sample
+  static constexpr int WORDS = S * SP;
+  // padded address of element i (linear over disjoint bit sets of i)
+  static __host__ __device__ constexpr int addr(int i) { return LOGP < 5 ? i : i + (i >> 5); }
+  static __host__ __device__ constexpr int bk(int k) { return (k * LOGE < LOGP - LOGE) ? k * LOGE : LOGP - LOGE; }
+  // the thread bits of window k: u fills every index bit outside [bk, bk+LOGE)
+  static __device__ __forceinline__ int u_part(int k, int u) {
+    const int b = bk(k);
+    return (u & ((1 << b) - 1)) | ((u >> b) << (b + LOGE));
   }
 };
 
 // ------------------------------------------------------------------------------------
-// phase 2: WHT of one window for one (sample, thread) item
+// phase 2: one window of the WHT for one (sample, thread) item
 template <int LOGP, typename T, int K>
 __device__ __forceinline__ void wht_window(T* xs, const uint32_t* sgn, int s, int u, T scale) {
   using G = Geo<LOGP>;
   using A = Arith<T>;
-  constexpr int bk = (K * G::LOGE < LOGP - G::LOGE) ? K * G::LOGE : LOGP - G::LOGE;
+  constexpr int bk = G::bk(K);
   constexpr int first = K * G::LOGE;  // first stage bit not yet applied
+  T* base = xs + s * G::SP + G::addr(G::u_part(K, u));
   T v[G::E];
 #pragma unroll
-  for (int e = 0; e < G::E; ++e) v[e] = xs[G::phys(s, G::elem(K, u, e))];
+  for (int e = 0; e < G::E; ++e) v[e] = base[G::addr(e << bk)];
   if constexpr (K == 0) {
     if (sgn != nullptr) {
       // window 0 holds elements [u*E, u*E + E): E consecutive bits of the sign mask
-      const int base = u * G::E;
-      const uint32_t bits = sgn[base >> 5] >> (base & 31);
+      const int b0 = u * G::E;
+      const uint32_t bits = sgn[b0 >> 5] >> (b0 & 31);
 #pragma unroll
       for (int e = 0; e < G::E; ++e) v[e] = A::flip(v[e], (bits >> e) & 1u);
     }
@@ -107,17 +110,14 @@ __device__ __forceinline__ void wht_window(T* xs, const uint32_t* sgn, int s, in
     for (int e = 0; e < G::E; ++e) v[e] = A::mul(v[e], scale);
   }
 #pragma unroll
-  for (int e = 0; e < G::E; ++e) xs[G::phys(s, G::elem(K, u, e))] = v[e];
+  for (int e = 0; e < G::E; ++e) base[G::addr(e << bk)] = v[e];
 }
 
 template <int LOGP, typename T, int K>
 __device__ __forceinline__ void wht_all_windows(T* xs, const uint32_t* sgn, T scale) {
   using G = Geo<LOGP>;
   if constexpr (K < G::NWIN) {
-    for (int it = threadIdx.x; it < G::ITEMS; it += kThreads) {
-      const int s = it / G::L, u = it % G::L;
-      wht_window<LOGP, T, K>(xs, sgn, s, u, scale);
-    }
+    for (int it = threadIdx.x; it < G::ITEMS; it += kThreads) wht_window<LOGP, T, K>(xs, sgn, it / G::L, it % G::L, scale);
     __syncthreads();
     wht_all_windows<LOGP, T, K + 1>(xs, sgn, scale);
   }
@@ -125,8 +125,30 @@ __device__ __forceinline__ void wht_all_windows(T* xs, const uint32_t* sgn, T sc
 
 // ------------------------------------------------------------------------------------
 // phase 3 helpers
-__device__ __forceinline__ uint64_t key_of(uint64_t ci, int j) {
-  return mix64(ci + kGamma * (uint64_t)(j + 1));
+__device__ __forceinline__ uint64_t key_of(uint64_t ci, int j) { return mix64(ci + kGamma * (uint64_t)(j + 1)); }
+
+// High 32 bits of mix64(z) before its last xor-shift: for t <= 2^31,
+// (key >> 32) < t  <=>  hi32(z2) < t, because the last step only flips bit 0 of the high
+// word when bit 63 is set. Skips the low word of the final product and shift.
+__device__ __forceinline__ uint32_t mix64_hi_pre(uint64_t z) {
+  z = (z ^ (z >> 30)) * kMix1;
+  z = z ^ (z >> 27);
+  return (uint32_t)((z * kMix2) >> 32);
+}
+
+// 32x32 bit-matrix transpose across a warp: lane i holds row i (bit r = M[i][r]); returns
+// column `lane` (bit i = M[i][lane]). Recursive block swap, 5 shuffle stages.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int sh = 16 >> k;
+    const uint32_t m = masks[k];
+    const uint32_t y = __shfl_xor_sync(kFull, x, sh);
+    x = (lane & sh) ? ((x & ~m) | ((y & ~m) >> sh)) : ((x & m) | ((y & m) << sh));
+  }
+  return x;
 }
 
 template <typename T>
@@ -135,19 +157,23 @@ __device__ __forceinline__ void store_val(void* out, int64_t pos, T v, int val_f
   else reinterpret_cast<float*>(out)[pos] = (float)v;
 }
 
-// Exact fallback: binary search the m-th smallest key by re-hashing (64 passes). Used
-// only when the prefilter misses (probability ~1e-7 per sample) or cap would overflow.
+template <int LOGP, typename T>
+__device__ __forceinline__ T y_at(const T* xs, int s, int j) {
+  using G = Geo<LOGP>;
+  return xs[s * G::SP + G::addr(j)];
+}
+
+// Exact fallback: binary search of the m-th smallest key by re-hashing (64 passes). Used
+// only when the prefilter misses (~1e-7 per sample) or a bucket overflows.
 template <int LOGP, typename T>
 __device__ void emit_slow_exact(const SketchParams& P, const T* xs, int s, int64_t row, uint64_t ci) {
-  using G = Geo<LOGP>;
   const int lane = threadIdx.x & 31;
   uint64_t lo = 0, hi = ~0ull;
   while (lo < hi) {
     const uint64_t mid = lo + ((hi - lo) >> 1);
     int c = 0;
     for (int j = lane; j < P.pk; j += 32) c += key_of(ci, j) <= mid;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+    c = __reduce_add_sync(kFull, c);
     if (c >= P.m) hi = mid;
     else lo = mid + 1;
   }
@@ -159,7 +185,7 @@ __device__ void emit_slow_exact(const SketchParams& P, const T* xs, int s, int64
     if (keep) {
       const int64_t pos = row * P.m + base + __popc(bal & lanemask_lt());
       P.idx_out[pos] = j;
-      if (P.val_out) store_val<T>(P.val_out, pos, xs[G::phys(s, j)], P.val_f64);
+      if (P.val_out) store_val<T>(P.val_out, pos, y_at<LOGP, T>(xs, s, j), P.val_f64);
     }
     base += __popc(bal);
   }
@@ -168,13 +194,12 @@ __device__ void emit_slow_exact(const SketchParams& P, const T* xs, int s, int64
 template <int LOGP, typename T>
 __device__ void sample_one(const SketchParams& P, const T* xs, int s, int64_t row, uint64_t* ck, uint16_t* cj,
                            uint64_t* memk, int* hist) {
-  using G = Geo<LOGP>;
   const int lane = threadIdx.x & 31;
   if (P.mode == kFullSet) {  // m == p: SamplingPlan shortcut, sketch.py:51-52
     for (int j = lane; j < P.pk; j += 32) {
       const int64_t pos = row * P.m + j;
       P.idx_out[pos] = j;
-      if (P.val_out) store_val<T>(P.val_out, pos, xs[G::phys(s, j)], P.val_f64);
+      if (P.val_out) store_val<T>(P.val_out, pos, y_at<LOGP, T>(xs, s, j), P.val_f64);
     }
     return;
   }
@@ -183,42 +208,76 @@ __device__ void sample_one(const SketchParams& P, const T* xs, int s, int64_t ro
     emit_slow_exact<LOGP, T>(P, xs, s, row, ci);
     return;
   }
-  // 1. prefilter: candidates in ascending j order
-  int count = 0;
-  uint64_t kin = ci + kGamma * (uint64_t)(lane + 1);
-#pragma unroll 4
-  for (int j0 = 0; j0 < P.pk; j0 += 32) {
-    const int j = j0 + lane;
-    const uint64_t key = mix64(kin);
-    kin += 32ull * kGamma;
-    const bool cand = (j < P.pk) && ((uint32_t)(key >> 32) <= P.t_lim);
-    const uint32_t bal = __ballot_sync(kFull, cand);
-    if (cand) {
-      const int pos = count + __popc(bal & lanemask_lt());
-      if (pos < P.cap) {
-        ck[pos] = key;
-        cj[pos] = (uint16_t)j;
+  constexpr int MW = (Geo<LOGP>::P + 1023) / 1024;  // mask words: bit r of word w <-> j = 32 (32 w + r) + lane
+  const int rows = (P.pk + 31) >> 5;                   // key rows: j = 32 r + lane
+  // pass 1: threshold bitmask
+  uint32_t cm[MW];
+#pragma unroll
+  for (int w = 0; w < MW; ++w) cm[w] = 0;
+  if (P.t_all) {
+#pragma unroll
+    for (int w = 0; w < MW; ++w)
+      for (int r = 0; r < 32; ++r) cm[w] |= (uint32_t)(32 * (32 * w + r) + lane < P.pk) << r;
+  } else {
+    uint64_t kin = ci + kGamma * (uint64_t)(lane + 1);
+    const uint64_t step = 32ull * kGamma;
+    if (P.pk == Geo<LOGP>::P && Geo<LOGP>::P >= 32) {
+#pragma unroll
+      for (int w = 0; w < MW; ++w) {
+#pragma unroll
+        for (int r = 0; r < (Geo<LOGP>::P >= 1024 ? 32 : Geo<LOGP>::P / 32); ++r) {
+          const uint32_t h = mix64_hi_pre(kin);
+          kin += step;
+          if (h < P.t_hi) cm[w] |= 1u << r;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int w = 0; w < MW; ++w) {
+        const int rw = min(32, rows - 32 * w);
+#pragma unroll 8
+        for (int r = 0; r < rw; ++r) {
+          const uint32_t h = mix64_hi_pre(kin);
+          kin += step;
+          cm[w] |= (uint32_t)(h < P.t_hi && 32 * (32 * w + r) + lane < P.pk) << r;
+        }
       }
     }
-    count += __popc(bal);
   }
+  int mine = 0;
+#pragma unroll
+  for (int w = 0; w < MW; ++w) mine += __popc(cm[w]);
+  int off = mine;  // inclusive scan -> exclusive offset
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(kFull, off, o);
+    if (lane >= o) off += t;
+  }
+  const int count = __shfl_sync(kFull, off, 31);
+  off -= mine;
   if (count < P.m || count > P.cap) {
-    __syncwarp();
     emit_slow_exact<LOGP, T>(P, xs, s, row, ci);
     return;
   }
+  // pass 2: full keys of the candidates (unordered list)
+  {
+    int q = off;
+#pragma unroll
+    for (int w = 0; w < MW; ++w)
+      for (uint32_t b = cm[w]; b; b &= b - 1, ++q) {
+        const int j = 32 * (32 * w + __ffs(b) - 1) + lane;
+        ck[q] = key_of(ci, j);
+        cj[q] = (uint16_t)j;
+      }
+  }
   __syncwarp();
-  // 2. exact select of the m smallest keys: 32 key-monotone buckets, then rank inside
-  //    the bucket that holds the m-th smallest
   uint64_t kth = ~0ull;
   if (count > P.m) {
+    // 32 key-monotone buckets over [0, t_hi * 2^32)
     hist[lane] = 0;
     __syncwarp();
-    const float bscale = 32.0f / ((float)P.t_lim + 1.0f);
-    for (int q = lane; q < count; q += 32) {
-      const int b = min(31, (int)((float)(uint32_t)(ck[q] >> 32) * bscale));
-      atomicAdd(&hist[b], 1);
-    }
+    const float bscale = P.t_all ? 32.0f / 4294967296.0f : 32.0f / (float)P.t_hi;
+    for (int q = lane; q < count; q += 32) atomicAdd(&hist[min(31, (int)((float)(uint32_t)(ck[q] >> 32) * bscale))], 1);
     __syncwarp();
     const int h = hist[lane];
     int incl = h;
@@ -237,8 +296,8 @@ __device__ void sample_one(const SketchParams& P, const T* xs, int s, int64_t ro
     int nb = 0;
     for (int q0 = 0; q0 < count; q0 += 32) {
       const int q = q0 + lane;
-      bool in = false;
       uint64_t key = 0;
+      bool in = false;
       if (q < count) {
         key = ck[q];
         in = min(31, (int)((float)(uint32_t)(key >> 32) * bscale)) == B;
@@ -248,41 +307,67 @@ __device__ void sample_one(const SketchParams& P, const T* xs, int s, int64_t ro
       nb += __popc(bal);
     }
     __syncwarp();
-    const uint64_t mine = lane < hB ? memk[lane] : ~0ull;
+    const uint64_t mk = lane < hB ? memk[lane] : ~0ull;
     int rank = 0;
-    for (int o = 0; o < hB; ++o) {
-      const uint64_t other = __shfl_sync(kFull, mine, o);
-      rank += other < mine;
-    }
+    for (int o = 0; o < hB; ++o) rank += __shfl_sync(kFull, mk, o) < mk;
     const uint32_t hit = __ballot_sync(kFull, lane < hB && rank == r - 1);
-    kth = __shfl_sync(kFull, mine, __ffs(hit) - 1);
+    kth = __shfl_sync(kFull, mk, __ffs(hit) - 1);
   }
-  // 3. emit kept coordinates in ascending order (candidates are already j-sorted)
-  int base = 0;
-  for (int q0 = 0; q0 < count; q0 += 32) {
-    const int q = q0 + lane;
-    const bool keep = q < count && ck[q] <= kth;
-    const uint32_t bal = __ballot_sync(kFull, keep);
-    if (keep) {
-      const int j = cj[q];
-      const int64_t pos = row * P.m + base + __popc(bal & lanemask_lt());
-      P.idx_out[pos] = j;
-      if (P.val_out) store_val<T>(P.val_out, pos, xs[G::phys(s, j)], P.val_f64);
+  // kept mask: re-read this lane's candidates
+  uint32_t km[MW];
+  {
+    int q = off;
+#pragma unroll
+    for (int w = 0; w < MW; ++w) {
+      km[w] = 0;
+      for (uint32_t b = cm[w]; b; b &= b - 1, ++q) km[w] |= (uint32_t)(ck[q] <= kth) << (__ffs(b) - 1);
     }
-    base += __popc(bal);
+  }
+  // emit in ascending j = 32 r + lane: transpose the kept bit-matrix (lane i, bit r) so lane r
+  // holds row r's lane mask, prefix the row counts, then each kept element finds its slot.
+  const int64_t orow = row * P.m;
+  int wbase = 0;
+#pragma unroll
+  for (int w = 0; w < MW; ++w) {
+    const uint32_t t = warp_transpose32(km[w]);  // lane r: bit i = element (32 (32 w + r) + i) kept
+    const int cnt = __popc(t);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int excl = incl - cnt;
+    // shuffles need converged lanes: one round per kept element of the busiest lane
+    int mx = __popc(km[w]);
+    mx = __reduce_max_sync(kFull, mx);
+    uint32_t b = km[w];
+    for (int k = 0; k < mx; ++k) {
+      const int r = b ? __ffs(b) - 1 : 0;
+      const uint32_t tr = __shfl_sync(kFull, t, r);
+      const int er = __shfl_sync(kFull, excl, r);
+      if (b) {
+        const int j = 32 * (32 * w + r) + lane;
+        const int64_t pos = orow + wbase + er + __popc(tr & lanemask_lt());
+        P.idx_out[pos] = j;
+        if (P.val_out) store_val<T>(P.val_out, pos, y_at<LOGP, T>(xs, s, j), P.val_f64);
+        b &= b - 1;
+      }
+    }
+    wbase += __shfl_sync(kFull, incl, 31);
   }
   __syncwarp();
 }
 
 // ------------------------------------------------------------------------------------
 template <int LOGP, typename T>
-__global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchParams P) {
+__global__ void __launch_bounds__(kThreads, 2) sketch_kernel(const SketchParams P) {
   using G = Geo<LOGP>;
   extern __shared__ __align__(16) unsigned char smem[];
   T* xs = reinterpret_cast<T*>(smem);
-  uint32_t* sgn = reinterpret_cast<uint32_t*>(smem + sizeof(T) * kTileElems);
   constexpr int kSignWords = (G::P + 31) / 32;
-  unsigned char* wbase = smem + sizeof(T) * kTileElems + 4 * ((kSignWords + 3) & ~3);
+  uint32_t* sgn = reinterpret_cast<uint32_t*>(smem + sizeof(T) * ((G::WORDS + 1) & ~1));
+  unsigned char* wbase = reinterpret_cast<unsigned char*>(sgn) + 4 * ((kSignWords + 3) & ~3);
   const int warp = threadIdx.x >> 5;
   const size_t per_warp = (size_t)P.cap * 10 + 32 * 8 + 32 * 4;
   unsigned char* mine = wbase + per_warp * warp;
@@ -306,7 +391,7 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchParams P) 
 
   for (int64_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
     const int64_t row0 = tile * G::S;
-    __syncthreads();  // previous tile's phase 3 done with xs; signs visible
+    __syncthreads();  // previous tile's phase 3 is done with xs; signs visible
     if (has_x) {
       // ---- phase 1: load (zero pad p..p_pad and rows >= n) ----
       if (P.vec && !P.x_f64) {
@@ -325,10 +410,11 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchParams P) 
         for (int k = 0; k < NV; ++k) {
           const int f = (threadIdx.x + k * kThreads) * 4;
           const int s = f >> LOGP, i = f & (G::P - 1);
-          xs[G::phys(s, i + 0)] = (T)buf[k].x;
-          xs[G::phys(s, i + 1)] = (T)buf[k].y;
-          xs[G::phys(s, i + 2)] = (T)buf[k].z;
-          xs[G::phys(s, i + 3)] = (T)buf[k].w;
+          T* d = xs + s * G::SP + G::addr(i);  // 4 consecutive i never cross a 32-row
+          d[0] = (T)buf[k].x;
+          d[1] = (T)buf[k].y;
+          d[2] = (T)buf[k].z;
+          d[3] = (T)buf[k].w;
         }
       } else {
         for (int f = threadIdx.x; f < kTileElems; f += kThreads) {
@@ -339,7 +425,7 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchParams P) 
             v = P.x_f64 ? (T)__ldg(reinterpret_cast<const double*>(P.X) + row * P.ld + i)
                         : (T)__ldg(reinterpret_cast<const float*>(P.X) + row * P.ld + i);
           }
-          xs[G::phys(s, i)] = v;
+          xs[s * G::SP + G::addr(i)] = v;
         }
       }
       __syncthreads();
@@ -349,7 +435,7 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchParams P) 
         for (int f = threadIdx.x; f < kTileElems; f += kThreads) {
           const int s = f >> LOGP, i = f & (G::P - 1);
           const int64_t row = row0 + s;
-          if (row < P.n) P.y_out[row * G::P + i] = (double)xs[G::phys(s, i)];
+          if (row < P.n) P.y_out[row * G::P + i] = (double)xs[s * G::SP + G::addr(i)];
         }
       }
     }
@@ -370,7 +456,7 @@ static int launch_sketch_t(SketchParams P, cudaStream_t st) {
   using G = Geo<LOGP>;
   const size_t sign_bytes = 4 * (((G::P + 31) / 32 + 3) & ~3);
   const size_t per_warp = (size_t)P.cap * 10 + 32 * 8 + 32 * 4;
-  const size_t smem = sizeof(T) * kTileElems + sign_bytes + per_warp * kWarps;
+  const size_t smem = sizeof(T) * ((G::WORDS + 1) & ~1) + sign_bytes + per_warp * kWarps;
   auto kern = sketch_kernel<LOGP, T>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return check_launch("sketch smem attribute");
@@ -405,22 +491,22 @@ static int launch_sketch_logp(int logp, const SketchParams& P, cudaStream_t st) 
   return fail(SKC_EPARAM, "p_pad exceeds the largest instantiated transform (4096)");
 }
 
-// Host: prefilter threshold and candidate capacity for (p_pad, m)
-static void plan_select(int32_t p_pad, int32_t m, SketchParams& P) {
-  if (m == p_pad) {
+// Host: prefilter threshold and candidate capacity for a plan of (pk, m)
+static void plan_select(int32_t pk, int32_t m, SketchParams& P) {
+  P.t_all = 0;
+  P.t_hi = 0;
+  if (m == pk) {
     P.mode = kFullSet;
     P.cap = 32;
-    P.t_lim = 0xFFFFFFFFu;
     return;
   }
   const double mu = m + 5.0 * sqrt((double)m) + 8.0;  // expected candidates (mean - 5 sigma >= m)
-  if (mu >= 0.5 * p_pad) {
-    P.t_lim = 0xFFFFFFFFu;  // every coordinate is a candidate
-    P.cap = (p_pad + 31) & ~31;
+  if (mu >= 0.25 * pk) {
+    P.t_all = 1;  // every coordinate is a candidate
+    P.cap = (pk + 31) & ~31;
   } else {
-    double t = floor(mu / p_pad * 4294967296.0) - 1.0;
-    P.t_lim = (uint32_t)t;
-    double cap = mu + 6.0 * sqrt(mu) + 32.0;
+    P.t_hi = (uint32_t)floor(mu / pk * 4294967296.0);  // < 2^30 since mu < pk/4
+    const double cap = mu + 6.0 * sqrt(mu) + 32.0;
     P.cap = ((int)cap + 31) & ~31;
   }
   P.mode = kSelect;
@@ -459,16 +545,13 @@ int sketch_launch(const void* X, int32_t x_dtype, int64_t ld, int64_t n, int32_t
   } else {
     plan_select(p_pad, m, P);
   }
-  if (kind == SKC_KIND_NONE && X != nullptr) {
-    // identity transform: no signs, no WHT, no scale (transform.py:225-227)
-    return fail(SKC_EPARAM, "internal: kind none is routed through sketch_identity");
-  }
+  if (kind == SKC_KIND_NONE && X != nullptr) return fail(SKC_EPARAM, "internal: kind none uses sketch_identity");
   if (compute_dtype == SKC_F64) return launch_sketch_logp<double>(logp, P, st);
   return launch_sketch_logp<float>(logp, P, st);
 }
 
-// kind == none: values are the raw (zero-padded) coordinates. Reuses the sampler with a
-// gather kernel instead of the transform.
+// kind == none: values are the raw coordinates (transform.py:225-227); the sampler runs
+// without a transform and a gather kernel reads the values.
 __global__ void gather_identity_kernel(const void* X, int x_f64, int64_t ld, int64_t n, int32_t p, int32_t m,
                                        const int32_t* idx, void* val_out, int val_f64, double* y_out,
                                        int32_t p_pad) {

@@ -3,8 +3,10 @@ fixtures and the pinned CPU oracle.
 
 Tolerances:
   indices, counts, labels          bit-exact
-  fp64 values / mean / covariance  bit-exact for the sketch values and the transform;
-                                   1e-12 relative for estimators (parallel sum order)
+  fp64 sketch values, transforms   bit-exact
+  mean                             1e-12 relative (parallel fp64 sum order)
+  covariance                       1e-6 relative Frobenius (int32x2 fixed-point accumulator,
+                                   ~1e-7 typical; the north_star bound is 1e-5)
   fp32 fast path                   values 2e-6 relative, covariance 1e-5 relative Frobenius
                                    (the north_star bound)
 """
@@ -218,13 +220,15 @@ def test_estimators_hand_instances(skc):
     spec = skc.PreconditionSpec.create("none", 6)
     sk = skc.sketch_stream(X, spec, skc.SamplingPlan(4, 6, 6))
     est = skc.estimate_covariance(sk)
-    assert np.abs(est.matrix - X @ X.T / 9).max() < 1e-12 and est.n_used == 9
+    # exact at m=p (test_estimators.py:69-76); K3's fixed-point quantum bounds the error at
+    # ~6e-8 * tau^2 per product ("K3"), so the bound here is 1e-7, not 1e-12
+    assert np.abs(est.matrix - X @ X.T / 9).max() < 1e-7 and est.n_used == 9
     x = np.array([[1.0], [2.0], [3.0]])
     acc = np.zeros((3, 3))
     for s in [(0, 1), (0, 2), (1, 2)]:
         hs = skc.SparseSketch.from_host(skc.PreconditionSpec.create("none", 3), 1, np.array([s]), x[list(s), 0][None, :])
         acc += skc.estimate_covariance(hs).matrix
-    assert np.abs(acc / 3 - x @ x.T).max() < 1e-12
+    assert np.abs(acc / 3 - x @ x.T).max() < 1e-7
     with pytest.raises(skc.ParameterError):
         skc.estimate_covariance(skc.sketch_stream(X[:5], skc.PreconditionSpec.create("none", 5),
                                                   skc.SamplingPlan(7, 5, 1)))
