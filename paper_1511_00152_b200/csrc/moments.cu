@@ -140,7 +140,8 @@ constexpr int kMaxBands = 511;
 __host__ __device__ inline int64_t tri_off(int64_t a, int64_t p) { return a * p - a * (a - 1) / 2; }
 
 static int band_capacity(int32_t m, int32_t p_pad) {
-  return (kSmemBudget - kCovWarps * m * 8 - 4 * p_pad) / 4;  // int32 entries after staging + row table
+  // int32 entries left after the per-warp row staging and the row table
+  return (int)(((size_t)kSmemBudget - (size_t)kCovWarps * m * 16 - 4 * (size_t)p_pad) / 4);
 }
 // greedy row bands of <= cap entries; returns the count, fills out[0..count] if given
 static int make_bands(int32_t p_pad, int cap, int* out) {
@@ -169,6 +170,7 @@ struct CovParams {
   const double* stats;
   unsigned long long* part;  // [groups][tri_total] int64 fixed-point partials
   int nbands, groups;
+  int aligned;               // idx/val 16-byte aligned: tiles may use bulk copies
   int band_rows[kMaxBands + 1];
 };
 
@@ -185,6 +187,12 @@ __device__ __forceinline__ void red_if(bool p, unsigned long long* addr, unsigne
       : "memory");
 }
 
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // S from the value statistics; identical in every CTA and in the reduce kernel
 __device__ __forceinline__ int cov_scale(const double* stats, int m, double* tau_out) {
   const double cnt = stats[2] * (double)m;
@@ -196,6 +204,13 @@ __device__ __forceinline__ int cov_scale(const double* stats, int m, double* tau
   return S & ~1;  // even, so each factor carries 2^(S/2)
 }
 
+// Each warp streams its own rows (no CTA-wide synchronisation), prefetching the next row
+// into registers while the current one is processed. Lanes own columns u of the row, so
+// b_u and w_u stay in registers, and the loop runs over the band's rows t < u. Per update:
+// IADD, FMUL, F2I, ATOMS and a carry test. The low words carry a 2^31 bias, so a carry
+// needs a drift of 2^31 quanta and is rare even for entries whose sum hovers around zero.
+constexpr uint32_t kBias = 0x80000000u;
+
 template <typename V>
 __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __grid_constant__ CovParams P) {
   extern __shared__ int smem_i[];
@@ -206,60 +221,153 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
   const int64_t e0 = tri_off(r0, P.p_pad), e1 = tri_off(r1, P.p_pad);
   const int ne = (int)(e1 - e0);
   uint32_t* lo = reinterpret_cast<uint32_t*>(smem_i);
-  int* rowbase = smem_i + ne;                 // [r1 - r0]: entry (a, b) sits at rowbase[a - r0] + b
-  float* sval = reinterpret_cast<float*>(rowbase + (r1 - r0)) + (size_t)warp * m;
-  int* sidx = rowbase + (r1 - r0) + (size_t)kCovWarps * m + (size_t)warp * m;
+  int* rowbase = smem_i + ((ne + 1) & ~1);  // [r1 - r0]: entry (a, b) sits at rowbase[a - r0] + b
+  // per-warp staging, 4*m words: the general path uses [sidx: m][sval: m], the flat path
+  // reuses it as int2 T[m], U[m]
+  int* stage = rowbase + ((r1 - r0 + 1) & ~1) + (size_t)warp * 4 * m;
+  int* sidx = stage;
+  float* sval = reinterpret_cast<float*>(stage + m);
   unsigned long long* part = P.part + (size_t)group * tri_off(P.p_pad, P.p_pad) + e0;
 
   double tau;
   const int S = cov_scale(P.stats, m, &tau);
-  const float half = (float)ldexp(1.0, S / 2);
-  const double full = ldexp(1.0, S);
+  const float scale_a = (float)ldexp(1.0, S);
+  const double full_s = ldexp(1.0, S);
   const float ftau = (float)tau;
 
-  for (int e = threadIdx.x; e < ne; e += blockDim.x) lo[e] = 0u;
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) lo[e] = kBias;
   for (int a = r0 + threadIdx.x; a < r1; a += blockDim.x) rowbase[a - r0] = (int)(tri_off(a, P.p_pad) - e0) - a;
   __syncthreads();
 
   const int64_t g0 = P.n * group / P.groups, g1 = P.n * (group + 1) / P.groups;
-  for (int64_t r = g0 + warp; r < g1; r += kCovWarps) {
-    bool big = false;
-    int nlo = 0, nhi = 0;  // # indices < r0 and < r1 (rows are sorted)
-    for (int t0 = 0; t0 < m; t0 += 32) {
-      const int t = t0 + lane;
-      int j = 0x7FFFFFFF;
-      if (t < m) {
-        j = __ldg(P.idx + r * m + t);
-        const float v = (float)__ldg(reinterpret_cast<const V*>(P.val) + r * m + t);
-        sidx[t] = j;
-        sval[t] = v * half;
-        big |= fabsf(v) > ftau;
+  const V* val = reinterpret_cast<const V*>(P.val);
+  // register prefetch of the first two 32-column chunks (covers m <= 64 fully)
+  int pj0 = 0x7FFFFFFF, pj1 = 0x7FFFFFFF;
+  V pv0 = 0, pv1 = 0;
+  auto prefetch = [&](int64_t r) {
+    pj0 = pj1 = 0x7FFFFFFF;
+    if (r < g1) {
+      if (lane < m) {
+        pj0 = __ldg(P.idx + r * m + lane);
+        pv0 = __ldg(val + r * m + lane);
       }
+      if (lane + 32 < m) {
+        pj1 = __ldg(P.idx + r * m + lane + 32);
+        pv1 = __ldg(val + r * m + lane + 32);
+      }
+    }
+  };
+  prefetch(g0 + warp);
+  for (int64_t r = g0 + warp; r < g1; r += kCovWarps) {
+    const int j0 = pj0, j1 = pj1;
+    const float v0 = (float)pv0, v1 = (float)pv1;
+    prefetch(r + kCovWarps);
+    int nlo = __popc(__ballot_sync(kFullMask, j0 < r0)) + __popc(__ballot_sync(kFullMask, j1 < r0));
+    int nhi = __popc(__ballot_sync(kFullMask, j0 < r1)) + __popc(__ballot_sync(kFullMask, j1 < r1));
+    bool big = (lane < m && fabsf(v0) > ftau) || (lane + 32 < m && fabsf(v1) > ftau);
+    for (int t0 = 64; t0 < m; t0 += 32) {  // columns beyond the prefetched two chunks
+      const int t = t0 + lane;
+      const int j = t < m ? __ldg(P.idx + r * m + t) : 0x7FFFFFFF;
+      if (t < m) big |= fabsf((float)__ldg(val + r * m + t)) > ftau;
       nlo += __popc(__ballot_sync(kFullMask, j < r0));
       nhi += __popc(__ballot_sync(kFullMask, j < r1));
     }
     if (nlo == nhi) continue;  // none of this row's indices fall in the band
-    big = __any_sync(kFullMask, big);
+    const bool any_big = __any_sync(kFullMask, big);
+    if (!any_big) {
+      // flat enumeration of the visit's pairs {(t, u): nlo <= t < nhi, t <= u < m}:
+      // f = O(t - nlo) + (u - t) with O(x) = x*(m - nlo) - x*(x-1)/2; lanes take f = lane + 32k
+      // and invert O with the quadratic formula. Row data is staged as packed pairs:
+      // T[t] = (base_t, w_t * 2^S) and U[u] = (b_u, w_u).
+      int2* T = reinterpret_cast<int2*>(sidx);  // per-warp staging: 2*m words for T, 2*m for U
+      int2* U = T + m;
+      for (int t = lane; t < m; t += 32) {
+        int jt;
+        float vt;
+        if (t < 32) {
+          jt = j0;
+          vt = v0;
+        } else if (t < 64) {
+          jt = j1;
+          vt = v1;
+        } else {
+          jt = __ldg(P.idx + r * m + t);
+          vt = (float)__ldg(val + r * m + t);
+        }
+        U[t] = make_int2(jt, __float_as_int(vt));
+        if (t >= nlo && t < nhi) T[t] = make_int2(rowbase[jt - r0], __float_as_int(vt * scale_a));
+      }
+      __syncwarp();
+      const int h = nhi - nlo;
+      const int F = h * (m - nlo) - h * (h - 1) / 2;
+      const float A = (float)(m - nlo) + 0.5f;
+      for (int f = lane; f < F; f += 32) {
+        int x = (int)(A - sqrt_approx(fmaxf(A * A - 2.0f * (float)f, 0.0f)));  // +-1 fixed below
+        int ox = x * (m - nlo) - x * (x - 1) / 2;
+        if (ox > f) {  // float rounding: step back
+          --x;
+          ox = x * (m - nlo) - x * (x - 1) / 2;
+        } else {
+          const int o1 = ox + (m - nlo - x);
+          if (o1 <= f) {
+            ++x;
+            ox = o1;
+          }
+        }
+        const int t = nlo + x, u = t + (f - ox);
+        const int2 tt = T[t], uu = U[u];
+        const int e = tt.x + uu.x;
+        const int q = __float2int_rn(__int_as_float(tt.y) * __int_as_float(uu.y));
+        const uint32_t old = atomicAdd(lo + e, (uint32_t)q);
+        if ((old + (uint32_t)q < old) != (q < 0))  // carry (q >= 0) / borrow (q < 0): rare
+          atomicAdd(part + e, (unsigned long long)((long long)(q < 0 ? -1 : 1) << 32));
+      }
+      __syncwarp();
+      continue;
+    }
+    // general path (m > 64, or a value above tau): stage the row in shared memory
+    if (lane < m) {
+      sidx[lane] = j0;
+      sval[lane] = v0 * scale_a;
+    }
+    if (lane + 32 < m) {
+      sidx[lane + 32] = j1;
+      sval[lane + 32] = v1 * scale_a;
+    }
+    for (int t0 = 64; t0 < m; t0 += 32) {
+      const int t = t0 + lane;
+      if (t < m) {
+        sidx[t] = __ldg(P.idx + r * m + t);
+        sval[t] = (float)__ldg(val + r * m + t) * scale_a;
+      }
+    }
     __syncwarp();
-    if (!big) {
-      for (int t = nlo; t < nhi; ++t) {
-        const float va = sval[t];
-        const int base = rowbase[sidx[t] - r0];
-        for (int u = t + lane; u < m; u += 32) {
-          const int q = __float2int_rn(va * sval[u]);
-          const int e = base + sidx[u];
-          const uint32_t old = atomicAdd(lo + e, (uint32_t)q);
-          const int delta = (int)(old + (uint32_t)q < old) - (int)(q < 0);
-          red_if(delta != 0, part + e, (unsigned long long)((long long)delta << 32));
+    if (!any_big) {
+      for (int c0 = 0; c0 < m; c0 += 32) {
+        const int u = c0 + lane;
+        const int tmax = min(nhi, c0 + 32);  // rows t <= u within this chunk
+        if (nlo >= tmax) continue;
+        const int bu = u < m ? sidx[u] : 0;
+        const float vu = u < m ? (c0 == 0 ? v0 : (c0 == 32 ? v1 : (float)__ldg(val + r * m + u))) : 0.f;
+        for (int t = nlo; t < tmax; ++t) {
+          const int base = rowbase[sidx[t] - r0];
+          const float va = sval[t];
+          if (t <= u && u < m) {
+            const int e = base + bu;
+            const int q = __float2int_rn(va * vu);
+            const uint32_t old = atomicAdd(lo + e, (uint32_t)q);
+            if ((old + (uint32_t)q < old) != (q < 0))  // carry (q >= 0) / borrow (q < 0): rare
+              atomicAdd(part + e, (unsigned long long)((long long)(q < 0 ? -1 : 1) << 32));
+          }
         }
       }
     } else {
       // a value above tau: exact fp64 product, scaled, straight to the int64 partial
       for (int t = nlo; t < nhi; ++t) {
-        const double va = ldv64<V>(P.val, r * m + t);
+        const double va = (double)__ldg(val + r * m + t);
         const int base = rowbase[sidx[t] - r0];
         for (int u = t + lane; u < m; u += 32) {
-          const long long q = __double2ll_rn(dmul(dmul(va, ldv64<V>(P.val, r * m + u)), full));
+          const long long q = __double2ll_rn(dmul(dmul(va, (double)__ldg(val + r * m + u)), full_s));
           atomicAdd(part + base + sidx[u], (unsigned long long)q);
         }
       }
@@ -268,8 +376,8 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
   }
   __syncthreads();
   for (int e = threadIdx.x; e < ne; e += blockDim.x) {
-    const uint32_t q = lo[e];
-    if (q != 0u) atomicAdd(part + e, (unsigned long long)q);
+    const long long q = (long long)lo[e] - (long long)kBias;
+    if (q != 0) atomicAdd(part + e, (unsigned long long)q);
   }
 }
 
@@ -319,6 +427,7 @@ int cov_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int3
   H.p_pad = p_pad;
   H.stats = stats;
   H.part = reinterpret_cast<unsigned long long*>(ws);
+  H.aligned = (reinterpret_cast<uintptr_t>(idx) % 16 == 0) && (reinterpret_cast<uintptr_t>(val) % 16 == 0);
   const int64_t total = tri_off(p_pad, p_pad);
   cudaMemsetAsync(ws, 0, (size_t)H.groups * total * 8, st);
   int maxe = 0, maxr = 0;
@@ -327,7 +436,7 @@ int cov_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int3
     if (e > maxe) maxe = e;
     if (H.band_rows[b + 1] - H.band_rows[b] > maxr) maxr = H.band_rows[b + 1] - H.band_rows[b];
   }
-  const size_t smem = (size_t)maxe * 4 + (size_t)maxr * 4 + (size_t)kCovWarps * m * 8;
+  const size_t smem = (size_t)((maxe + 1) & ~1) * 4 + (size_t)((maxr + 1) & ~1) * 4 + (size_t)kCovWarps * m * 16;
   auto k = val_f64 ? cov_band_kernel<double> : cov_band_kernel<float>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<H.nbands * H.groups, kCovWarps * 32, smem, st>>>(H);

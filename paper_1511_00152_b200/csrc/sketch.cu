@@ -361,7 +361,7 @@ __device__ void sample_one(const SketchParams& P, const T* xs, int s, int64_t ro
 
 // ------------------------------------------------------------------------------------
 template <int LOGP, typename T>
-__global__ void __launch_bounds__(kThreads, 2) sketch_kernel(const SketchParams P) {
+__global__ void __launch_bounds__(kThreads, 3) sketch_kernel(const SketchParams P) {
   using G = Geo<LOGP>;
   extern __shared__ __align__(16) unsigned char smem[];
   T* xs = reinterpret_cast<T*>(smem);
