@@ -36,7 +36,12 @@ def u64(x: int) -> int:
 
 
 def default_device() -> torch.device:
-    return torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cuda")
+    """The current CUDA device; raises DeviceError when there is none (no CPU fallback)."""
+    if not torch.cuda.is_available():
+        from .errors import DeviceError
+
+        raise DeviceError("no CUDA device: the sketch hot path runs only on the GPU")
+    return torch.device("cuda", torch.cuda.current_device())
 
 
 @dataclass(frozen=True)
