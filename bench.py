@@ -222,6 +222,24 @@ def run_reference(args, cfg):
     }
 
 
+def profiled_traffic(workload, n, stage):
+    """dram read+write bytes per launch of the stage's kernel, from the committed ncu capture
+    (profiles/round1_<wl>_ncu_full.json) when it was taken at this exact size, else None."""
+    names = {"sketch": "sketch_kernel", "covariance": "cov_band_kernel", "moments": "moments_kernel"}
+    path = os.path.join(ROOT, "profiles", f"round1_{workload}_ncu_full.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        if f"n=2^{int(np.log2(n))}" not in d["config"] or (1 << int(np.log2(n))) != n:
+            return None
+        for k, v in d["kernels"].items():
+            if k.startswith(names.get(stage, "?")):
+                return v.get("traffic_bytes")
+    except Exception:
+        return None
+    return None
+
+
 def metric_name(cfg):
     if cfg["kind"] == "cov":
         return "samples/s precondition+sparsify+covariance"
@@ -387,13 +405,24 @@ def main():
     ms_step = float(t.item())
     value = work_units / (ms_step * 1e-3)
 
-    # roofline of the dominant kernel (HBM-bound; algorithmic bytes per launch / mean launch time)
+    # roofline of the dominant kernel (HBM; algorithmic bytes per launch / mean launch time)
     dom = max(stage_ms, key=lambda k: stage_ms[k])
-    dom_bytes = unit_bytes[dom] * (n if cfg["kind"] == "cov" else n)
+    dom_bytes = unit_bytes[dom] * n
     achieved = dom_bytes / (stage_ms[dom] * 1e-3) / 1e9
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src,
+                "frac": achieved / hbm_peak, "traffic": profiled_traffic(args.workload, n, dom), "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": dom_bytes}
+    if cfg["kind"] == "cov":
+        # every stage, and the pass as a whole, against the HBM roofline; K3's own bound is the
+        # shared-memory ATOMS.ADD rate (tools/microbench: 1.23e12 updates/s on this pool's B200)
+        per_stage = {k: {"algorithmic_GBps": unit_bytes[k] * n / (stage_ms[k] * 1e-3) / 1e9,
+                         "frac_hbm": unit_bytes[k] * n / (stage_ms[k] * 1e-3) / 1e9 / hbm_peak}
+                     for k in stage_ms if stage_ms[k] > 0 and unit_bytes[k] > 0}
+        upd = n * m * (m + 1) / 2 / (stage_ms["covariance"] * 1e-3)
+        per_stage["covariance"]["smem_atomic_updates_per_s"] = upd
+        per_stage["covariance"]["frac_of_measured_atoms_peak"] = upd / 1.226e12
+        roofline["stages"] = per_stage
+        roofline["pass_frac_hbm"] = (4 * p + 8 * m) * (n / (ms_step * 1e-3)) / 1e9 / hbm_peak
 
     out = {
         "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
