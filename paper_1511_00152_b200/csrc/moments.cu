@@ -187,12 +187,6 @@ __device__ __forceinline__ void red_if(bool p, unsigned long long* addr, unsigne
       : "memory");
 }
 
-__device__ __forceinline__ float sqrt_approx(float x) {
-  float y;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
 // S from the value statistics; identical in every CTA and in the reduce kernel
 __device__ __forceinline__ int cov_scale(const double* stats, int m, double* tau_out) {
   const double cnt = stats[2] * (double)m;
@@ -298,23 +292,20 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
         if (t >= nlo && t < nhi) T[t] = make_int2(rowbase[jt - r0], __float_as_int(vt * scale_a));
       }
       __syncwarp();
+      // fold row i with row h-1-i (lengths add up to Lp): the trapezoid becomes a rectangle
+      // of floor(h/2) rows of Lp, plus a half row when h is odd; f -> (r, c) by one reciprocal
+      // multiply ((f + 0.5) / Lp keeps a fractional part >= 2^-8, so fp32 floor is exact)
       const int h = nhi - nlo;
+      const int Lp = 2 * (m - nlo) - h + 1;
       const int F = h * (m - nlo) - h * (h - 1) / 2;
-      const float A = (float)(m - nlo) + 0.5f;
+      const float inv = 1.0f / (float)Lp;
       for (int f = lane; f < F; f += 32) {
-        int x = (int)(A - sqrt_approx(fmaxf(A * A - 2.0f * (float)f, 0.0f)));  // +-1 fixed below
-        int ox = x * (m - nlo) - x * (x - 1) / 2;
-        if (ox > f) {  // float rounding: step back
-          --x;
-          ox = x * (m - nlo) - x * (x - 1) / 2;
-        } else {
-          const int o1 = ox + (m - nlo - x);
-          if (o1 <= f) {
-            ++x;
-            ox = o1;
-          }
-        }
-        const int t = nlo + x, u = t + (f - ox);
+        const int rr = (int)(((float)f + 0.5f) * inv);
+        const int c = f - rr * Lp;
+        const int Lr = m - nlo - rr;  // length of row nlo + rr
+        const bool first = c < Lr;
+        const int t = first ? nlo + rr : nhi - 1 - rr;
+        const int u = t + (first ? c : c - Lr);
         const int2 tt = T[t], uu = U[u];
         const int e = tt.x + uu.x;
         const int q = __float2int_rn(__int_as_float(tt.y) * __int_as_float(uu.y));
