@@ -40,7 +40,41 @@ __global__ void moments_kernel(const int32_t* __restrict__ idx, const V* __restr
   const int64_t c0 = n * blockIdx.x / gridDim.x, c1 = n * (blockIdx.x + 1) / gridDim.x;
   const int64_t r0 = c0 + (c1 - c0) * warp / warps, r1 = c0 + (c1 - c0) * (warp + 1) / warps;
   double sq = 0.0, mx = 0.0;
-  for (int64_t r = r0; r < r1; ++r) {
+  // rows in batches of 4: all loads of a batch are issued before the shared-memory updates
+  constexpr int kB = 4, kMaxC = 4;  // kMaxC lane-chunks per row cover m <= 128 from registers
+  int64_t r = r0;
+  if (m <= 32 * kMaxC) {
+    for (; r + kB <= r1; r += kB) {
+      int jj[kB][kMaxC];
+      double vv[kB][kMaxC];
+#pragma unroll
+      for (int b = 0; b < kB; ++b)
+#pragma unroll
+        for (int c = 0; c < kMaxC; ++c) {
+          const int t = lane + 32 * c;
+          jj[b][c] = -1;
+          vv[b][c] = 0.0;
+          if (t < m) {
+            jj[b][c] = __ldg(idx + (r + b) * m + t);
+            vv[b][c] = (double)__ldg(val + (r + b) * m + t);
+          }
+        }
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+#pragma unroll
+        for (int c = 0; c < kMaxC; ++c) {
+          if (jj[b][c] >= 0) {
+            const double v = vv[b][c];
+            mine[jj[b][c]] = dadd(mine[jj[b][c]], v);
+            sq = dadd(sq, dmul(v, v));
+            mx = fmax(mx, fabs(v));
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+  for (; r < r1; ++r) {
     for (int t = lane; t < m; t += 32) {
       const int j = __ldg(idx + r * m + t);
       const double v = (double)__ldg(val + r * m + t);
