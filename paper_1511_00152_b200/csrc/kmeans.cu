@@ -46,13 +46,25 @@ __device__ double pw_rec(const double* a, int64_t n) {
   return dadd(pw_rec(a, n2), pw_rec(a + n2, n - n2));
 }
 
-// Same association as pw_rec, with the top D levels split across 2^D threads.
+// Same association as pw_rec: the top D levels of the recursion are split across 2^D
+// threads (each computes one subtree), then combined bottom-up level by level in parallel.
+// Node (d, path) keeps its value in slot path << (D - d), the slot of its leftmost leaf.
 constexpr int kPwDepth = 10;
-__device__ double pw_combine(const double* res, int d, int path, int64_t n) {
-  if (n <= 128 || d == kPwDepth) return res[path << (kPwDepth - d)];
-  int64_t n2 = n / 2;
-  n2 -= n2 % 8;
-  return dadd(pw_combine(res, d + 1, path * 2, n2), pw_combine(res, d + 1, path * 2 + 1, n - n2));
+
+__device__ __forceinline__ int64_t pw_node_len(int64_t n, int d, int path, bool* leaf_above) {
+  // length of node (d, path); leaf_above = an ancestor (or itself before depth d) is a leaf
+  int64_t len = n;
+  *leaf_above = false;
+  for (int k = 0; k < d; ++k) {
+    if (len <= 128) {
+      *leaf_above = true;
+      return len;
+    }
+    int64_t n2 = len / 2;
+    n2 -= n2 % 8;
+    len = ((path >> (d - 1 - k)) & 1) ? len - n2 : n2;
+  }
+  return len;
 }
 
 __global__ void __launch_bounds__(1 << kPwDepth) pairwise_kernel(const double* __restrict__ x, int64_t n,
@@ -78,7 +90,18 @@ __global__ void __launch_bounds__(1 << kPwDepth) pairwise_kernel(const double* _
   }
   res[t] = active ? pw_rec(x + off, len) : 0.0;
   __syncthreads();
-  if (t == 0) out[0] = pw_combine(res, 0, 0, n);
+  for (int d = kPwDepth - 1; d >= 0; --d) {
+    if (t < (1 << d)) {
+      bool leaf_above;
+      const int64_t L = pw_node_len(n, d, t, &leaf_above);
+      if (!leaf_above && L > 128) {  // internal node: left + right child
+        const int sh = kPwDepth - d;
+        res[t << sh] = dadd(res[(2 * t) << (sh - 1)], res[(2 * t + 1) << (sh - 1)]);
+      }
+    }
+    __syncthreads();
+  }
+  if (t == 0) out[0] = res[0];
 }
 
 int pairwise_launch(const double* x, int64_t n, double* out, cudaStream_t st) {
@@ -88,65 +111,112 @@ int pairwise_launch(const double* x, int64_t n, double* out, cudaStream_t st) {
 
 // ---------------------------------------------------------------------------------
 // assign
-__global__ void km_tables_kernel(const double* __restrict__ mu, int64_t total, double* __restrict__ m2,
-                                 double* __restrict__ msq) {
+constexpr int kAsgWarps = 8;
+
+// packed per-(j,k) table: {-2 mu, mu*mu} (np.vstack([-2.0 * mu, mu * mu]), cluster.py:182)
+__global__ void km_tables2_kernel(const double* __restrict__ mu, int64_t total, double2* __restrict__ tab) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= total) return;
   const double v = mu[e];
-  m2[e] = dmul(-2.0, v);  // np.vstack([-2.0 * mu, mu * mu]) (cluster.py:182)
-  msq[e] = dmul(v, v);
+  tab[e] = make_double2(dmul(-2.0, v), dmul(v, v));
 }
 
-// colsq of one row, numpy pairwise order over m squared values (cluster.py:148)
-__device__ double row_colsq(const double* sv, int m) {
-  // sv holds the squares
-  return pw_rec(sv, m);
-}
-
-constexpr int kAsgWarps = 8;
-
-template <typename V>
+// A warp holds G = 32/KP points; lane = g*KP + k. For K > KP the lane loops over k += KP.
+// colsq: numpy pairwise order on 8 lanes of the group (m <= 128), else pw_rec on one lane.
+// d2[k] = sum_t v_t*(-2 mu[j_t,k]) then + sum_t mu[j_t,k]^2 (csr_matvecs axpy order) + colsq.
+template <typename V, int KP>
 __global__ void __launch_bounds__(kAsgWarps * 32)
     km_assign_kernel(const int32_t* __restrict__ idx, const void* __restrict__ val, int64_t n, int m,
-                     const double* __restrict__ m2, const double* __restrict__ msq, int K,
-                     const int32_t* __restrict__ prev, int32_t* __restrict__ labels, double* __restrict__ d2min,
-                     int64_t* __restrict__ blk_changed, double* __restrict__ blk_max, int64_t* __restrict__ blk_arg) {
+                     const double2* __restrict__ tab, int K, const int32_t* __restrict__ prev,
+                     int32_t* __restrict__ labels, double* __restrict__ d2min, int64_t* __restrict__ blk_changed,
+                     double* __restrict__ blk_max, int64_t* __restrict__ blk_arg) {
+  constexpr int G = 32 / KP;
   extern __shared__ unsigned char sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int* sidx = reinterpret_cast<int*>(sm) + (size_t)warp * m;
-  double* sval = reinterpret_cast<double*>(sm + (((size_t)kAsgWarps * m * 4 + 15) & ~(size_t)15)) + (size_t)warp * 2 * m;
-  double* ssq = sval + m;
+  const int g = lane / KP, k0 = lane % KP;
+  int* sidx = reinterpret_cast<int*>(sm) + (size_t)warp * G * m;
+  double* sval = reinterpret_cast<double*>(sm + (((size_t)kAsgWarps * G * m * 4 + 15) & ~(size_t)15)) +
+                 (size_t)warp * G * m;
   int64_t changed = 0;
   double bmax = -1.0;
   int64_t barg = -1;
   const int64_t gw = (int64_t)blockIdx.x * kAsgWarps + warp, nw = (int64_t)gridDim.x * kAsgWarps;
-  for (int64_t i = gw; i < n; i += nw) {
-    for (int t = lane; t < m; t += 32) {
-      sidx[t] = __ldg(idx + i * m + t);
-      const double v = ldd<V>(val, i * m + t);
-      sval[t] = v;
-      ssq[t] = dmul(v, v);
+  for (int64_t i0 = gw * G; i0 < n; i0 += nw * G) {
+    __syncwarp();
+    for (int e = lane; e < G * m; e += 32) {
+      const int gg = e / m, t = e - gg * m;
+      const int64_t i = i0 + gg;
+      if (i < n) {
+        sidx[gg * m + t] = __ldg(idx + i * m + t);
+        sval[gg * m + t] = ldd<V>(val, i * m + t);
+      }
     }
     __syncwarp();
+    const int64_t i = i0 + g;
+    const int* si = sidx + g * m;
+    const double* sv = sval + g * m;
+    // colsq = (v*v).sum() in numpy's pairwise order
     double colsq = 0.0;
-    if (lane == 0) colsq = row_colsq(ssq, m);
-    colsq = __shfl_sync(kFM, colsq, 0);
+    if (m < 8) {
+      if (k0 == 0)
+        for (int t = 0; t < m; ++t) colsq = dadd(colsq, dmul(sv[t], sv[t]));
+    } else if (m <= 128) {
+      double r = 0.0;
+      if (k0 < 8) {
+        r = dmul(sv[k0], sv[k0]);
+        for (int t = 8 + k0; t < m - (m % 8); t += 8) r = dadd(r, dmul(sv[t], sv[t]));
+      }
+      // ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)) across lanes k0 = 0..7 of the group
+      const double r1 = __shfl_down_sync(kFM, r, 1, KP);
+      const double s01 = dadd(r, r1);                       // valid at k0 = 0,2,4,6
+      const double s23 = __shfl_down_sync(kFM, s01, 2, KP);
+      const double q = dadd(s01, s23);                      // valid at k0 = 0,4
+      const double q2 = __shfl_down_sync(kFM, q, 4, KP);
+      if (k0 == 0) {
+        colsq = dadd(q, q2);
+        for (int t = m - (m % 8); t < m; ++t) colsq = dadd(colsq, dmul(sv[t], sv[t]));
+      }
+    } else if (k0 == 0) {
+      double* tmp = const_cast<double*>(sv);  // square in place (the row is re-staged next time)
+      for (int t = 0; t < m; ++t) tmp[t] = dmul(sv[t], sv[t]);
+      colsq = pw_rec(tmp, m);
+      for (int t = 0; t < m; ++t) tmp[t] = ldd<V>(val, i * m + t);
+    }
+    __syncwarp();
+    colsq = __shfl_sync(kFM, colsq, g * KP, 32);
     double best = 0.0;
     int bk = -1;
-    for (int k0 = 0; k0 < K; k0 += 32) {
-      const int k = k0 + lane;
-      double d2 = 0.0;
-      if (k < K) {
-        double acc = 0.0;  // csr_matvecs axpy order: values part, then ones part
-        for (int t = 0; t < m; ++t) acc = dadd(acc, dmul(sval[t], __ldg(m2 + (int64_t)sidx[t] * K + k)));
-        for (int t = 0; t < m; ++t) acc = dadd(acc, __ldg(msq + (int64_t)sidx[t] * K + k));
-        d2 = dadd(acc, colsq);
+    for (int kb = 0; kb < K; kb += KP) {
+      const int k = kb + k0;
+      double v = __longlong_as_double(0x7FF0000000000000LL);
+      int kk = 0x7FFFFFFF;
+      if (k < K && i < n) {
+        double acc = 0.0;
+        int t = 0;
+        for (; t + 4 <= m; t += 4) {
+          const double2 a0 = __ldg(tab + (int64_t)si[t] * K + k), a1 = __ldg(tab + (int64_t)si[t + 1] * K + k);
+          const double2 a2 = __ldg(tab + (int64_t)si[t + 2] * K + k), a3 = __ldg(tab + (int64_t)si[t + 3] * K + k);
+          acc = dadd(acc, dmul(sv[t], a0.x));
+          acc = dadd(acc, dmul(sv[t + 1], a1.x));
+          acc = dadd(acc, dmul(sv[t + 2], a2.x));
+          acc = dadd(acc, dmul(sv[t + 3], a3.x));
+        }
+        for (; t < m; ++t) acc = dadd(acc, dmul(sv[t], __ldg(tab + (int64_t)si[t] * K + k).x));
+        for (t = 0; t + 4 <= m; t += 4) {
+          const double b0 = __ldg(tab + (int64_t)si[t] * K + k).y, b1 = __ldg(tab + (int64_t)si[t + 1] * K + k).y;
+          const double b2 = __ldg(tab + (int64_t)si[t + 2] * K + k).y, b3 = __ldg(tab + (int64_t)si[t + 3] * K + k).y;
+          acc = dadd(acc, b0);
+          acc = dadd(acc, b1);
+          acc = dadd(acc, b2);
+          acc = dadd(acc, b3);
+        }
+        for (; t < m; ++t) acc = dadd(acc, __ldg(tab + (int64_t)si[t] * K + k).y);
+        v = dadd(acc, colsq);
+        kk = k;
       }
-      // first minimum (np.argmin): lower k wins ties
-      double v = k < K ? d2 : __longlong_as_double(0x7FF0000000000000LL);
-      int kk = k < K ? k : 0x7FFFFFFF;
+      // first minimum over the group (np.argmin: lower k wins ties)
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
+      for (int o = KP / 2; o > 0; o >>= 1) {
         const double ov = __shfl_xor_sync(kFM, v, o);
         const int ok = __shfl_xor_sync(kFM, kk, o);
         if (ov < v || (ov == v && ok < kk)) {
@@ -159,19 +229,28 @@ __global__ void __launch_bounds__(kAsgWarps * 32)
         bk = kk;
       }
     }
-    const double dm = best > 0.0 ? best : 0.0;  // np.clip(.., 0, None)
-    if (lane == 0) {
+    if (k0 == 0 && i < n) {
+      const double dm = best > 0.0 ? best : 0.0;  // np.clip(.., 0, None)
       labels[i] = bk;
       d2min[i] = dm;
       if (prev != nullptr) changed += prev[i] != bk;
-      if (dm > bmax) {  // rows visited in ascending order per warp: keeps the first max
+      if (dm > bmax) {  // each lane sees its points in ascending order: keeps the first max
         bmax = dm;
         barg = i;
       }
     }
-    __syncwarp();
   }
-  // block reduction: changed sum, (max, first index)
+  // block reduction over all lanes: changed sum, (max, first index)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t oc = __shfl_xor_sync(kFM, changed, o), oa = __shfl_xor_sync(kFM, barg, o);
+    const double om = __shfl_xor_sync(kFM, bmax, o);
+    changed += oc;
+    if (oa >= 0 && (om > bmax || (om == bmax && (barg < 0 || oa < barg)))) {
+      bmax = om;
+      barg = oa;
+    }
+  }
   __shared__ int64_t s_ch[kAsgWarps], s_arg[kAsgWarps];
   __shared__ double s_mx[kAsgWarps];
   if (lane == 0) {
@@ -185,7 +264,7 @@ __global__ void __launch_bounds__(kAsgWarps * 32)
     double mx = -1.0;
     for (int w = 0; w < kAsgWarps; ++w) {
       c += s_ch[w];
-      if (s_arg[w] >= 0 && (s_mx[w] > mx || (s_mx[w] == mx && s_arg[w] < a))) {
+      if (s_arg[w] >= 0 && (s_mx[w] > mx || (s_mx[w] == mx && (a < 0 || s_arg[w] < a)))) {
         mx = s_mx[w];
         a = s_arg[w];
       }
@@ -198,19 +277,49 @@ __global__ void __launch_bounds__(kAsgWarps * 32)
 
 __global__ void km_assign_reduce_kernel(const int64_t* __restrict__ blk_changed, const double* __restrict__ blk_max,
                                         const int64_t* __restrict__ blk_arg, int nb, int64_t* out, double* d2max) {
-  if (threadIdx.x != 0) return;
   int64_t c = 0, a = -1;
   double mx = -1.0;
-  for (int b = 0; b < nb; ++b) {
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
     c += blk_changed[b];
     if (blk_arg[b] >= 0 && (blk_max[b] > mx || (blk_max[b] == mx && blk_arg[b] < a))) {
       mx = blk_max[b];
       a = blk_arg[b];
     }
   }
-  out[0] = c;
-  out[1] = a;
-  if (d2max) d2max[0] = mx;
+  // warp then block combine: (max value, smallest index among ties), sum of changed
+  __shared__ int64_t sc[32], sa[32];
+  __shared__ double sm[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t oc = __shfl_xor_sync(kFM, c, o), oa = __shfl_xor_sync(kFM, a, o);
+    const double om = __shfl_xor_sync(kFM, mx, o);
+    c += oc;
+    if (oa >= 0 && (om > mx || (om == mx && (a < 0 || oa < a)))) {
+      mx = om;
+      a = oa;
+    }
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sc[w] = c;
+    sa[w] = a;
+    sm[w] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t C = 0, A = -1;
+    double M = -1.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      C += sc[i];
+      if (sa[i] >= 0 && (sm[i] > M || (sm[i] == M && (A < 0 || sa[i] < A)))) {
+        M = sm[i];
+        A = sa[i];
+      }
+    }
+    out[0] = C;
+    out[1] = A;
+    if (d2max) d2max[0] = M;
+  }
 }
 
 static int assign_grid(int64_t n) {
@@ -224,28 +333,43 @@ size_t assign_ws(int64_t n, int32_t p_pad, int32_t K) {
   return (size_t)2 * p_pad * K * sizeof(double) + (size_t)assign_grid(n) * 24 + 64;
 }
 
+template <typename V, int KP>
+static void launch_assign_kp(int G, const int32_t* idx, const void* val, int64_t n, int32_t m, const double2* tab,
+                             int32_t K, const int32_t* prev, int32_t* labels, double* d2min, int64_t* bch,
+                             double* bmx, int64_t* barg, cudaStream_t st) {
+  constexpr int GP = 32 / KP;
+  const size_t smem = (((size_t)kAsgWarps * GP * m * 4 + 15) & ~(size_t)15) + (size_t)kAsgWarps * GP * m * 8;
+  auto k = km_assign_kernel<V, KP>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k<<<G, kAsgWarps * 32, smem, st>>>(idx, val, n, m, tab, K, prev, labels, d2min, bch, bmx, barg);
+}
+
 int assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, const double* mu,
                   int32_t p_pad, int32_t K, const int32_t* prev, int32_t* labels, double* d2min, int64_t* out,
                   double* d2max, void* ws, cudaStream_t st) {
-  double* m2 = reinterpret_cast<double*>(ws);
-  double* msq = m2 + (size_t)p_pad * K;
+  double2* tab = reinterpret_cast<double2*>(ws);
   const int G = assign_grid(n);
-  int64_t* bch = reinterpret_cast<int64_t*>(msq + (size_t)p_pad * K);
+  int64_t* bch = reinterpret_cast<int64_t*>(tab + (size_t)p_pad * K);
   double* bmx = reinterpret_cast<double*>(bch + G);
   int64_t* barg = reinterpret_cast<int64_t*>(bmx + G);
   const int64_t total = (int64_t)p_pad * K;
-  km_tables_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(mu, total, m2, msq);
-  int rc = check_launch("km_tables_kernel");
+  km_tables2_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(mu, total, tab);
+  int rc = check_launch("km_tables2_kernel");
   if (rc) return rc;
   if (n > 0) {
-    const size_t smem = (((size_t)kAsgWarps * m * 4 + 15) & ~(size_t)15) + (size_t)kAsgWarps * 2 * m * 8;
-    auto k = val_f64 ? km_assign_kernel<double> : km_assign_kernel<float>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<G, kAsgWarps * 32, smem, st>>>(idx, val, n, m, m2, msq, K, prev, labels, d2min, bch, bmx, barg);
+    if (val_f64) {
+      if (K <= 8) launch_assign_kp<double, 8>(G, idx, val, n, m, tab, K, prev, labels, d2min, bch, bmx, barg, st);
+      else if (K <= 16) launch_assign_kp<double, 16>(G, idx, val, n, m, tab, K, prev, labels, d2min, bch, bmx, barg, st);
+      else launch_assign_kp<double, 32>(G, idx, val, n, m, tab, K, prev, labels, d2min, bch, bmx, barg, st);
+    } else {
+      if (K <= 8) launch_assign_kp<float, 8>(G, idx, val, n, m, tab, K, prev, labels, d2min, bch, bmx, barg, st);
+      else if (K <= 16) launch_assign_kp<float, 16>(G, idx, val, n, m, tab, K, prev, labels, d2min, bch, bmx, barg, st);
+      else launch_assign_kp<float, 32>(G, idx, val, n, m, tab, K, prev, labels, d2min, bch, bmx, barg, st);
+    }
     rc = check_launch("km_assign_kernel");
     if (rc) return rc;
   }
-  km_assign_reduce_kernel<<<1, 32, 0, st>>>(bch, bmx, barg, n > 0 ? G : 0, out, d2max);
+  km_assign_reduce_kernel<<<1, 1024, 0, st>>>(bch, bmx, barg, n > 0 ? G : 0, out, d2max);
   return check_launch("km_assign_reduce_kernel");
 }
 
@@ -256,16 +380,18 @@ constexpr int kPartWarps = 8;
 
 struct PartLayout {
   int64_t nblk, nchunk_max, ch;
-  size_t off_hist, off_base, off_perm, off_sizes, off_coff, off_chunks, off_psum, off_pcnt, total;
+  size_t off_hist, off_base, off_perm, off_sizes, off_coff, off_cfirst, off_chunks, off_psum, off_pcnt, total;
 };
 
 static PartLayout part_layout(int64_t n, int32_t p_pad, int32_t K) {
   PartLayout L{};
   L.nblk = (n + kSortBlock - 1) / kSortBlock;
   if (L.nblk < 1) L.nblk = 1;
-  int64_t ch = n / (4 * (int64_t)sm_count());
+  int64_t ch = n / (2 * (int64_t)sm_count());
+  const int64_t minch = (int64_t)32 * p_pad / 8;  // per-chunk setup ~ W*p words vs ch*m/32 work
+  if (ch < minch) ch = minch;
   if (ch < 512) ch = 512;
-  if (ch > 16384) ch = 16384;
+  if (ch > 32768) ch = 32768;
   L.ch = ch;
   L.nchunk_max = (n + ch - 1) / ch + K;
   size_t o = 0;
@@ -279,6 +405,7 @@ static PartLayout part_layout(int64_t n, int32_t p_pad, int32_t K) {
   L.off_perm = take((size_t)(n > 0 ? n : 1) * 4);
   L.off_sizes = take((size_t)K * 8);
   L.off_coff = take((size_t)(K + 1) * 8);
+  L.off_cfirst = take((size_t)(K + 1) * 8);
   L.off_chunks = take((size_t)L.nchunk_max * 16);
   L.off_psum = take((size_t)L.nchunk_max * p_pad * 8);
   L.off_pcnt = take((size_t)L.nchunk_max * p_pad * 4);
@@ -335,22 +462,58 @@ __global__ void km_scan_kernel(const int32_t* __restrict__ hist, int64_t nblk, i
   if (threadIdx.x == 0) sizes[k] = carry;
 }
 
-// cluster offsets and the chunk table (cluster-major, fixed chunk length)
+// cluster offsets, first chunk of each cluster, and the chunk table (cluster-major, fixed
+// chunk length). One block: a warp-cooperative scan over K, then every thread fills the
+// entries of its own clusters.
 __global__ void km_offsets_kernel(const int64_t* __restrict__ sizes, int K, int64_t ch, int64_t nchunk_max,
-                                  int64_t* __restrict__ coff, int64_t* __restrict__ chunks) {
-  if (threadIdx.x != 0) return;
-  int64_t off = 0, c = 0;
-  for (int k = 0; k < K; ++k) {
-    coff[k] = off;
-    for (int64_t s = 0; s < sizes[k]; s += ch) {
-      chunks[2 * c] = off + s;                                        // start in perm
-      chunks[2 * c + 1] = ((int64_t)k << 32) | (uint32_t)min(ch, sizes[k] - s);  // k | len
-      ++c;
-    }
-    off += sizes[k];
+                                  int64_t* __restrict__ coff, int64_t* __restrict__ cfirst,
+                                  int64_t* __restrict__ chunks) {
+  __shared__ int64_t carry_s, carry_c;
+  if (threadIdx.x == 0) {
+    carry_s = 0;
+    carry_c = 0;
   }
-  coff[K] = off;
-  for (; c < nchunk_max; ++c) {
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    for (int k0 = 0; k0 < K; k0 += 32) {
+      const int k = k0 + lane;
+      const int64_t sz = k < K ? sizes[k] : 0;
+      const int64_t nc = (sz + ch - 1) / ch;
+      int64_t is = sz, ic = nc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t ys = __shfl_up_sync(kFM, is, o), yc = __shfl_up_sync(kFM, ic, o);
+        if (lane >= o) {
+          is += ys;
+          ic += yc;
+        }
+      }
+      if (k < K) {
+        coff[k] = carry_s + is - sz;
+        cfirst[k] = carry_c + ic - nc;
+      }
+      __syncwarp();
+      if (lane == 31) {
+        carry_s += is;
+        carry_c += ic;
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      coff[K] = carry_s;
+      cfirst[K] = carry_c;
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    int64_t c = cfirst[k];
+    for (int64_t s0 = 0; s0 < sizes[k]; s0 += ch, ++c) {
+      chunks[2 * c] = coff[k] + s0;                                             // start in perm
+      chunks[2 * c + 1] = ((int64_t)k << 32) | (uint32_t)min(ch, sizes[k] - s0);  // k | len
+    }
+  }
+  for (int64_t c = cfirst[K] + threadIdx.x; c < nchunk_max; c += blockDim.x) {
     chunks[2 * c] = 0;
     chunks[2 * c + 1] = -1;
   }
@@ -427,18 +590,14 @@ __global__ void __launch_bounds__(kPartWarps * 32)
 
 // sums[j][k] / counts[j][k]: chunks of cluster k added in order
 __global__ void km_chunk_reduce_kernel(const double* __restrict__ psum, const int32_t* __restrict__ pcnt,
-                                       const int64_t* __restrict__ chunks, const int64_t* __restrict__ sizes,
-                                       int32_t p_pad, int K, int64_t ch, double* __restrict__ sums,
-                                       int64_t* __restrict__ counts) {
+                                       const int64_t* __restrict__ cfirst, int32_t p_pad, int K,
+                                       double* __restrict__ sums, int64_t* __restrict__ counts) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)p_pad * K) return;
   const int j = (int)(e / K), k = (int)(e % K);
-  int64_t c0 = 0;
-  for (int kk = 0; kk < k; ++kk) c0 += (sizes[kk] + ch - 1) / ch;
-  const int64_t nc = (sizes[k] + ch - 1) / ch;
   double s = 0.0;
   int64_t cnt = 0;
-  for (int64_t c = c0; c < c0 + nc; ++c) {
+  for (int64_t c = cfirst[k]; c < cfirst[k + 1]; ++c) {
     s = dadd(s, psum[(size_t)c * p_pad + j]);
     cnt += pcnt[(size_t)c * p_pad + j];
   }
@@ -455,6 +614,7 @@ int partials_launch(const int32_t* idx, const void* val, int val_f64, int64_t n,
   int64_t* base = reinterpret_cast<int64_t*>(w + L.off_base);
   int32_t* perm = reinterpret_cast<int32_t*>(w + L.off_perm);
   int64_t* coff = reinterpret_cast<int64_t*>(w + L.off_coff);
+  int64_t* cfirst = reinterpret_cast<int64_t*>(w + L.off_cfirst);
   int64_t* chunks = reinterpret_cast<int64_t*>(w + L.off_chunks);
   double* psum = reinterpret_cast<double*>(w + L.off_psum);
   int32_t* pcnt = reinterpret_cast<int32_t*>(w + L.off_pcnt);
@@ -469,7 +629,7 @@ int partials_launch(const int32_t* idx, const void* val, int val_f64, int64_t n,
   }
   km_scan_kernel<<<K, 256, 0, st>>>(hist, L.nblk, base, sizes);
   if ((rc = check_launch("km_scan_kernel"))) return rc;
-  km_offsets_kernel<<<1, 32, 0, st>>>(sizes, K, L.ch, L.nchunk_max, coff, chunks);
+  km_offsets_kernel<<<1, 1024, 0, st>>>(sizes, K, L.ch, L.nchunk_max, coff, cfirst, chunks);
   if ((rc = check_launch("km_offsets_kernel"))) return rc;
   if (n > 0) {
     const size_t ssm = (size_t)K * 8;
@@ -483,8 +643,8 @@ int partials_launch(const int32_t* idx, const void* val, int val_f64, int64_t n,
     if ((rc = check_launch("km_chunk_kernel"))) return rc;
   }
   const int64_t tot = (int64_t)p_pad * K;
-  km_chunk_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(psum, pcnt, chunks, sizes, p_pad, K, L.ch,
-                                                                          sums, counts);
+  km_chunk_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(psum, pcnt, cfirst, p_pad, K, sums,
+                                                                          counts);
   return check_launch("km_chunk_reduce_kernel");
 }
 
