@@ -122,8 +122,11 @@ class SketchKMeans:
                       out.data_ptr(), d2max.data_ptr(), ws.data_ptr(), ws.numel(), self._st())
 
     def objective(self, d2min: torch.Tensor, out: torch.Tensor) -> None:
+        L = _lib.lib()
+        ws = self._workspace("pairwise", L.skc_pairwise_sum_workspace(self.n))
         with torch.cuda.device(self.dev):
-            _lib.call("skc_pairwise_sum", d2min.data_ptr(), self.n, out.data_ptr(), 0, 0, self._st())
+            _lib.call("skc_pairwise_sum", d2min.data_ptr(), self.n, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                      self._st())
 
     def partials(self, labels: torch.Tensor, K: int):
         """cluster.py:189-208 partial sums: (sums, counts, sizes) on the device."""

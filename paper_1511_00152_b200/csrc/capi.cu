@@ -58,7 +58,8 @@ int signs_launch(uint64_t, int32_t, int32_t, double*, cudaStream_t);
 size_t assign_ws(int64_t, int32_t, int32_t);
 int assign_launch(const int32_t*, const void*, int, int64_t, int32_t, const double*, int32_t, int32_t, const int32_t*,
                   int32_t*, double*, int64_t*, double*, void*, cudaStream_t);
-int pairwise_launch(const double*, int64_t, double*, cudaStream_t);
+int pairwise_launch(const double*, int64_t, double*, void*, cudaStream_t);
+size_t pairwise_ws();
 size_t partials_ws(int64_t, int32_t, int32_t);
 int partials_check(int32_t, int32_t);
 int partials_launch(const int32_t*, const void*, int, int64_t, int32_t, const int32_t*, int32_t, int32_t, double*,
@@ -239,14 +240,13 @@ int skc_kmeans_assign(const int32_t* idx, const void* val, int32_t val_dtype, in
 
 size_t skc_pairwise_sum_workspace(int64_t n) {
   (void)n;
-  return 0;
+  return pairwise_ws();
 }
 
 int skc_pairwise_sum(const double* x, int64_t n, double* out, void* workspace, size_t ws_bytes, void* stream) {
-  (void)workspace;
-  (void)ws_bytes;
   if (n < 0) return fail(SKC_EDIM, "negative length");
-  return pairwise_launch(x, n, out, S(stream));
+  if (ws_bytes < pairwise_ws()) return fail(SKC_EPARAM, "workspace too small");
+  return pairwise_launch(x, n, out, workspace, S(stream));
 }
 
 size_t skc_kmeans_partials_workspace(int64_t n, int32_t m, int32_t p_pad, int32_t K) {

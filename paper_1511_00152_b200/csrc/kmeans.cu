@@ -46,36 +46,16 @@ __device__ double pw_rec(const double* a, int64_t n) {
   return dadd(pw_rec(a, n2), pw_rec(a + n2, n - n2));
 }
 
-// Same association as pw_rec: the top D levels of the recursion are split across 2^D
-// threads (each computes one subtree), then combined bottom-up level by level in parallel.
-// Node (d, path) keeps its value in slot path << (D - d), the slot of its leftmost leaf.
-constexpr int kPwDepth = 10;
+constexpr int kPwDeep = 14;  // subtrees at depth 14: one thread each, 64 blocks
 
-__device__ __forceinline__ int64_t pw_node_len(int64_t n, int d, int path, bool* leaf_above) {
-  // length of node (d, path); leaf_above = an ancestor (or itself before depth d) is a leaf
-  int64_t len = n;
-  *leaf_above = false;
-  for (int k = 0; k < d; ++k) {
-    if (len <= 128) {
-      *leaf_above = true;
-      return len;
-    }
-    int64_t n2 = len / 2;
-    n2 -= n2 % 8;
-    len = ((path >> (d - 1 - k)) & 1) ? len - n2 : n2;
-  }
-  return len;
-}
-
-__global__ void __launch_bounds__(1 << kPwDepth) pairwise_kernel(const double* __restrict__ x, int64_t n,
-                                                                  double* __restrict__ out) {
-  __shared__ double res[1 << kPwDepth];
-  const int t = threadIdx.x;
+__global__ void __launch_bounds__(256) pairwise_leaves_kernel(const double* __restrict__ x, int64_t n,
+                                                              double* __restrict__ res) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;  // path of depth kPwDeep
   int64_t off = 0, len = n;
   bool active = true;
-  for (int d = 0; d < kPwDepth; ++d) {
-    const int bit = (t >> (kPwDepth - 1 - d)) & 1;
-    if (len <= 128) {  // leaf above depth D: owned by the all-zero suffix path
+  for (int d = 0; d < kPwDeep; ++d) {
+    const int bit = (t >> (kPwDeep - 1 - d)) & 1;
+    if (len <= 128) {  // leaf above the split depth: owned by the all-zero suffix path
       if (bit) active = false;
       continue;
     }
@@ -89,24 +69,43 @@ __global__ void __launch_bounds__(1 << kPwDepth) pairwise_kernel(const double* _
     }
   }
   res[t] = active ? pw_rec(x + off, len) : 0.0;
-  __syncthreads();
-  for (int d = kPwDepth - 1; d >= 0; --d) {
-    if (t < (1 << d)) {
+}
+
+__global__ void __launch_bounds__(1024) pairwise_combine_kernel(double* __restrict__ res, int64_t n,
+                                                                double* __restrict__ out) {
+  for (int d = kPwDeep - 1; d >= 0; --d) {
+    for (int t = threadIdx.x; t < (1 << d); t += blockDim.x) {
       bool leaf_above;
-      const int64_t L = pw_node_len(n, d, t, &leaf_above);
-      if (!leaf_above && L > 128) {  // internal node: left + right child
-        const int sh = kPwDepth - d;
-        res[t << sh] = dadd(res[(2 * t) << (sh - 1)], res[(2 * t + 1) << (sh - 1)]);
+      int64_t L = n;
+      leaf_above = false;
+      for (int k = 0; k < d; ++k) {
+        if (L <= 128) {
+          leaf_above = true;
+          break;
+        }
+        int64_t n2 = L / 2;
+        n2 -= n2 % 8;
+        L = ((t >> (d - 1 - k)) & 1) ? L - n2 : n2;
+      }
+      if (!leaf_above && L > 128) {
+        const int sh = kPwDeep - d;
+        res[(size_t)t << sh] = dadd(res[(size_t)(2 * t) << (sh - 1)], res[(size_t)(2 * t + 1) << (sh - 1)]);
       }
     }
     __syncthreads();
   }
-  if (t == 0) out[0] = res[0];
+  if (threadIdx.x == 0) out[0] = res[0];
 }
 
-int pairwise_launch(const double* x, int64_t n, double* out, cudaStream_t st) {
-  pairwise_kernel<<<1, 1 << kPwDepth, 0, st>>>(x, n, out);
-  return check_launch("pairwise_kernel");
+size_t pairwise_ws() { return ((size_t)1 << kPwDeep) * sizeof(double); }
+
+int pairwise_launch(const double* x, int64_t n, double* out, void* ws, cudaStream_t st) {
+  double* res = reinterpret_cast<double*>(ws);
+  pairwise_leaves_kernel<<<(1 << kPwDeep) / 256, 256, 0, st>>>(x, n, res);
+  int rc = check_launch("pairwise_leaves_kernel");
+  if (rc) return rc;
+  pairwise_combine_kernel<<<1, 1024, 0, st>>>(res, n, out);
+  return check_launch("pairwise_combine_kernel");
 }
 
 // ---------------------------------------------------------------------------------
@@ -124,32 +123,46 @@ __global__ void km_tables2_kernel(const double* __restrict__ mu, int64_t total, 
 // A warp holds G = 32/KP points; lane = g*KP + k. For K > KP the lane loops over k += KP.
 // colsq: numpy pairwise order on 8 lanes of the group (m <= 128), else pw_rec on one lane.
 // d2[k] = sum_t v_t*(-2 mu[j_t,k]) then + sum_t mu[j_t,k]^2 (csr_matvecs axpy order) + colsq.
-template <typename V, int KP>
-__global__ void __launch_bounds__(kAsgWarps * 32)
+// SMEM_TAB: the packed (p, K) table is staged in shared memory (small p*K, e.g. C2).
+template <typename V, int KP, bool SMEM_TAB>
+__global__ void __launch_bounds__(kAsgWarps * 32, 4)
     km_assign_kernel(const int32_t* __restrict__ idx, const void* __restrict__ val, int64_t n, int m,
-                     const double2* __restrict__ tab, int K, const int32_t* __restrict__ prev,
+                     const double2* __restrict__ gtab, int K, int p_pad, const int32_t* __restrict__ prev,
                      int32_t* __restrict__ labels, double* __restrict__ d2min, int64_t* __restrict__ blk_changed,
                      double* __restrict__ blk_max, int64_t* __restrict__ blk_arg) {
   constexpr int G = 32 / KP;
-  extern __shared__ unsigned char sm[];
+  extern __shared__ __align__(16) unsigned char sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane / KP, k0 = lane % KP;
-  int* sidx = reinterpret_cast<int*>(sm) + (size_t)warp * G * m;
-  double* sval = reinterpret_cast<double*>(sm + (((size_t)kAsgWarps * G * m * 4 + 15) & ~(size_t)15)) +
-                 (size_t)warp * G * m;
+  // layout: [table (SMEM_TAB)] [per warp: sidx G*m int | sval G*m double | msq 32*m double]
+  size_t off = 0;
+  const double2* tab = gtab;
+  if constexpr (SMEM_TAB) {
+    double2* st = reinterpret_cast<double2*>(sm);
+    for (int e = threadIdx.x; e < p_pad * K; e += blockDim.x) st[e] = gtab[e];
+    tab = st;
+    off = (size_t)p_pad * K * 16;
+    __syncthreads();
+  }
+  const size_t per_warp = ((size_t)G * m * 4 + 15) / 16 * 16 + (size_t)G * m * 8;
+  unsigned char* wb = sm + off + per_warp * warp;
+  int* sidx = reinterpret_cast<int*>(wb);  // row offsets j*K
+  double* sval = reinterpret_cast<double*>(wb + ((size_t)G * m * 4 + 15) / 16 * 16);
   int64_t changed = 0;
   double bmax = -1.0;
   int64_t barg = -1;
-  const int64_t gw = (int64_t)blockIdx.x * kAsgWarps + warp, nw = (int64_t)gridDim.x * kAsgWarps;
+  const int nwarps = blockDim.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * nwarps + warp, nw = (int64_t)gridDim.x * nwarps;
   for (int64_t i0 = gw * G; i0 < n; i0 += nw * G) {
     __syncwarp();
-    for (int e = lane; e < G * m; e += 32) {
-      const int gg = e / m, t = e - gg * m;
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
       const int64_t i = i0 + gg;
-      if (i < n) {
-        sidx[gg * m + t] = __ldg(idx + i * m + t);
-        sval[gg * m + t] = ldd<V>(val, i * m + t);
-      }
+      if (i < n)
+        for (int t = lane; t < m; t += 32) {
+          sidx[gg * m + t] = __ldg(idx + i * m + t) * K;
+          sval[gg * m + t] = ldd<V>(val, i * m + t);
+        }
     }
     __syncwarp();
     const int64_t i = i0 + g;
@@ -168,16 +181,16 @@ __global__ void __launch_bounds__(kAsgWarps * 32)
       }
       // ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)) across lanes k0 = 0..7 of the group
       const double r1 = __shfl_down_sync(kFM, r, 1, KP);
-      const double s01 = dadd(r, r1);                       // valid at k0 = 0,2,4,6
+      const double s01 = dadd(r, r1);
       const double s23 = __shfl_down_sync(kFM, s01, 2, KP);
-      const double q = dadd(s01, s23);                      // valid at k0 = 0,4
+      const double q = dadd(s01, s23);
       const double q2 = __shfl_down_sync(kFM, q, 4, KP);
       if (k0 == 0) {
         colsq = dadd(q, q2);
         for (int t = m - (m % 8); t < m; ++t) colsq = dadd(colsq, dmul(sv[t], sv[t]));
       }
     } else if (k0 == 0) {
-      double* tmp = const_cast<double*>(sv);  // square in place (the row is re-staged next time)
+      double* tmp = const_cast<double*>(sv);  // square in place, restore after
       for (int t = 0; t < m; ++t) tmp[t] = dmul(sv[t], sv[t]);
       colsq = pw_rec(tmp, m);
       for (int t = 0; t < m; ++t) tmp[t] = ldd<V>(val, i * m + t);
@@ -191,26 +204,27 @@ __global__ void __launch_bounds__(kAsgWarps * 32)
       double v = __longlong_as_double(0x7FF0000000000000LL);
       int kk = 0x7FFFFFFF;
       if (k < K && i < n) {
+        const double2* tk = tab + k;
         double acc = 0.0;
         int t = 0;
+        const double* tkx = reinterpret_cast<const double*>(tk);
         for (; t + 4 <= m; t += 4) {
-          const double2 a0 = __ldg(tab + (int64_t)si[t] * K + k), a1 = __ldg(tab + (int64_t)si[t + 1] * K + k);
-          const double2 a2 = __ldg(tab + (int64_t)si[t + 2] * K + k), a3 = __ldg(tab + (int64_t)si[t + 3] * K + k);
-          acc = dadd(acc, dmul(sv[t], a0.x));
-          acc = dadd(acc, dmul(sv[t + 1], a1.x));
-          acc = dadd(acc, dmul(sv[t + 2], a2.x));
-          acc = dadd(acc, dmul(sv[t + 3], a3.x));
+          const double a0 = tkx[2 * si[t]], a1 = tkx[2 * si[t + 1]], a2 = tkx[2 * si[t + 2]], a3 = tkx[2 * si[t + 3]];
+          acc = dadd(acc, dmul(sv[t], a0));
+          acc = dadd(acc, dmul(sv[t + 1], a1));
+          acc = dadd(acc, dmul(sv[t + 2], a2));
+          acc = dadd(acc, dmul(sv[t + 3], a3));
         }
-        for (; t < m; ++t) acc = dadd(acc, dmul(sv[t], __ldg(tab + (int64_t)si[t] * K + k).x));
+        for (; t < m; ++t) acc = dadd(acc, dmul(sv[t], tkx[2 * si[t]]));
         for (t = 0; t + 4 <= m; t += 4) {
-          const double b0 = __ldg(tab + (int64_t)si[t] * K + k).y, b1 = __ldg(tab + (int64_t)si[t + 1] * K + k).y;
-          const double b2 = __ldg(tab + (int64_t)si[t + 2] * K + k).y, b3 = __ldg(tab + (int64_t)si[t + 3] * K + k).y;
+          const double b0 = tkx[2 * si[t] + 1], b1 = tkx[2 * si[t + 1] + 1], b2 = tkx[2 * si[t + 2] + 1],
+                       b3 = tkx[2 * si[t + 3] + 1];
           acc = dadd(acc, b0);
           acc = dadd(acc, b1);
           acc = dadd(acc, b2);
           acc = dadd(acc, b3);
         }
-        for (; t < m; ++t) acc = dadd(acc, __ldg(tab + (int64_t)si[t] * K + k).y);
+        for (; t < m; ++t) acc = dadd(acc, tkx[2 * si[t] + 1]);
         v = dadd(acc, colsq);
         kk = k;
       }
@@ -262,7 +276,7 @@ __global__ void __launch_bounds__(kAsgWarps * 32)
   if (threadIdx.x == 0) {
     int64_t c = 0, a = -1;
     double mx = -1.0;
-    for (int w = 0; w < kAsgWarps; ++w) {
+    for (int w = 0; w < nwarps; ++w) {
       c += s_ch[w];
       if (s_arg[w] >= 0 && (s_mx[w] > mx || (s_mx[w] == mx && (a < 0 || s_arg[w] < a)))) {
         mx = s_mx[w];
@@ -335,13 +349,24 @@ size_t assign_ws(int64_t n, int32_t p_pad, int32_t K) {
 
 template <typename V, int KP>
 static void launch_assign_kp(int G, const int32_t* idx, const void* val, int64_t n, int32_t m, const double2* tab,
-                             int32_t K, const int32_t* prev, int32_t* labels, double* d2min, int64_t* bch,
-                             double* bmx, int64_t* barg, cudaStream_t st) {
+                             int32_t K, int32_t p_pad, const int32_t* prev, int32_t* labels, double* d2min,
+                             int64_t* bch, double* bmx, int64_t* barg, cudaStream_t st) {
   constexpr int GP = 32 / KP;
-  const size_t smem = (((size_t)kAsgWarps * GP * m * 4 + 15) & ~(size_t)15) + (size_t)kAsgWarps * GP * m * 8;
-  auto k = km_assign_kernel<V, KP>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k<<<G, kAsgWarps * 32, smem, st>>>(idx, val, n, m, tab, K, prev, labels, d2min, bch, bmx, barg);
+  const size_t per_warp = ((size_t)GP * m * 4 + 15) / 16 * 16 + (size_t)GP * m * 8;
+  const size_t tab_bytes = (size_t)p_pad * K * 16;
+  int warps = kAsgWarps;
+  while (warps > 1 && per_warp * warps > 50 * 1024) warps >>= 1;  // 4 CTAs per SM
+  if (tab_bytes + per_warp * warps <= 50 * 1024) {
+    auto k = km_assign_kernel<V, KP, true>;
+    const size_t smem = tab_bytes + per_warp * warps;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<G, warps * 32, smem, st>>>(idx, val, n, m, tab, K, p_pad, prev, labels, d2min, bch, bmx, barg);
+  } else {
+    auto k = km_assign_kernel<V, KP, false>;
+    const size_t smem = per_warp * warps;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<G, warps * 32, smem, st>>>(idx, val, n, m, tab, K, p_pad, prev, labels, d2min, bch, bmx, barg);
+  }
 }
 
 int assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, const double* mu,
@@ -358,13 +383,13 @@ int assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, i
   if (rc) return rc;
   if (n > 0) {
     if (val_f64) {
-      if (K <= 8) launch_assign_kp<double, 8>(G, idx, val, n, m, tab, K, prev, labels, d2min, bch, bmx, barg, st);
-      else if (K <= 16) launch_assign_kp<double, 16>(G, idx, val, n, m, tab, K, prev, labels, d2min, bch, bmx, barg, st);
-      else launch_assign_kp<double, 32>(G, idx, val, n, m, tab, K, prev, labels, d2min, bch, bmx, barg, st);
+      if (K <= 8) launch_assign_kp<double, 8>(G, idx, val, n, m, tab, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);
+      else if (K <= 16) launch_assign_kp<double, 16>(G, idx, val, n, m, tab, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);
+      else launch_assign_kp<double, 32>(G, idx, val, n, m, tab, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);
     } else {
-      if (K <= 8) launch_assign_kp<float, 8>(G, idx, val, n, m, tab, K, prev, labels, d2min, bch, bmx, barg, st);
-      else if (K <= 16) launch_assign_kp<float, 16>(G, idx, val, n, m, tab, K, prev, labels, d2min, bch, bmx, barg, st);
-      else launch_assign_kp<float, 32>(G, idx, val, n, m, tab, K, prev, labels, d2min, bch, bmx, barg, st);
+      if (K <= 8) launch_assign_kp<float, 8>(G, idx, val, n, m, tab, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);
+      else if (K <= 16) launch_assign_kp<float, 16>(G, idx, val, n, m, tab, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);
+      else launch_assign_kp<float, 32>(G, idx, val, n, m, tab, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);
     }
     rc = check_launch("km_assign_kernel");
     if (rc) return rc;
@@ -564,7 +589,38 @@ __global__ void __launch_bounds__(kPartWarps * 32)
   }
   __syncwarp();
   const int q0 = len * warp / kPartWarps, q1 = len * (warp + 1) / kPartWarps;
-  for (int q = q0; q < q1; ++q) {
+  int q = q0;
+  if (m <= 64) {  // batches of 4 points: perm and row loads issued before the updates
+    for (; q + 4 <= q1; q += 4) {
+      int64_t pi[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) pi[b] = perm[start + q + b];
+      int jj[4][2];
+      double vv[4][2];
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int c2 = 0; c2 < 2; ++c2) {
+          const int t = lane + 32 * c2;
+          jj[b][c2] = -1;
+          if (t < m) {
+            jj[b][c2] = __ldg(idx + pi[b] * m + t);
+            vv[b][c2] = ldd<V>(val, pi[b] * m + t);
+          }
+        }
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+#pragma unroll
+        for (int c2 = 0; c2 < 2; ++c2)
+          if (jj[b][c2] >= 0) {
+            ws[jj[b][c2]] = dadd(ws[jj[b][c2]], vv[b][c2]);
+            wc[jj[b][c2]] += 1;
+          }
+        __syncwarp();
+      }
+    }
+  }
+  for (; q < q1; ++q) {
     const int64_t i = perm[start + q];
     for (int t = lane; t < m; t += 32) {
       const int j = __ldg(idx + i * m + t);
