@@ -269,101 +269,105 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
 
   const int64_t g0 = P.n * group / P.groups, g1 = P.n * (group + 1) / P.groups;
   const V* val = reinterpret_cast<const V*>(P.val);
-  // register prefetch of the first two 32-column chunks (covers m <= 64 fully)
-  int pj0 = 0x7FFFFFFF, pj1 = 0x7FFFFFFF;
+  const uint32_t lo_sh = (uint32_t)__cvta_generic_to_shared(lo);
+  // running row pointers; lanes hold columns lane and lane + 32 of the row (clamped loads
+  // stay inside the row, lanes past m are masked by a sentinel index)
+  const int64_t stride = (int64_t)kCovWarps * m;
+  const int32_t* ip = P.idx + (g0 + warp) * (int64_t)m;
+  const V* vp = val + (g0 + warp) * (int64_t)m;
+  const int cl0 = min(lane, m - 1), cl1 = min(lane + 32, m - 1);
+  const bool has0 = lane < m, has1 = lane + 32 < m;
+  int pj0 = 0, pj1 = 0;
   V pv0 = 0, pv1 = 0;
-  auto prefetch = [&](int64_t r) {
-    pj0 = pj1 = 0x7FFFFFFF;
-    if (r < g1) {
-      if (lane < m) {
-        pj0 = __ldg(P.idx + r * m + lane);
-        pv0 = __ldg(val + r * m + lane);
-      }
-      if (lane + 32 < m) {
-        pj1 = __ldg(P.idx + r * m + lane + 32);
-        pv1 = __ldg(val + r * m + lane + 32);
-      }
-    }
-  };
-  prefetch(g0 + warp);
+  if (g0 + warp < g1) {
+    pj0 = __ldg(ip + cl0);
+    pj1 = __ldg(ip + cl1);
+    pv0 = __ldg(vp + cl0);
+    pv1 = __ldg(vp + cl1);
+  }
+  // per-warp staging, 4*m words: the flat path uses int2 T[m] = (shared byte address of
+  // row t's entries, w_t * 2^S) and U[m] = (4 * b_u, w_u); the general path [sidx][sval]
+  int2* T = reinterpret_cast<int2*>(sidx);
+  int2* U = T + m;
   for (int64_t r = g0 + warp; r < g1; r += kCovWarps) {
-    const int j0 = pj0, j1 = pj1;
+    const int j0 = has0 ? pj0 : 0x7FFFFFFF, j1 = has1 ? pj1 : 0x7FFFFFFF;
     const float v0 = (float)pv0, v1 = (float)pv1;
-    prefetch(r + kCovWarps);
+    const int32_t* ir = ip;
+    const V* vr = vp;
+    ip += stride;
+    vp += stride;
+    if (r + kCovWarps < g1) {
+      pj0 = __ldg(ip + cl0);
+      pj1 = __ldg(ip + cl1);
+      pv0 = __ldg(vp + cl0);
+      pv1 = __ldg(vp + cl1);
+    }
     int nlo = __popc(__ballot_sync(kFullMask, j0 < r0)) + __popc(__ballot_sync(kFullMask, j1 < r0));
     int nhi = __popc(__ballot_sync(kFullMask, j0 < r1)) + __popc(__ballot_sync(kFullMask, j1 < r1));
-    bool big = (lane < m && fabsf(v0) > ftau) || (lane + 32 < m && fabsf(v1) > ftau);
-    for (int t0 = 64; t0 < m; t0 += 32) {  // columns beyond the prefetched two chunks
+    bool big = (has0 && fabsf(v0) > ftau) || (has1 && fabsf(v1) > ftau);
+    for (int t0 = 64; t0 < m; t0 += 32) {  // columns beyond the two register chunks
       const int t = t0 + lane;
-      const int j = t < m ? __ldg(P.idx + r * m + t) : 0x7FFFFFFF;
-      if (t < m) big |= fabsf((float)__ldg(val + r * m + t)) > ftau;
+      const int j = t < m ? __ldg(ir + t) : 0x7FFFFFFF;
+      if (t < m) big |= fabsf((float)__ldg(vr + t)) > ftau;
       nlo += __popc(__ballot_sync(kFullMask, j < r0));
       nhi += __popc(__ballot_sync(kFullMask, j < r1));
     }
     if (nlo == nhi) continue;  // none of this row's indices fall in the band
     const bool any_big = __any_sync(kFullMask, big);
-    if (!any_big) {
-      // flat enumeration of the visit's pairs {(t, u): nlo <= t < nhi, t <= u < m}:
-      // f = O(t - nlo) + (u - t) with O(x) = x*(m - nlo) - x*(x-1)/2; lanes take f = lane + 32k
-      // and invert O with the quadratic formula. Row data is staged as packed pairs:
-      // T[t] = (base_t, w_t * 2^S) and U[u] = (b_u, w_u).
-      int2* T = reinterpret_cast<int2*>(sidx);  // per-warp staging: 2*m words for T, 2*m for U
-      int2* U = T + m;
-      for (int t = lane; t < m; t += 32) {
-        int jt;
-        float vt;
-        if (t < 32) {
-          jt = j0;
-          vt = v0;
-        } else if (t < 64) {
-          jt = j1;
-          vt = v1;
-        } else {
-          jt = __ldg(P.idx + r * m + t);
-          vt = (float)__ldg(val + r * m + t);
-        }
-        U[t] = make_int2(jt, __float_as_int(vt));
-        if (t >= nlo && t < nhi) T[t] = make_int2(rowbase[jt - r0], __float_as_int(vt * scale_a));
-      }
+    if (!any_big && m <= 64) {
+      // flat enumeration of the visit's pairs {(t, u): nlo <= t < nhi, t <= u < m}. Row x of
+      // the trapezoid (t = nlo + x) has length mn - x; folding row x with row h-1-x gives a
+      // rectangle of floor(h/2) rows of Lp = 2 mn - h + 1 (plus a half row when h is odd).
+      // Lane f -> rr = floor((f + 0.5) / Lp) by an approximate reciprocal (the fraction
+      // stays >= 1/(2 Lp) > 2^-9, far above the rounding error), c = f - rr * Lp, and
+      //   c <  mn - rr: t = nlo + rr,        u = t + c
+      //   otherwise:    t = nhi - 1 - rr,    u = c + nhi - 1 - mn
+      if (has0) U[lane] = make_int2(j0 << 2, __float_as_int(v0));
+      if (has1) U[lane + 32] = make_int2(j1 << 2, __float_as_int(v1));
+      if (lane >= nlo && lane < nhi)
+        T[lane] = make_int2((int)lo_sh + 4 * rowbase[j0 - r0], __float_as_int(v0 * scale_a));
+      if (lane + 32 >= nlo && lane + 32 < nhi)
+        T[lane + 32] = make_int2((int)lo_sh + 4 * rowbase[j1 - r0], __float_as_int(v1 * scale_a));
       __syncwarp();
-      // fold row i with row h-1-i (lengths add up to Lp): the trapezoid becomes a rectangle
-      // of floor(h/2) rows of Lp, plus a half row when h is odd; f -> (r, c) by one reciprocal
-      // multiply ((f + 0.5) / Lp keeps a fractional part >= 2^-8, so fp32 floor is exact)
-      const int h = nhi - nlo;
-      const int Lp = 2 * (m - nlo) - h + 1;
-      const int F = h * (m - nlo) - h * (h - 1) / 2;
-      const float inv = 1.0f / (float)Lp;
-      for (int f = lane; f < F; f += 32) {
-        const int rr = (int)(((float)f + 0.5f) * inv);
+      const int h = nhi - nlo, mn = m - nlo;
+      const int Lp = 2 * mn - h + 1;
+      const int F = h * mn - (h * (h - 1) >> 1);
+      float inv;
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"((float)Lp));
+      const int kB = nhi - 1 - mn, tB = nhi - 1;
+      float ff = (float)lane + 0.5f;
+      for (int f = lane; f < F; f += 32, ff += 32.0f) {
+        const int rr = (int)(ff * inv);
         const int c = f - rr * Lp;
-        const int Lr = m - nlo - rr;  // length of row nlo + rr
-        const bool first = c < Lr;
-        const int t = first ? nlo + rr : nhi - 1 - rr;
-        const int u = t + (first ? c : c - Lr);
+        const bool first = c + rr < mn;
+        const int x = nlo + rr;
+        const int t = first ? x : tB - rr;
+        const int u = c + (first ? x : kB);
         const int2 tt = T[t], uu = U[u];
-        const int e = tt.x + uu.x;
+        const uint32_t addr = (uint32_t)(tt.x + uu.x);
         const int q = __float2int_rn(__int_as_float(tt.y) * __int_as_float(uu.y));
-        const uint32_t old = atomicAdd(lo + e, (uint32_t)q);
+        uint32_t old;
+        asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"((uint32_t)q) : "memory");
         if ((old + (uint32_t)q < old) != (q < 0))  // carry (q >= 0) / borrow (q < 0): rare
-          atomicAdd(part + e, (unsigned long long)((long long)(q < 0 ? -1 : 1) << 32));
+          atomicAdd(part + ((addr - lo_sh) >> 2), (unsigned long long)((long long)(q < 0 ? -1 : 1) << 32));
       }
       __syncwarp();
       continue;
     }
     // general path (m > 64, or a value above tau): stage the row in shared memory
-    if (lane < m) {
+    if (has0) {
       sidx[lane] = j0;
       sval[lane] = v0 * scale_a;
     }
-    if (lane + 32 < m) {
+    if (has1) {
       sidx[lane + 32] = j1;
       sval[lane + 32] = v1 * scale_a;
     }
     for (int t0 = 64; t0 < m; t0 += 32) {
       const int t = t0 + lane;
       if (t < m) {
-        sidx[t] = __ldg(P.idx + r * m + t);
-        sval[t] = (float)__ldg(val + r * m + t) * scale_a;
+        sidx[t] = __ldg(ir + t);
+        sval[t] = (float)__ldg(vr + t) * scale_a;
       }
     }
     __syncwarp();
@@ -373,7 +377,7 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
         const int tmax = min(nhi, c0 + 32);  // rows t <= u within this chunk
         if (nlo >= tmax) continue;
         const int bu = u < m ? sidx[u] : 0;
-        const float vu = u < m ? (c0 == 0 ? v0 : (c0 == 32 ? v1 : (float)__ldg(val + r * m + u))) : 0.f;
+        const float vu = u < m ? (c0 == 0 ? v0 : (c0 == 32 ? v1 : (float)__ldg(vr + u))) : 0.f;
         for (int t = nlo; t < tmax; ++t) {
           const int base = rowbase[sidx[t] - r0];
           const float va = sval[t];
@@ -389,10 +393,10 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
     } else {
       // a value above tau: exact fp64 product, scaled, straight to the int64 partial
       for (int t = nlo; t < nhi; ++t) {
-        const double va = (double)__ldg(val + r * m + t);
+        const double va = (double)__ldg(vr + t);
         const int base = rowbase[sidx[t] - r0];
         for (int u = t + lane; u < m; u += 32) {
-          const long long q = __double2ll_rn(dmul(dmul(va, (double)__ldg(val + r * m + u)), full_s));
+          const long long q = __double2ll_rn(dmul(dmul(va, (double)__ldg(vr + u)), full_s));
           atomicAdd(part + base + sidx[u], (unsigned long long)q);
         }
       }
