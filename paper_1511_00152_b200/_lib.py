@@ -15,7 +15,8 @@ import torch
 from .errors import DeviceError, DimensionError, ParameterError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "_lib", "libsketchcu.so")
+# SKC_LIB selects an alternative build of the same library (kernel A/B experiments)
+SO_PATH = os.environ.get("SKC_LIB") or os.path.join(_HERE, "_lib", "libsketchcu.so")
 
 SKC_OK, SKC_EDIM, SKC_EPARAM, SKC_ECUDA = 0, 1, 2, 3
 KIND_CODES = {"hadamard": 0, "dct": 1, "none": 2}

@@ -2,6 +2,7 @@
 // K4 covariance finalize, K7 adjoint transform (mean / PCs / centres).
 // Reference: estimators.py:30-66, transform.py:153-200.
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -270,41 +271,30 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
   const int64_t g0 = P.n * group / P.groups, g1 = P.n * (group + 1) / P.groups;
   const V* val = reinterpret_cast<const V*>(P.val);
   const uint32_t lo_sh = (uint32_t)__cvta_generic_to_shared(lo);
-  // running row pointers; lanes hold columns lane and lane + 32 of the row (clamped loads
-  // stay inside the row, lanes past m are masked by a sentinel index)
+  // lanes hold columns lane and lane + 32 of a row; the next row loads into registers
+  // while the warp processes the current one (a two-set ping-pong measured slower: code size)
   const int64_t stride = (int64_t)kCovWarps * m;
-  const int32_t* ip = P.idx + (g0 + warp) * (int64_t)m;
-  const V* vp = val + (g0 + warp) * (int64_t)m;
-  const int cl0 = min(lane, m - 1), cl1 = min(lane + 32, m - 1);
+  const int32_t* ip = P.idx + (g0 + warp) * (int64_t)m + lane;  // lane's column in the row
+  const V* vp = val + (g0 + warp) * (int64_t)m + lane;
   const bool has0 = lane < m, has1 = lane + 32 < m;
-  int pj0 = 0, pj1 = 0;
-  V pv0 = 0, pv1 = 0;
-  if (g0 + warp < g1) {
-    pj0 = __ldg(ip + cl0);
-    pj1 = __ldg(ip + cl1);
-    pv0 = __ldg(vp + cl0);
-    pv1 = __ldg(vp + cl1);
-  }
+  int aj0 = 0x7FFFFFFF, aj1 = 0x7FFFFFFF;
+  V av0 = 0, av1 = 0;
+  auto load = [&](int64_t r, const int32_t* ipr, const V* vpr, int& j0, int& j1, V& v0, V& v1) {
+    if (r < g1) {
+      if (has0) j0 = __ldg(ipr), v0 = __ldg(vpr);
+      if (has1) j1 = __ldg(ipr + 32), v1 = __ldg(vpr + 32);
+    }
+  };
   // per-warp staging, 4*m words: the flat path uses int2 T[m] = (shared byte address of
   // row t's entries, w_t * 2^S) and U[m] = (4 * b_u, w_u); the general path [sidx][sval]
   int2* T = reinterpret_cast<int2*>(sidx);
   int2* U = T + m;
-  for (int64_t r = g0 + warp; r < g1; r += kCovWarps) {
-    const int j0 = has0 ? pj0 : 0x7FFFFFFF, j1 = has1 ? pj1 : 0x7FFFFFFF;
-    const float v0 = (float)pv0, v1 = (float)pv1;
-    const int32_t* ir = ip;
-    const V* vr = vp;
-    ip += stride;
-    vp += stride;
-    if (r + kCovWarps < g1) {
-      pj0 = __ldg(ip + cl0);
-      pj1 = __ldg(ip + cl1);
-      pv0 = __ldg(vp + cl0);
-      pv1 = __ldg(vp + cl1);
-    }
+  auto visit = [&](const int64_t r, const int j0, const int j1, const float v0, const float v1) {
+    const int32_t* ir = P.idx + r * m;  // the row, for columns >= 64 and the general path
+    const V* vr = val + r * m;
     int nlo = __popc(__ballot_sync(kFullMask, j0 < r0)) + __popc(__ballot_sync(kFullMask, j1 < r0));
     int nhi = __popc(__ballot_sync(kFullMask, j0 < r1)) + __popc(__ballot_sync(kFullMask, j1 < r1));
-    bool big = (has0 && fabsf(v0) > ftau) || (has1 && fabsf(v1) > ftau);
+    bool big = fabsf(v0) > ftau || fabsf(v1) > ftau;  // lanes past m hold 0
     for (int t0 = 64; t0 < m; t0 += 32) {  // columns beyond the two register chunks
       const int t = t0 + lane;
       const int j = t < m ? __ldg(ir + t) : 0x7FFFFFFF;
@@ -312,7 +302,7 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
       nlo += __popc(__ballot_sync(kFullMask, j < r0));
       nhi += __popc(__ballot_sync(kFullMask, j < r1));
     }
-    if (nlo == nhi) continue;  // none of this row's indices fall in the band
+    if (nlo == nhi) return;  // none of this row's indices fall in the band
     const bool any_big = __any_sync(kFullMask, big);
     if (!any_big && m <= 64) {
       // flat enumeration of the visit's pairs {(t, u): nlo <= t < nhi, t <= u < m}. Row x of
@@ -332,6 +322,7 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
       const int h = nhi - nlo, mn = m - nlo;
       const int Lp = 2 * mn - h + 1;
       const int F = h * mn - (h * (h - 1) >> 1);
+      // rr = floor((f + 0.5) / Lp) in fp32 (an IMAD.HI magic-number division measured slower)
       float inv;
       asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"((float)Lp));
       const int kB = nhi - 1 - mn, tB = nhi - 1;
@@ -352,7 +343,7 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
           atomicAdd(part + ((addr - lo_sh) >> 2), (unsigned long long)((long long)(q < 0 ? -1 : 1) << 32));
       }
       __syncwarp();
-      continue;
+      return;
     }
     // general path (m > 64, or a value above tau): stage the row in shared memory
     if (has0) {
@@ -402,6 +393,17 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
       }
     }
     __syncwarp();
+  };
+  int64_t r = g0 + warp;
+  load(r, ip, vp, aj0, aj1, av0, av1);
+  while (r < g1) {
+    const int j0 = aj0, j1 = aj1;
+    const float v0 = (float)av0, v1 = (float)av1;
+    ip += stride;
+    vp += stride;
+    load(r + kCovWarps, ip, vp, aj0, aj1, av0, av1);
+    visit(r, j0, j1, v0, v1);
+    r += kCovWarps;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < ne; e += blockDim.x) {
@@ -442,9 +444,8 @@ size_t cov_ws(int64_t n, int32_t m, int32_t p_pad) {
   return (size_t)g * tri_off(p_pad, p_pad) * sizeof(unsigned long long);
 }
 
-int cov_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, int32_t p_pad,
-               const double* stats, double* tri, void* ws, cudaStream_t st) {
-  if (n == 0) return SKC_OK;
+static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, int32_t p_pad,
+                           const double* stats, double* tri, void* ws, cudaStream_t st) {
   CovParams H;
   const int cap = band_capacity(m, p_pad);
   H.nbands = make_bands(p_pad, cap, H.band_rows);
@@ -473,6 +474,22 @@ int cov_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int3
   if (rc) return rc;
   cov_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(H.part, H.groups, total, m, stats, tri);
   return check_launch("cov_reduce_kernel");
+}
+
+int cov_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, int32_t p_pad,
+               const double* stats, double* tri, void* ws, cudaStream_t st) {
+  // the kernel addresses a group's rows with 32-bit element offsets: split huge inputs
+  const int groups = cov_groups(make_bands(p_pad, band_capacity(m, p_pad), nullptr), n);
+  int64_t max_rows = (int64_t)groups * ((((int64_t)1 << 31) / m) - kCovWarps);
+  if (const char* e = getenv("SKC_COV_SPLIT_ROWS")) max_rows = atoll(e) > 0 ? atoll(e) : max_rows;  // tests
+  const size_t vsz = val_f64 ? 8 : 4;
+  for (int64_t r0 = 0; r0 < n; r0 += max_rows) {
+    const int64_t c = n - r0 < max_rows ? n - r0 : max_rows;
+    const int rc = cov_launch_part(idx + r0 * m, static_cast<const char*>(val) + (size_t)(r0 * m) * vsz, val_f64, c,
+                                   m, p_pad, stats, tri, ws, st);
+    if (rc) return rc;
+  }
+  return SKC_OK;
 }
 
 // ======================================================================================

@@ -253,6 +253,22 @@ def test_covariance_heavy_tails_and_determinism(skc):
     assert rel_fro(C1, Co) < 1e-6
 
 
+def test_covariance_split_launches(skc, monkeypatch):
+    # inputs beyond 2^31 elements per row group run as several launches; force the split
+    # on a small input (fixed-point sums per launch, fp64 sum of launches: 1e-12)
+    rng = np.random.default_rng(12)
+    p, n = 256, 9000
+    X = rng.standard_normal((p, n)).astype(np.float32)
+    spec = skc.PreconditionSpec.create("hadamard", p, 5)
+    sk = skc.sketch_stream(X, spec, skc.SamplingPlan(6, p, 20), compute="f32")
+    C1 = skc.estimate_covariance(sk).matrix
+    monkeypatch.setenv("SKC_COV_SPLIT_ROWS", "2500")
+    C2 = skc.estimate_covariance(sk).matrix
+    assert rel_fro(C2, C1) < 1e-12
+    Co = O.estimate_covariance(sk.host_indices(), sk.host_values().astype(np.float64), p, nthreads=8)
+    assert rel_fro(C2, Co) < 1e-6
+
+
 # ---------------------------------------------------------------- L3b K-means
 @pytest.mark.parametrize("name", ["c2", "c5", "small", "empty"])
 @pytest.mark.parametrize("compute", ["f64"])
