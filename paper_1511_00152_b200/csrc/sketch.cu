@@ -15,7 +15,8 @@
 //            _hash.py:46-56) and keeps the high word only for a threshold test, as a
 //            per-lane bitmask. Pass 2 re-hashes the ~m+5sqrt(m) candidates in full into
 //            a per-warp list. An exact bucket select finds the m smallest keys
-//            (sketch.py:53-56), and a row-ballot loop emits them in ascending index order.
+//            (sketch.py:53-56); the kept set becomes a row bitmask, and each lane emits
+//            its rows' elements at prefix-sum slots in ascending index order.
 #include <math.h>
 
 #include "common.cuh"
@@ -125,6 +126,12 @@ __device__ __forceinline__ void wht_all_windows(T* xs, const uint32_t* sgn, T sc
 
 // ------------------------------------------------------------------------------------
 // phase 3 helpers
+// per-warp scratch: keys [cap] u64, bucket keys [32] u64, histogram [32], kept-row
+// bitmask [P/32] u32, candidate indices [cap] u16 (16-byte multiple)
+template <int LOGP>
+__host__ __device__ constexpr size_t warp_bytes(int cap) {
+  return ((size_t)cap * 10 + 256 + 128 + 4 * (((1 << LOGP) + 31) / 32) + 15) & ~(size_t)15;
+}
 __device__ __forceinline__ uint64_t key_of(uint64_t ci, int j) { return mix64(ci + kGamma * (uint64_t)(j + 1)); }
 
 // High 32 bits of mix64(z) before its last xor-shift: for t <= 2^31,
@@ -134,21 +141,6 @@ __device__ __forceinline__ uint32_t mix64_hi_pre(uint64_t z) {
   z = (z ^ (z >> 30)) * kMix1;
   z = z ^ (z >> 27);
   return (uint32_t)((z * kMix2) >> 32);
-}
-
-// 32x32 bit-matrix transpose across a warp: lane i holds row i (bit r = M[i][r]); returns
-// column `lane` (bit i = M[i][lane]). Recursive block swap, 5 shuffle stages.
-__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
-#pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    const int sh = 16 >> k;
-    const uint32_t m = masks[k];
-    const uint32_t y = __shfl_xor_sync(kFull, x, sh);
-    x = (lane & sh) ? ((x & ~m) | ((y & ~m) >> sh)) : ((x & m) | ((y & m) << sh));
-  }
-  return x;
 }
 
 template <typename T>
@@ -193,7 +185,7 @@ __device__ void emit_slow_exact(const SketchParams& P, const T* xs, int s, int64
 
 template <int LOGP, typename T>
 __device__ void sample_one(const SketchParams& P, const T* xs, int s, int64_t row, uint64_t* ck, uint16_t* cj,
-                           uint64_t* memk, int* hist) {
+                           uint64_t* memk, int* hist, uint32_t* rmask) {
   const int lane = threadIdx.x & 31;
   if (P.mode == kFullSet) {  // m == p: SamplingPlan shortcut, sketch.py:51-52
     for (int j = lane; j < P.pk; j += 32) {
@@ -259,26 +251,27 @@ __device__ void sample_one(const SketchParams& P, const T* xs, int s, int64_t ro
     emit_slow_exact<LOGP, T>(P, xs, s, row, ci);
     return;
   }
-  // pass 2: full keys of the candidates (unordered list)
+  // pass 2: candidate indices (each lane fills its slots [off, off + mine)), then full keys
+  // and the bucket histogram, lane-strided over the list
   {
     int q = off;
 #pragma unroll
     for (int w = 0; w < MW; ++w)
-      for (uint32_t b = cm[w]; b; b &= b - 1, ++q) {
-        const int j = 32 * (32 * w + __ffs(b) - 1) + lane;
-        ck[q] = key_of(ci, j);
-        cj[q] = (uint16_t)j;
-      }
+      for (uint32_t b = cm[w]; b; b &= b - 1, ++q) cj[q] = (uint16_t)(32 * (32 * w + __ffs(b) - 1) + lane);
+  }
+  const bool sel = count > P.m;
+  // 32 key-monotone buckets over [0, t_hi * 2^32)
+  const float bscale = P.t_all ? 32.0f / 4294967296.0f : 32.0f / (float)P.t_hi;
+  if (sel) hist[lane] = 0;
+  __syncwarp();
+  for (int q = lane; q < count; q += 32) {
+    const uint64_t key = key_of(ci, cj[q]);
+    ck[q] = key;
+    if (sel) atomicAdd(&hist[min(31, (int)((float)(uint32_t)(key >> 32) * bscale))], 1);
   }
   __syncwarp();
   uint64_t kth = ~0ull;
-  if (count > P.m) {
-    // 32 key-monotone buckets over [0, t_hi * 2^32)
-    hist[lane] = 0;
-    __syncwarp();
-    const float bscale = P.t_all ? 32.0f / 4294967296.0f : 32.0f / (float)P.t_hi;
-    for (int q = lane; q < count; q += 32) atomicAdd(&hist[min(31, (int)((float)(uint32_t)(ck[q] >> 32) * bscale))], 1);
-    __syncwarp();
+  if (sel) {
     const int h = hist[lane];
     int incl = h;
 #pragma unroll
@@ -313,23 +306,26 @@ __device__ void sample_one(const SketchParams& P, const T* xs, int s, int64_t ro
     const uint32_t hit = __ballot_sync(kFull, lane < hB && rank == r - 1);
     kth = __shfl_sync(kFull, mk, __ffs(hit) - 1);
   }
-  // kept mask: re-read this lane's candidates
-  uint32_t km[MW];
-  {
-    int q = off;
-#pragma unroll
-    for (int w = 0; w < MW; ++w) {
-      km[w] = 0;
-      for (uint32_t b = cm[w]; b; b &= b - 1, ++q) km[w] |= (uint32_t)(ck[q] <= kth) << (__ffs(b) - 1);
+  // kept set as a row bitmask: bit (j & 31) of word (j >> 5)
+  for (int q = lane; q < count; q += 32) {
+    if (ck[q] <= kth) {
+      const int j = cj[q];
+      atomicOr(&rmask[j >> 5], 1u << (j & 31));
     }
   }
-  // emit in ascending j = 32 r + lane: transpose the kept bit-matrix (lane i, bit r) so lane r
-  // holds row r's lane mask, prefix the row counts, then each kept element finds its slot.
+  __syncwarp();
+  // emit in ascending j: lane owns rows 32 w + lane; a prefix of the row counts gives each
+  // row's first slot, then the lane writes its row's kept elements in bit order
   const int64_t orow = row * P.m;
   int wbase = 0;
 #pragma unroll
   for (int w = 0; w < MW; ++w) {
-    const uint32_t t = warp_transpose32(km[w]);  // lane r: bit i = element (32 (32 w + r) + i) kept
+    const int rr = 32 * w + lane;
+    uint32_t t = 0;
+    if (rr < rows) {
+      t = rmask[rr];
+      rmask[rr] = 0;  // clean for the warp's next sample
+    }
     const int cnt = __popc(t);
     int incl = cnt;
 #pragma unroll
@@ -337,22 +333,11 @@ __device__ void sample_one(const SketchParams& P, const T* xs, int s, int64_t ro
       const int y = __shfl_up_sync(kFull, incl, o);
       if (lane >= o) incl += y;
     }
-    const int excl = incl - cnt;
-    // shuffles need converged lanes: one round per kept element of the busiest lane
-    int mx = __popc(km[w]);
-    mx = __reduce_max_sync(kFull, mx);
-    uint32_t b = km[w];
-    for (int k = 0; k < mx; ++k) {
-      const int r = b ? __ffs(b) - 1 : 0;
-      const uint32_t tr = __shfl_sync(kFull, t, r);
-      const int er = __shfl_sync(kFull, excl, r);
-      if (b) {
-        const int j = 32 * (32 * w + r) + lane;
-        const int64_t pos = orow + wbase + er + __popc(tr & lanemask_lt());
-        P.idx_out[pos] = j;
-        if (P.val_out) store_val<T>(P.val_out, pos, y_at<LOGP, T>(xs, s, j), P.val_f64);
-        b &= b - 1;
-      }
+    int64_t pos = orow + wbase + incl - cnt;
+    for (; t; t &= t - 1, ++pos) {
+      const int j = 32 * rr + __ffs(t) - 1;
+      P.idx_out[pos] = j;
+      if (P.val_out) store_val<T>(P.val_out, pos, y_at<LOGP, T>(xs, s, j), P.val_f64);
     }
     wbase += __shfl_sync(kFull, incl, 31);
   }
@@ -369,12 +354,15 @@ __global__ void __launch_bounds__(kThreads, 3) sketch_kernel(const SketchParams 
   uint32_t* sgn = reinterpret_cast<uint32_t*>(smem + sizeof(T) * ((G::WORDS + 1) & ~1));
   unsigned char* wbase = reinterpret_cast<unsigned char*>(sgn) + 4 * ((kSignWords + 3) & ~3);
   const int warp = threadIdx.x >> 5;
-  const size_t per_warp = (size_t)P.cap * 10 + 32 * 8 + 32 * 4;
+  constexpr int kRowWords = (G::P + 31) / 32;  // kept-set bitmask words
+  const size_t per_warp = warp_bytes<LOGP>(P.cap);
   unsigned char* mine = wbase + per_warp * warp;
   uint64_t* ck = reinterpret_cast<uint64_t*>(mine);
   uint64_t* memk = reinterpret_cast<uint64_t*>(mine + (size_t)P.cap * 8);
   int* hist = reinterpret_cast<int*>(mine + (size_t)P.cap * 8 + 256);
-  uint16_t* cj = reinterpret_cast<uint16_t*>(mine + (size_t)P.cap * 8 + 256 + 128);
+  uint32_t* rmask = reinterpret_cast<uint32_t*>(mine + (size_t)P.cap * 8 + 256 + 128);
+  uint16_t* cj = reinterpret_cast<uint16_t*>(mine + (size_t)P.cap * 8 + 256 + 128 + 4 * kRowWords);
+  for (int i = threadIdx.x & 31; i < kRowWords; i += 32) rmask[i] = 0;
 
   const bool has_x = P.X != nullptr;
   if (has_x && P.use_signs) {  // D diagonal, _hash.py:38-43, regenerated per CTA
@@ -444,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 3) sketch_kernel(const SketchParams 
       for (int s = warp; s < G::S; s += kWarps) {
         const int64_t row = row0 + s;
         if (row >= P.n) break;
-        sample_one<LOGP, T>(P, xs, s, row, ck, cj, memk, hist);
+        sample_one<LOGP, T>(P, xs, s, row, ck, cj, memk, hist, rmask);
       }
     }
   }
@@ -455,8 +443,7 @@ template <int LOGP, typename T>
 static int launch_sketch_t(SketchParams P, cudaStream_t st) {
   using G = Geo<LOGP>;
   const size_t sign_bytes = 4 * (((G::P + 31) / 32 + 3) & ~3);
-  const size_t per_warp = (size_t)P.cap * 10 + 32 * 8 + 32 * 4;
-  const size_t smem = sizeof(T) * ((G::WORDS + 1) & ~1) + sign_bytes + per_warp * kWarps;
+  const size_t smem = sizeof(T) * ((G::WORDS + 1) & ~1) + sign_bytes + warp_bytes<LOGP>(P.cap) * kWarps;
   auto kern = sketch_kernel<LOGP, T>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return check_launch("sketch smem attribute");
