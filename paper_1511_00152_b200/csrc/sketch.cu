@@ -19,6 +19,8 @@
 //            its rows' elements at prefix-sum slots in ascending index order.
 #include <math.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace skc {
@@ -74,6 +76,32 @@ struct Geo {
 };
 
 // ------------------------------------------------------------------------------------
+// packed fp32 pairs (sm_100 FADD2 / FMUL2)
+__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void unpack2(uint64_t x, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(x));
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// ------------------------------------------------------------------------------------
 // phase 2: one window of the WHT for one (sample, thread) item
 template <int LOGP, typename T, int K>
 __device__ __forceinline__ void wht_window(T* xs, const uint32_t* sgn, int s, int u, T scale) {
@@ -94,21 +122,58 @@ __device__ __forceinline__ void wht_window(T* xs, const uint32_t* sgn, int s, in
       for (int e = 0; e < G::E; ++e) v[e] = A::flip(v[e], (bits >> e) & 1u);
     }
   }
+  if constexpr (std::is_same<T, float>::value && G::E >= 4) {
+    // fp32: stages with h >= 2 run on packed pairs (v[e], v[e+1]) with FADD2; each lane is
+    // an IEEE add/sub/mul with round-to-nearest, so results equal the scalar order exactly
+    uint64_t w[G::E / 2];
 #pragma unroll
-  for (int b = first; b < bk + G::LOGE; ++b) {
-    const int h = 1 << (b - bk);
+    for (int k = 0; k < G::E / 2; ++k) w[k] = pack2(v[2 * k], v[2 * k + 1]);
 #pragma unroll
-    for (int e = 0; e < G::E; ++e) {
-      if ((e & h) == 0) {
-        const T a = v[e], c = v[e + h];
-        v[e] = A::add(a, c);
-        v[e + h] = A::sub(a, c);
+    for (int b = first; b < bk + G::LOGE; ++b) {
+      const int h = 1 << (b - bk);
+      if (h == 1) {
+#pragma unroll
+        for (int k = 0; k < G::E / 2; ++k) {
+          float a, c;
+          unpack2(w[k], a, c);
+          w[k] = pack2(fadd(a, c), fsub(a, c));
+        }
+      } else {
+        const int hp = h >> 1;
+#pragma unroll
+        for (int k = 0; k < G::E / 2; ++k) {
+          if (((2 * k) & h) == 0) {
+            const uint64_t x = w[k], y = w[k + hp];
+            w[k] = add2(x, y);
+            w[k + hp] = sub2(x, y);
+          }
+        }
       }
     }
-  }
-  if constexpr (K == G::NWIN - 1) {
+    if constexpr (K == G::NWIN - 1) {
+      const uint64_t sc = pack2(scale, scale);
 #pragma unroll
-    for (int e = 0; e < G::E; ++e) v[e] = A::mul(v[e], scale);
+      for (int k = 0; k < G::E / 2; ++k) w[k] = mul2(w[k], sc);
+    }
+#pragma unroll
+    for (int k = 0; k < G::E / 2; ++k) unpack2(w[k], v[2 * k], v[2 * k + 1]);
+  } else {
+#pragma unroll
+    for (int b = first; b < bk + G::LOGE; ++b) {
+      const int h = 1 << (b - bk);
+#pragma unroll
+      for (int e = 0; e < G::E; ++e) {
+        if ((e & h) == 0) {
+          const T a = v[e], c = v[e + h];
+          v[e] = A::add(a, c);
+          v[e + h] = A::sub(a, c);
+        }
+      }
+    }
+    if constexpr (K == G::NWIN - 1) {
+#pragma unroll
+      for (int e = 0; e < G::E; ++e) v[e] = A::mul(v[e], scale);
+    }
   }
 #pragma unroll
   for (int e = 0; e < G::E; ++e) base[G::addr(e << bk)] = v[e];
