@@ -373,10 +373,8 @@ __device__ void sample_one(const SketchParams& P, const T* xs, int s, int64_t ro
   }
   // kept set as a row bitmask: bit (j & 31) of word (j >> 5)
   for (int q = lane; q < count; q += 32) {
-    if (ck[q] <= kth) {
-      const int j = cj[q];
-      atomicOr(&rmask[j >> 5], 1u << (j & 31));
-    }
+    const int j = cj[q];
+    atomicOr(&rmask[j >> 5], (uint32_t)(ck[q] <= kth) << (j & 31));
   }
   __syncwarp();
   // emit in ascending j: lane owns rows 32 w + lane; a prefix of the row counts gives each
@@ -449,21 +447,25 @@ __global__ void __launch_bounds__(kThreads, 3) sketch_kernel(const SketchParams 
       // ---- phase 1: load (zero pad p..p_pad and rows >= n) ----
       if (P.vec && !P.x_f64) {
         constexpr int NV = kTileElems / 4 / kThreads;
+        // thread t loads 16 bytes at element f = 4 (t + k kThreads) of the tile: sample
+        // s_k = f >> LOGP, column i_k = f & (P-1). Both are compile-time offsets from k = 0.
+        const int f0 = threadIdx.x * 4;
+        const int s0 = f0 >> LOGP, i0 = f0 & (G::P - 1);
+        const float* xb = reinterpret_cast<const float*>(P.X) + (row0 + s0) * P.ld + i0;
+        const int64_t rows_left = P.n - row0;
         float4 buf[NV];
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
-          const int f = (threadIdx.x + k * kThreads) * 4;
-          const int s = f >> LOGP, i = f & (G::P - 1);
-          const int64_t row = row0 + s;
-          buf[k] = row < P.n ? __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(P.X) +
-                                                                    row * P.ld + i))
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
+          const int f = f0 + k * kThreads * 4;  // s_k - s0 and i_k - i0 fold to constants
+          const int sk = f >> LOGP, ik = f & (G::P - 1);
+          buf[k] = sk < rows_left ? __ldg(reinterpret_cast<const float4*>(xb + (sk - s0) * P.ld + (ik - i0)))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
-          const int f = (threadIdx.x + k * kThreads) * 4;
-          const int s = f >> LOGP, i = f & (G::P - 1);
-          T* d = xs + s * G::SP + G::addr(i);  // 4 consecutive i never cross a 32-row
+          const int f = f0 + k * kThreads * 4;
+          const int sk = f >> LOGP, ik = f & (G::P - 1);
+          T* d = xs + sk * G::SP + G::addr(ik);  // 4 consecutive i never cross a 32-row
           d[0] = (T)buf[k].x;
           d[1] = (T)buf[k].y;
           d[2] = (T)buf[k].z;
