@@ -63,10 +63,15 @@ struct Geo {
   static constexpr int S = kTileElems / P;
   static constexpr int NWIN = LOGE == 0 ? 1 : (LOGP + LOGE - 1) / LOGE;
   static constexpr int ITEMS = S * L;
-  static constexpr int SP = LOGP < 5 ? P : (P / 32) * 33;  // words per sample
+  // Padded layout: each 32-element row of a sample takes 36 words, and consecutive samples
+  // sit SP words apart with SP = 4 (mod 32). Rows start 16-byte aligned, so 4-element
+  // groups move as single 16-byte copies and vector LDS/STS. Every window access below is
+  // bank-conflict-free, including windows whose lanes span several samples.
+  static constexpr int SP0 = LOGP < 5 ? P : (P / 32) * 36;
+  static constexpr int SP = LOGP < 5 ? P : SP0 + ((4 - SP0 % 32) + 32) % 32;  // words per sample
   static constexpr int WORDS = S * SP;
   // padded address of element i (linear over disjoint bit sets of i)
-  static __host__ __device__ constexpr int addr(int i) { return LOGP < 5 ? i : i + (i >> 5); }
+  static __host__ __device__ constexpr int addr(int i) { return LOGP < 5 ? i : i + 4 * (i >> 5); }
   static __host__ __device__ constexpr int bk(int k) { return (k * LOGE < LOGP - LOGE) ? k * LOGE : LOGP - LOGE; }
   // the thread bits of window k: u fills every index bit outside [bk, bk+LOGE)
   static __device__ __forceinline__ int u_part(int k, int u) {
@@ -111,8 +116,22 @@ __device__ __forceinline__ void wht_window(T* xs, const uint32_t* sgn, int s, in
   constexpr int first = K * G::LOGE;  // first stage bit not yet applied
   T* base = xs + s * G::SP + G::addr(G::u_part(K, u));
   T v[G::E];
+  // window 0 of a padded layout reads E = 32 consecutive, 16-byte aligned elements
+  using V16 = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  constexpr int PER = 16 / sizeof(T);
+  constexpr bool kVec = bk == 0 && G::E == 32;
+  if constexpr (kVec) {
 #pragma unroll
-  for (int e = 0; e < G::E; ++e) v[e] = base[G::addr(e << bk)];
+    for (int c = 0; c < G::E / PER; ++c) {
+      const V16 t = reinterpret_cast<const V16*>(base)[c];
+      const T* tp = reinterpret_cast<const T*>(&t);
+#pragma unroll
+      for (int q = 0; q < PER; ++q) v[c * PER + q] = tp[q];
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < G::E; ++e) v[e] = base[G::addr(e << bk)];
+  }
   if constexpr (K == 0) {
     if (sgn != nullptr) {
       // window 0 holds elements [u*E, u*E + E): E consecutive bits of the sign mask
@@ -175,8 +194,19 @@ __device__ __forceinline__ void wht_window(T* xs, const uint32_t* sgn, int s, in
       for (int e = 0; e < G::E; ++e) v[e] = A::mul(v[e], scale);
     }
   }
+  if constexpr (kVec) {
 #pragma unroll
-  for (int e = 0; e < G::E; ++e) base[G::addr(e << bk)] = v[e];
+    for (int c = 0; c < G::E / PER; ++c) {
+      V16 t;
+      T* tp = reinterpret_cast<T*>(&t);
+#pragma unroll
+      for (int q = 0; q < PER; ++q) tp[q] = v[c * PER + q];
+      reinterpret_cast<V16*>(base)[c] = t;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < G::E; ++e) base[G::addr(e << bk)] = v[e];
+  }
 }
 
 template <int LOGP, typename T, int K>
@@ -193,9 +223,15 @@ __device__ __forceinline__ void wht_all_windows(T* xs, const uint32_t* sgn, T sc
 // phase 3 helpers
 // per-warp scratch: keys [cap] u64, bucket keys [32] u64, histogram [32], kept-row
 // bitmask [P/32] u32, candidate indices [cap] u16 (16-byte multiple)
+// The kept-set masks of all the warp's samples in a tile stay live from selection (before
+// the transform) to emission (after it): max(P/32, 32) words for P >= 32.
+template <int LOGP>
+__host__ __device__ constexpr int mask_words() {
+  return LOGP < 5 ? 1 : ((1 << LOGP) / 32 > 32 ? (1 << LOGP) / 32 : 32);
+}
 template <int LOGP>
 __host__ __device__ constexpr size_t warp_bytes(int cap) {
-  return ((size_t)cap * 10 + 256 + 128 + 4 * (((1 << LOGP) + 31) / 32) + 15) & ~(size_t)15;
+  return ((size_t)cap * 10 + 256 + 128 + 4 * mask_words<LOGP>() + 15) & ~(size_t)15;
 }
 __device__ __forceinline__ uint64_t key_of(uint64_t ci, int j) { return mix64(ci + kGamma * (uint64_t)(j + 1)); }
 
@@ -248,25 +284,25 @@ __device__ void emit_slow_exact(const SketchParams& P, const T* xs, int s, int64
   }
 }
 
-template <int LOGP, typename T>
-__device__ void sample_one(const SketchParams& P, const T* xs, int s, int64_t row, uint64_t* ck, uint16_t* cj,
-                           uint64_t* memk, int* hist, uint32_t* rmask) {
+__device__ __forceinline__ uint64_t column_state(const SketchParams& P, int64_t row) {
+  return mix64(P.s_tag + kGamma * (uint64_t)(P.col0 + row + 1));  // _hash.py:54
+}
+
+// Selection for one sample (needs no sample data): sets the kept set in rmask, bit
+// (j & 31) of word (j >> 5). Returns false when the sample must take the exact slow path.
+template <int LOGP>
+__device__ bool select_one(const SketchParams& P, int64_t row, uint64_t* ck, uint16_t* cj, uint64_t* memk,
+                           int* hist, uint32_t* rmask) {
   const int lane = threadIdx.x & 31;
+  const int rows = (P.pk + 31) >> 5;  // key rows: j = 32 r + lane
   if (P.mode == kFullSet) {  // m == p: SamplingPlan shortcut, sketch.py:51-52
-    for (int j = lane; j < P.pk; j += 32) {
-      const int64_t pos = row * P.m + j;
-      P.idx_out[pos] = j;
-      if (P.val_out) store_val<T>(P.val_out, pos, y_at<LOGP, T>(xs, s, j), P.val_f64);
-    }
-    return;
+    for (int r = lane; r < rows; r += 32) rmask[r] = P.pk - 32 * r >= 32 ? kFull : (1u << (P.pk - 32 * r)) - 1u;
+    __syncwarp();
+    return true;
   }
-  const uint64_t ci = mix64(P.s_tag + kGamma * (uint64_t)(P.col0 + row + 1));  // _hash.py:54
-  if (P.mode == kSlowExact) {
-    emit_slow_exact<LOGP, T>(P, xs, s, row, ci);
-    return;
-  }
+  if (P.mode == kSlowExact) return false;
+  const uint64_t ci = column_state(P, row);
   constexpr int MW = (Geo<LOGP>::P + 1023) / 1024;  // mask words: bit r of word w <-> j = 32 (32 w + r) + lane
-  const int rows = (P.pk + 31) >> 5;                   // key rows: j = 32 r + lane
   // pass 1: threshold bitmask
   uint32_t cm[MW];
 #pragma unroll
@@ -312,10 +348,7 @@ __device__ void sample_one(const SketchParams& P, const T* xs, int s, int64_t ro
   }
   const int count = __shfl_sync(kFull, off, 31);
   off -= mine;
-  if (count < P.m || count > P.cap) {
-    emit_slow_exact<LOGP, T>(P, xs, s, row, ci);
-    return;
-  }
+  if (count < P.m || count > P.cap) return false;
   // pass 2: candidate indices (each lane fills its slots [off, off + mine)), then full keys
   // and the bucket histogram, lane-strided over the list
   {
@@ -347,10 +380,7 @@ __device__ void sample_one(const SketchParams& P, const T* xs, int s, int64_t ro
     const int B = __ffs(__ballot_sync(kFull, incl >= P.m)) - 1;
     const int hB = __shfl_sync(kFull, h, B);
     const int r = P.m - __shfl_sync(kFull, incl - h, B);  // keep the r smallest of bucket B
-    if (hB > 32) {
-      emit_slow_exact<LOGP, T>(P, xs, s, row, ci);
-      return;
-    }
+    if (hB > 32) return false;
     int nb = 0;
     for (int q0 = 0; q0 < count; q0 += 32) {
       const int q = q0 + lane;
@@ -377,8 +407,21 @@ __device__ void sample_one(const SketchParams& P, const T* xs, int s, int64_t ro
     atomicOr(&rmask[j >> 5], (uint32_t)(ck[q] <= kth) << (j & 31));
   }
   __syncwarp();
-  // emit in ascending j: lane owns rows 32 w + lane; a prefix of the row counts gives each
-  // row's first slot, then the lane writes its row's kept elements in bit order
+  return true;
+}
+
+// Emit one sample's kept set in ascending j: lane owns rows 32 w + lane; a prefix of the row
+// counts gives each row's first slot, then the lane writes its row's kept elements in bit
+// order and clears the row for the next sample.
+template <int LOGP, typename T>
+__device__ void emit_one(const SketchParams& P, const T* xs, int s, int64_t row, uint32_t* rmask, bool ok) {
+  const int lane = threadIdx.x & 31;
+  if (!ok) {
+    emit_slow_exact<LOGP, T>(P, xs, s, row, column_state(P, row));
+    return;
+  }
+  constexpr int MW = (Geo<LOGP>::P + 1023) / 1024;
+  const int rows = (P.pk + 31) >> 5;
   const int64_t orow = row * P.m;
   int wbase = 0;
 #pragma unroll
@@ -417,7 +460,8 @@ __global__ void __launch_bounds__(kThreads, 3) sketch_kernel(const SketchParams 
   uint32_t* sgn = reinterpret_cast<uint32_t*>(smem + sizeof(T) * ((G::WORDS + 1) & ~1));
   unsigned char* wbase = reinterpret_cast<unsigned char*>(sgn) + 4 * ((kSignWords + 3) & ~3);
   const int warp = threadIdx.x >> 5;
-  constexpr int kRowWords = (G::P + 31) / 32;  // kept-set bitmask words
+  constexpr int kRowWords = mask_words<LOGP>();  // kept-set bitmask words
+  constexpr int kSlot = LOGP < 5 ? 1 : G::P / 32;  // mask words per sample
   const size_t per_warp = warp_bytes<LOGP>(P.cap);
   unsigned char* mine = wbase + per_warp * warp;
   uint64_t* ck = reinterpret_cast<uint64_t*>(mine);
@@ -440,23 +484,45 @@ __global__ void __launch_bounds__(kThreads, 3) sketch_kernel(const SketchParams 
   }
   const T scale = (T)(1.0 / sqrt((double)G::P));  // transform.py:170
 
+  // P >= 32: a warp selects all its samples of the tile while the tile's 16-byte copies
+  // are in flight (the selection needs no data), then the CTA transforms and emits
+  constexpr bool kEarly = LOGP >= 5;
+  const bool async_load = has_x && std::is_same<T, float>::value && P.vec && !P.x_f64 && LOGP >= 2;
+  const bool sampling = P.mode != kNoSample;
   for (int64_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
     const int64_t row0 = tile * G::S;
-    __syncthreads();  // previous tile's phase 3 is done with xs; signs visible
+    const int64_t rows_left = P.n - row0;
+    __syncthreads();  // previous tile's emission is done with xs; signs visible
     if (has_x) {
       // ---- phase 1: load (zero pad p..p_pad and rows >= n) ----
-      if (P.vec && !P.x_f64) {
+      if (async_load) {
+        // thread t copies 16 bytes at element f = 4 (t + k kThreads) of the tile: sample
+        // s_k = f >> LOGP, column i_k = f & (P-1), compile-time offsets from k = 0
         constexpr int NV = kTileElems / 4 / kThreads;
-        // thread t loads 16 bytes at element f = 4 (t + k kThreads) of the tile: sample
-        // s_k = f >> LOGP, column i_k = f & (P-1). Both are compile-time offsets from k = 0.
         const int f0 = threadIdx.x * 4;
         const int s0 = f0 >> LOGP, i0 = f0 & (G::P - 1);
         const float* xb = reinterpret_cast<const float*>(P.X) + (row0 + s0) * P.ld + i0;
-        const int64_t rows_left = P.n - row0;
+        const uint32_t dst0 = (uint32_t)__cvta_generic_to_shared(xs);
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          const int f = f0 + k * kThreads * 4;
+          const int sk = f >> LOGP, ik = f & (G::P - 1);
+          const bool ok = sk < rows_left;
+          const float* src = ok ? xb + (sk - s0) * P.ld + (ik - i0) : reinterpret_cast<const float*>(P.X);
+          const uint32_t dst = dst0 + 4u * (uint32_t)(sk * G::SP + G::addr(ik));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0)
+                       : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      } else if (P.vec && !P.x_f64) {
+        constexpr int NV = kTileElems / 4 / kThreads;
+        const int f0 = threadIdx.x * 4;
+        const int s0 = f0 >> LOGP, i0 = f0 & (G::P - 1);
+        const float* xb = reinterpret_cast<const float*>(P.X) + (row0 + s0) * P.ld + i0;
         float4 buf[NV];
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
-          const int f = f0 + k * kThreads * 4;  // s_k - s0 and i_k - i0 fold to constants
+          const int f = f0 + k * kThreads * 4;
           const int sk = f >> LOGP, ik = f & (G::P - 1);
           buf[k] = sk < rows_left ? __ldg(reinterpret_cast<const float4*>(xb + (sk - s0) * P.ld + (ik - i0)))
                                   : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -483,6 +549,16 @@ __global__ void __launch_bounds__(kThreads, 3) sketch_kernel(const SketchParams 
           xs[s * G::SP + G::addr(i)] = v;
         }
       }
+    }
+    // ---- phase 3a: selection (one warp per sample) ----
+    uint32_t okbits = 0;
+    if (kEarly && sampling) {
+      int k = 0;
+      for (int s = warp; s < G::S && s < rows_left; s += kWarps, ++k)
+        okbits |= (uint32_t)select_one<LOGP>(P, row0 + s, ck, cj, memk, hist, rmask + k * kSlot) << k;
+    }
+    if (has_x) {
+      if (async_load) asm volatile("cp.async.wait_all;" ::: "memory");
       __syncthreads();
       // ---- phase 2: D then WHT then scale ----
       wht_all_windows<LOGP, T, 0>(xs, P.use_signs ? sgn : nullptr, scale);
@@ -494,12 +570,13 @@ __global__ void __launch_bounds__(kThreads, 3) sketch_kernel(const SketchParams 
         }
       }
     }
-    // ---- phase 3: sample + emit, one warp per sample ----
-    if (P.mode != kNoSample) {
-      for (int s = warp; s < G::S; s += kWarps) {
-        const int64_t row = row0 + s;
-        if (row >= P.n) break;
-        sample_one<LOGP, T>(P, xs, s, row, ck, cj, memk, hist, rmask);
+    // ---- phase 3b: emit, one warp per sample ----
+    if (sampling) {
+      int k = 0;
+      for (int s = warp; s < G::S && s < rows_left; s += kWarps, ++k) {
+        uint32_t* rm = rmask + (kEarly ? k * kSlot : 0);
+        const bool ok = kEarly ? (okbits >> k) & 1u : select_one<LOGP>(P, row0 + s, ck, cj, memk, hist, rm);
+        emit_one<LOGP, T>(P, xs, s, row0 + s, rm, ok);
       }
     }
   }
