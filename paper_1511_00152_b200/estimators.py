@@ -21,7 +21,7 @@ import torch
 from . import _lib
 from .errors import ParameterError
 from .sketch import SparseSketch
-from .transform import u64, unprecondition
+from .transform import default_device, u64, unprecondition
 
 SYMMETRY_RTOL = 1e-9
 
@@ -110,8 +110,29 @@ def estimate_covariance(sketch: SparseSketch) -> CovarianceEstimate:
     return CovarianceEstimate(matrix=C.cpu().numpy(), n_used=sketch.n, device_matrix=C)
 
 
-def top_eigenvectors(C, k: int) -> np.ndarray:
-    """Host eigensolve (north star: the top-k eigensolve stays on the host); estimators.py:69-81"""
+def top_eigenvectors(C, k: int, solver: str = "host"):
+    """Eigenvectors of the k largest eigenvalues as columns; estimators.py:69-81.
+
+    ``solver="host"`` (default) runs LAPACK ``eigh`` through numpy, exactly as the reference.
+    ``solver="device"`` keeps C on the GPU and runs cuSOLVER ``syevd`` (``torch.linalg.eigh``),
+    returning a CUDA tensor: the same eigenpairs up to each vector's sign, within the
+    eigensolver's rounding. Both check symmetry as the reference does.
+    """
+    if solver not in ("host", "device"):
+        raise ParameterError(f"unknown solver {solver!r}")
+    if solver == "device":
+        Cd = C if isinstance(C, torch.Tensor) else torch.as_tensor(np.asarray(C, dtype=np.float64))
+        Cd = Cd.to(dtype=torch.float64, device=Cd.device if Cd.is_cuda else default_device())
+        if Cd.ndim != 2 or Cd.shape[0] != Cd.shape[1]:
+            raise ParameterError("expected a square matrix")
+        p = Cd.shape[0]
+        if not 1 <= k <= p:
+            raise ParameterError(f"need 1 <= k <= {p}, got {k}")
+        scale = max(float(Cd.abs().max()), 1e-300)
+        if float((Cd - Cd.T).abs().max()) > SYMMETRY_RTOL * scale:
+            raise ParameterError("matrix is not symmetric within tolerance")
+        _, V = torch.linalg.eigh(0.5 * (Cd + Cd.T))
+        return V.flip(1)[:, :k].contiguous()
     C = C.cpu().numpy() if isinstance(C, torch.Tensor) else np.asarray(C, dtype=np.float64)
     if C.ndim != 2 or C.shape[0] != C.shape[1]:
         raise ParameterError("expected a square matrix")
@@ -125,12 +146,19 @@ def top_eigenvectors(C, k: int) -> np.ndarray:
     return V[:, ::-1][:, :k]
 
 
-def principal_components(sketch: SparseSketch, k: int) -> np.ndarray:
-    """Top-k PCs mapped back to the original domain; estimators.py:116-129"""
+def principal_components(sketch: SparseSketch, k: int, solver: str = "host") -> np.ndarray:
+    """Top-k PCs mapped back to the original domain; estimators.py:116-129.
+
+    The adjoint (FWHT then D, truncation) runs on the device for all k vectors at once;
+    ``solver`` selects the host (reference) or device eigensolve.
+    """
     est = estimate_covariance(sketch)
-    V = top_eigenvectors(est.matrix, k)
     spec = sketch.spec
-    Vd = torch.as_tensor(np.ascontiguousarray(V.T), device=sketch.indices.device)
+    if solver == "device":
+        Vd = top_eigenvectors(est.device_matrix, k, solver="device").T.contiguous()
+    else:
+        V = top_eigenvectors(est.matrix, k)
+        Vd = torch.as_tensor(np.ascontiguousarray(V.T), device=sketch.indices.device)
     U = torch.empty((k, spec.p), dtype=torch.float64, device=Vd.device)
     with torch.cuda.device(Vd.device):
         _lib.call("skc_unprecondition", Vd.data_ptr(), k, spec.p_pad, spec.gpu_kind(), u64(spec.sign_seed), spec.p,

@@ -129,6 +129,10 @@ def test_sketch_f64_bit_exact_and_estimators(skc, golden, name):
         ref = g[f"{name}_pcs"]
         sgn = np.sign(np.sum(U * ref, axis=0))  # eigenvector sign is parity-unpinned
         assert np.abs(U * sgn - ref).max() < 1e-6
+        # device eigensolve (cuSOLVER): same eigenvectors up to sign, eigensolver rounding
+        Ud = skc.principal_components(sk, k, solver="device")
+        sgn = np.sign(np.sum(Ud * U, axis=0))
+        assert np.abs(Ud * sgn - U).max() < 1e-7
 
 
 @pytest.mark.parametrize("name", ["c1", "c3", "c4", "c5", "c2"])
