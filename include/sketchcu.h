@@ -162,6 +162,17 @@ int skc_row_sqnorms(const void *val, int32_t val_dtype, int64_t n, int32_t m, do
 int skc_kmeans_d2_to_point(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m,
                            int32_t p_pad, int64_t c, const double *colsq, double *dense, double *out, void *stream);
 
+/* ---- SKCH1 file records (io.py:84-136) ---------------------------------------------
+ * A record is the sample's m u32 indices followed by its m f64 values, 12 m bytes, no
+ * padding; the file is a 61-byte header then n records. pack: (idx, val) -> out_words
+ * (n * 3m u32, device); fp32 values widen exactly to f64. unpack: the inverse into int32
+ * indices and f64 values. Replaces the numpy structured-dtype copies of write_sketch /
+ * read_sketch (io.py:88-136). */
+int skc_sketch_pack_records(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m,
+                            uint32_t *out_words, void *stream);
+int skc_sketch_unpack_records(const uint32_t *words, int64_t n, int32_t m, int32_t *idx_out, double *val_out,
+                              void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -39,7 +39,9 @@ int sm_count() {
   return cache[dev];
 }
 
-// kernels (sketch.cu, moments.cu, kmeans.cu)
+// kernels (sketch.cu, moments.cu, kmeans.cu, formats.cu)
+int pack_records_launch(const int32_t*, const void*, int, int64_t, int32_t, uint32_t*, cudaStream_t);
+int unpack_records_launch(const uint32_t*, int64_t, int32_t, int32_t*, double*, cudaStream_t);
 int sketch_launch(const void*, int32_t, int64_t, int64_t, int32_t, int32_t, int32_t, uint64_t, uint64_t, int64_t,
                   int32_t, int32_t, int32_t*, void*, int32_t, double*, cudaStream_t);
 int sketch_identity(const void*, int32_t, int64_t, int64_t, int32_t, int32_t, uint64_t, int64_t, int32_t, int32_t*,
@@ -291,6 +293,20 @@ int skc_kmeans_d2_to_point(const int32_t* idx, const void* val, int32_t val_dtyp
   if ((rc = check_dtype(val_dtype))) return rc;
   if (c < 0 || c >= n) return fail(SKC_EPARAM, "point index out of range");
   return d2_point_launch(idx, val, val_dtype == SKC_F64, n, m, p_pad, c, colsq, dense, out, S(stream));
+}
+
+int skc_sketch_pack_records(const int32_t* idx, const void* val, int32_t val_dtype, int64_t n, int32_t m,
+                            uint32_t* out_words, void* stream) {
+  int rc;
+  if ((rc = check_dtype(val_dtype))) return rc;
+  if (n < 0 || m < 1) return fail(SKC_EDIM, "need n >= 0 and m >= 1");
+  return pack_records_launch(idx, val, val_dtype == SKC_F64, n, m, out_words, S(stream));
+}
+
+int skc_sketch_unpack_records(const uint32_t* words, int64_t n, int32_t m, int32_t* idx_out, double* val_out,
+                              void* stream) {
+  if (n < 0 || m < 1) return fail(SKC_EDIM, "need n >= 0 and m >= 1");
+  return unpack_records_launch(words, n, m, idx_out, val_out, S(stream));
 }
 
 }  // extern "C"

@@ -246,6 +246,53 @@ def _launch_rows(rows: torch.Tensor, spec: PreconditionSpec, plan: SamplingPlan,
                   idx_out.data_ptr(), val_out.data_ptr(), _lib.dtype_code(val_out), _lib.stream_ptr(rows.device))
 
 
+def device_row_chunks(row_iter, device) -> Iterator[torch.Tensor]:
+    """CUDA (c, p) row chunks from host or device chunks, copying ahead of the consumer.
+
+    Host chunks (numpy or torch, any strides) go through two pinned staging buffers and a
+    copy stream: chunk k+1's host-to-device copy runs while the caller's kernels consume
+    chunk k on the current stream. Pinned contiguous torch chunks are copied directly.
+    CUDA chunks pass through.
+    """
+    device = torch.device(device)
+    copy_stream = None
+    ring = [None, None]
+    done = [None, None]
+    for k, chunk in enumerate(row_iter):
+        if isinstance(chunk, torch.Tensor) and chunk.is_cuda:
+            yield chunk
+            continue
+        t = chunk if isinstance(chunk, torch.Tensor) else torch.from_numpy(np.asarray(chunk))
+        if t.ndim != 2:
+            raise DimensionError(f"bad chunk: expected a 2-D block, got shape {tuple(t.shape)}")
+        if t.dtype not in (torch.float32, torch.float64):
+            t = t.to(torch.float64)
+        if copy_stream is None:
+            copy_stream = torch.cuda.Stream(device)
+        slot = k & 1
+        if t.is_pinned() and t.is_contiguous():
+            src = t
+        else:
+            if done[slot] is not None:
+                done[slot].synchronize()  # the previous copy out of this staging buffer finished
+            need = t.numel()
+            buf = ring[slot]
+            if buf is None or buf.dtype != t.dtype or buf.numel() < need:
+                buf = ring[slot] = torch.empty(max(need, 1), dtype=t.dtype, pin_memory=True)
+            src = buf[:need].view(t.shape)
+            src.copy_(t)
+        compute = torch.cuda.current_stream(device)
+        with torch.cuda.stream(copy_stream):
+            dev = torch.empty(t.shape, dtype=t.dtype, device=device)
+            dev.copy_(src, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy_stream)
+        done[slot] = ev
+        compute.wait_event(ev)
+        dev.record_stream(compute)
+        yield dev
+
+
 def sketch_stream(source, spec: PreconditionSpec, plan: SamplingPlan, *, compute: str = "f64",
                   values_dtype: Optional[torch.dtype] = None, device=None, col0: int = 0) -> SparseSketch:
     """Precondition and sample every column of ``source`` in one pass; sketch.py:196-223.
@@ -270,11 +317,8 @@ def sketch_stream(source, spec: PreconditionSpec, plan: SamplingPlan, *, compute
     values = torch.empty((n, plan.m), dtype=values_dtype, device=device)
     row_iter = source.row_chunks() if hasattr(source, "row_chunks") else (ch.T for ch in source.chunks())
     j0 = 0
-    for chunk in row_iter:
-        try:
-            rows, _ = as_device(chunk, device=device)
-        except Exception as exc:  # pragma: no cover - conversion failures carry the offset
-            raise DimensionError(f"bad chunk at column offset {j0}: {exc}") from exc
+    for chunk in device_row_chunks(row_iter, device):
+        rows = chunk
         if rows.ndim != 2 or rows.shape[1] != spec.p:
             raise DimensionError(
                 f"bad chunk at column offset {j0}: expected ({spec.p}, c) block, got {tuple(rows.T.shape)}"

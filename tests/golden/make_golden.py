@@ -192,8 +192,41 @@ def gen_kmeans():
     return d
 
 
+def gen_formats():
+    """SKCH1 / DNSE1 bytes written by the reference (io.py) for small seeded inputs."""
+    import tempfile
+
+    d = {}
+    cases = [("had", "hadamard", 20, 15, 1234, 0.3, 987, 2), ("none", "none", 13, 9, 0, 0.5, 31, 3),
+             ("had64", "hadamard", 64, 40, 77, 0.25, 5, 4)]
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, kind, p, n, ss, gamma, ms, xseed in cases:
+            X = np.random.default_rng(xseed).standard_normal((p, n))
+            spec = skp.PreconditionSpec.create(kind, p, sign_seed=ss)
+            plan = skp.plan_for(spec, gamma, master_seed=ms)
+            sk = skp.sketch_stream(X, spec, plan)
+            f = os.path.join(tmp, name + ".skch")
+            skp.write_sketch(f, sk)
+            d[f"{name}_X"] = X
+            d[f"{name}_meta"] = np.array([p, n, ss, ms], dtype=np.int64)
+            d[f"{name}_gamma"] = np.float64(gamma)
+            d[f"{name}_kind"] = np.array(kind)
+            d[f"{name}_skch"] = np.frombuffer(open(f, "rb").read(), dtype=np.uint8)
+            g = os.path.join(tmp, name + ".dnse")
+            skp.write_dense(g, X)
+            d[f"{name}_dnse"] = np.frombuffer(open(g, "rb").read(), dtype=np.uint8)
+    d["names"] = np.array([c[0] for c in cases])
+    return d
+
+
+GENERATORS = {"hash": gen_hash, "transform": gen_transform, "sketch": gen_sketch, "kmeans": gen_kmeans,
+              "formats": gen_formats}
+
+
 def main():
-    for fname, fn in [("hash", gen_hash), ("transform", gen_transform), ("sketch", gen_sketch), ("kmeans", gen_kmeans)]:
+    which = sys.argv[1:] or list(GENERATORS)
+    for fname in which:
+        fn = GENERATORS[fname]
         path = os.path.join(OUT, f"{fname}.npz")
         np.savez_compressed(path, **fn())
         print(f"wrote {path} ({os.path.getsize(path) / 1e3:.0f} kB)")
