@@ -173,6 +173,21 @@ int skc_sketch_pack_records(const int32_t *idx, const void *val, int32_t val_dty
 int skc_sketch_unpack_records(const uint32_t *words, int64_t n, int32_t m, int32_t *idx_out, double *val_out,
                               void *stream);
 
+/* ---- Two-pass K-means, second pass (cluster.py:407-456) ------------------------------
+ * Rows X (n, p) with leading dimension ld, fp32 or fp64; centres mu (K, p) fp64 row-major
+ * (original domain, the first pass's mu_hat transposed).
+ * skc_dense_assign: labels[i] = first argmin_k (|x_i|^2 - 2 <x_i, mu_k>) + |mu_k|^2 and
+ *   d2min[i] = max(that minimum, 0) (cluster.py:437-440); ws: skc_dense_assign_workspace bytes
+ *   (centre norms and a transposed, padded copy of mu).
+ * skc_dense_sums: sums[k] += sum of rows with labels[i] == k, counts[k] += their number
+ *   (cluster.py:434-436, 445); fp64 in a fixed order. ws: skc_dense_sums_workspace bytes. */
+size_t skc_dense_assign_workspace(int32_t p, int32_t K);
+int skc_dense_assign(const void *X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, const double *mu, int32_t K,
+                     void *ws, int32_t *labels, double *d2min, void *stream);
+size_t skc_dense_sums_workspace(int64_t n, int32_t p, int32_t K);
+int skc_dense_sums(const void *X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, const int32_t *labels, int32_t K,
+                   double *sums, int64_t *counts, void *ws, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -57,6 +57,10 @@ SIGNATURES = {
     "skc_kmeans_reseed": (_c.c_int, [_P, _P, _I32, _I32, _P, _I32, _I32, _P, _P]),
     "skc_sketch_pack_records": (_c.c_int, [_P, _P, _I32, _I64, _I32, _P, _P]),
     "skc_sketch_unpack_records": (_c.c_int, [_P, _I64, _I32, _P, _P, _P]),
+    "skc_dense_assign_workspace": (_c.c_size_t, [_I32, _I32]),
+    "skc_dense_assign": (_c.c_int, [_P, _I32, _I64, _I64, _I32, _P, _I32, _P, _P, _P, _P]),
+    "skc_dense_sums_workspace": (_c.c_size_t, [_I64, _I32, _I32]),
+    "skc_dense_sums": (_c.c_int, [_P, _I32, _I64, _I64, _I32, _P, _I32, _P, _P, _P, _P]),
 }
 
 _lock = threading.Lock()

@@ -23,7 +23,7 @@ import torch
 from . import _lib
 from . import dist
 from .errors import ParameterError
-from .sketch import SparseSketch, as_source, plan_for, sketch_stream
+from .sketch import SparseSketch, as_source, device_row_chunks, plan_for, sketch_stream
 from .transform import PreconditionSpec, unprecondition_columns
 
 ORIGINAL = "original"
@@ -351,3 +351,74 @@ def sparsified_kmeans(source, K: int, gamma: float, max_iter: int = 100, n_init:
     result = _sparsified_on_sketch(sketch, K, max_iter=max_iter, n_init=n_init, seed=seed, init=init)
     result.diagnostics.update(sketch_seconds=sketch_seconds, passes=getattr(source, "passes", None))
     return result
+
+
+def sparsified_kmeans_two_pass(source, K: int, gamma: float, max_iter: int = 100, n_init: int = 20, seed: int = 0,
+                               kind: str = "hadamard", chunk_cols: int = 8192, *, compute: str = "f64",
+                               device=None) -> KMeansResult:
+    """Sparsified K-means plus one pass over the raw rows; cluster.py:407-456.
+
+    The second pass runs on the GPU as the raw chunks stream in (pinned copies overlapped
+    with the kernels): ``skc_dense_assign`` re-assigns every point to its nearest first-pass
+    centre (first argmin of (|x|^2 - 2 <x, mu>) + |mu|^2, clipped objective) and
+    ``skc_dense_sums`` accumulates the exact original-domain means of the first-pass
+    clusters. Nothing further is iterated. Each chunk's objective is a numpy-order pairwise
+    sum, and the chunk sums add in chunk order, as the reference does.
+    """
+    source = as_source(source, chunk_cols=chunk_cols)
+    first = sparsified_kmeans(source, K, gamma, max_iter=max_iter, n_init=n_init, seed=seed, kind=kind,
+                              chunk_cols=chunk_cols, compute=compute, device=device)
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    mu_hat = np.asarray(first.centers.centers, dtype=np.float64)  # (p, K)
+    p, n = source.p, source.n
+    mu_rows = torch.as_tensor(np.ascontiguousarray(mu_hat.T), device=dev)  # (K, p)
+    lab1 = torch.as_tensor(np.asarray(first.assignments.labels, dtype=np.int32), device=dev)
+    labels2 = torch.empty(n, dtype=torch.int32, device=dev)
+    d2min = torch.empty(n, dtype=torch.float64, device=dev)
+    sums = torch.zeros((K, p), dtype=torch.float64, device=dev)
+    counts = torch.zeros(K, dtype=torch.int64, device=dev)
+    L = _lib.lib()
+    aws = _lib.workspace(L.skc_dense_assign_workspace(p, K), dev)
+    row_iter = source.row_chunks() if hasattr(source, "row_chunks") else (ch.T for ch in source.chunks())
+    chunk_obj, spans = [], []
+    j0 = 0
+    with torch.cuda.device(dev):
+        st = _lib.stream_ptr(dev)
+        for rows in device_row_chunks(row_iter, dev):
+            if rows.ndim != 2 or rows.shape[1] != p:
+                raise ParameterError(f"bad chunk at column offset {j0}: expected ({p}, c)")
+            if rows.stride(1) != 1:
+                rows = rows.contiguous()
+            c = rows.shape[0]
+            if j0 + c > n:
+                raise ParameterError(f"source yielded more than {n} columns")
+            xc = _lib.dtype_code(rows)
+            _lib.call("skc_dense_assign", rows.data_ptr(), xc, rows.stride(0), c, p, mu_rows.data_ptr(), K,
+                      aws.data_ptr(), labels2[j0:].data_ptr(), d2min[j0:].data_ptr(), st)
+            ws = _lib.workspace(L.skc_dense_sums_workspace(c, p, K), dev)
+            _lib.call("skc_dense_sums", rows.data_ptr(), xc, rows.stride(0), c, p, lab1[j0:].data_ptr(), K,
+                      sums.data_ptr(), counts.data_ptr(), ws.data_ptr(), st)
+            spans.append((j0, c))
+            j0 += c
+        if j0 != n:
+            raise ParameterError(f"source yielded {j0} columns, expected {n}")
+        obj_dev = torch.zeros(max(len(spans), 1), dtype=torch.float64, device=dev)
+        pw = _lib.workspace(L.skc_pairwise_sum_workspace(max((c for _, c in spans), default=1)), dev)
+        for t, (a, c) in enumerate(spans):
+            _lib.call("skc_pairwise_sum", d2min[a:].data_ptr(), c, obj_dev[t:].data_ptr(), pw.data_ptr(), pw.numel(), st)
+    obj = 0.0
+    for v in obj_dev.cpu().numpy()[: len(spans)]:
+        obj += float(v)
+    cnt = counts.cpu().numpy()
+    mu2 = sums.cpu().numpy().T.copy()  # (p, K)
+    nz = cnt > 0
+    mu2[:, nz] = mu2[:, nz] / cnt[nz].astype(np.float64)[None, :]
+    mu2[:, ~nz] = mu_hat[:, ~nz]
+    diagnostics = dict(first.diagnostics)
+    diagnostics.update(passes=getattr(source, "passes", None), first_pass_objective=first.objective)
+    return KMeansResult(
+        assignments=Assignments(labels=labels2.cpu().numpy().astype(np.int64)),
+        centers=CenterSet(K=K, centers=mu2, domain=ORIGINAL),
+        objective=obj,
+        diagnostics=diagnostics,
+    )

@@ -42,6 +42,12 @@ int sm_count() {
 // kernels (sketch.cu, moments.cu, kmeans.cu, formats.cu)
 int pack_records_launch(const int32_t*, const void*, int, int64_t, int32_t, uint32_t*, cudaStream_t);
 int unpack_records_launch(const uint32_t*, int64_t, int32_t, int32_t*, double*, cudaStream_t);
+size_t dense_sums_ws(int64_t, int32_t, int32_t);
+size_t dense_assign_ws(int32_t, int32_t);
+int dense_assign_launch(const void*, int, int64_t, int64_t, int32_t, const double*, int32_t, double*, int32_t*,
+                        double*, cudaStream_t);
+int dense_sums_launch(const void*, int, int64_t, int64_t, int32_t, const int32_t*, int32_t, double*, long long*, void*,
+                      cudaStream_t);
 int sketch_launch(const void*, int32_t, int64_t, int64_t, int32_t, int32_t, int32_t, uint64_t, uint64_t, int64_t,
                   int32_t, int32_t, int32_t*, void*, int32_t, double*, cudaStream_t);
 int sketch_identity(const void*, int32_t, int64_t, int64_t, int32_t, int32_t, uint64_t, int64_t, int32_t, int32_t*,
@@ -307,6 +313,34 @@ int skc_sketch_unpack_records(const uint32_t* words, int64_t n, int32_t m, int32
                               void* stream) {
   if (n < 0 || m < 1) return fail(SKC_EDIM, "need n >= 0 and m >= 1");
   return unpack_records_launch(words, n, m, idx_out, val_out, S(stream));
+}
+
+static int check_dense(int32_t x_dtype, int64_t ld, int64_t n, int32_t p, int32_t K) {
+  int rc;
+  if ((rc = check_dtype(x_dtype))) return rc;
+  if (n < 0 || p < 1 || ld < p) return fail(SKC_EDIM, "need n >= 0, p >= 1 and ld >= p");
+  if (K < 1) return fail(SKC_EPARAM, "need K >= 1");
+  return SKC_OK;
+}
+
+size_t skc_dense_assign_workspace(int32_t p, int32_t K) { return dense_assign_ws(p, K); }
+
+int skc_dense_assign(const void* X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, const double* mu, int32_t K,
+                     void* ws, int32_t* labels, double* d2min, void* stream) {
+  int rc;
+  if ((rc = check_dense(x_dtype, ld, n, p, K))) return rc;
+  return dense_assign_launch(X, x_dtype == SKC_F64, ld, n, p, mu, K, reinterpret_cast<double*>(ws), labels, d2min,
+                             S(stream));
+}
+
+size_t skc_dense_sums_workspace(int64_t n, int32_t p, int32_t K) { return dense_sums_ws(n, p, K); }
+
+int skc_dense_sums(const void* X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, const int32_t* labels, int32_t K,
+                   double* sums, int64_t* counts, void* ws, void* stream) {
+  int rc;
+  if ((rc = check_dense(x_dtype, ld, n, p, K))) return rc;
+  return dense_sums_launch(X, x_dtype == SKC_F64, ld, n, p, labels, K, sums, reinterpret_cast<long long*>(counts), ws,
+                           S(stream));
 }
 
 }  // extern "C"

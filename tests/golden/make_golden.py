@@ -219,8 +219,38 @@ def gen_formats():
     return d
 
 
+def gen_twopass():
+    """Reference sparsified_kmeans_two_pass (cluster.py:407-456) on seeded mixtures."""
+    d = {}
+    cases = [  # name, p, n, K, scale, gamma, n_init, seed, kind, chunk, max_iter
+        ("sep", 24, 400, 3, 4.0, 0.3, 3, 19, "hadamard", 100, 100),
+        ("mid", 64, 2000, 5, 1.0, 0.2, 2, 3, "hadamard", 512, 50),
+        ("none", 16, 150, 3, 3.0, 1.0, 3, 23, "none", 40, 100),
+        ("big", 200, 5000, 8, 1.5, 0.1, 2, 7, "hadamard", 1500, 30),
+    ]
+    for name, p, n, K, scale, gamma, n_init, seed, kind, chunk, max_iter in cases:
+        X = mixture(SEED + 17 * p + K, p, n, K, scale).astype(np.float64)
+        src = skp.ArraySource(X, chunk_cols=chunk)
+        res = skp.sparsified_kmeans_two_pass(src, K, gamma, max_iter=max_iter, n_init=n_init, seed=seed, kind=kind,
+                                             chunk_cols=chunk)
+        first = skp.sparsified_kmeans(X, K, gamma, max_iter=max_iter, n_init=n_init, seed=seed, kind=kind,
+                                      chunk_cols=chunk)
+        d[f"{name}_X_sha"] = np.array(digest(X))
+        d[f"{name}_cfg"] = np.array([p, n, K, n_init, seed, chunk, max_iter], dtype=np.int64)
+        d[f"{name}_f"] = np.array([scale, gamma], dtype=np.float64)
+        d[f"{name}_kind"] = np.array(kind)
+        d[f"{name}_labels"] = res.assignments.labels.astype(np.int32)
+        d[f"{name}_centers"] = res.centers.centers
+        d[f"{name}_objective"] = np.float64(res.objective)
+        d[f"{name}_first_labels"] = first.assignments.labels.astype(np.int32)
+        d[f"{name}_first_centers"] = first.centers.centers
+        d[f"{name}_first_objective"] = np.float64(first.objective)
+    d["names"] = np.array([c[0] for c in cases])
+    return d
+
+
 GENERATORS = {"hash": gen_hash, "transform": gen_transform, "sketch": gen_sketch, "kmeans": gen_kmeans,
-              "formats": gen_formats}
+              "formats": gen_formats, "twopass": gen_twopass}
 
 
 def main():
