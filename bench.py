@@ -224,9 +224,10 @@ def run_reference(args, cfg):
 
 def profiled_traffic(workload, n, stage):
     """dram read+write bytes per launch of the stage's kernel, from the committed ncu capture
-    (profiles/round1_<wl>_ncu_full.json) when it was taken at this exact size, else None."""
+    (profiles/<wl>_ncu_full.json, written by tools/ncu_summary.py) when it was taken at this
+    exact size, else None."""
     names = {"sketch": "sketch_kernel", "covariance": "cov_band_kernel", "moments": "moments_kernel"}
-    path = os.path.join(ROOT, "profiles", f"round1_{workload}_ncu_full.json")
+    path = os.path.join(ROOT, "profiles", f"{workload}_ncu_full.json")
     try:
         with open(path) as f:
             d = json.load(f)
