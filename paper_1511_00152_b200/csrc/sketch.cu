@@ -18,6 +18,7 @@
 //            (sketch.py:53-56); the kept set becomes a row bitmask, and each lane emits
 //            its rows' elements at prefix-sum slots in ascending index order.
 #include <math.h>
+#include <stdlib.h>
 
 #include <type_traits>
 
@@ -30,7 +31,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kTileElems = 8192;
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 
-enum SampleMode { kSelect = 0, kFullSet = 1, kSlowExact = 2, kNoSample = 3 };
+enum SampleMode { kSelect = 0, kFullSet = 1, kSlowExact = 2, kNoSample = 3, kGiven = 4 };
 
 struct SketchParams {
   const void* X;
@@ -44,6 +45,7 @@ struct SketchParams {
   uint64_t s_tag;      // mix64(master ^ TAG_SAMPLE)
   int64_t col0;
   int32_t* idx_out;
+  const int32_t* idx_in;  // kGiven: the kept indices (n, m), sorted per row
   void* val_out;
   int32_t val_f64;
   double* y_out;       // optional full transformed rows (n, p_pad) fp64
@@ -488,7 +490,7 @@ __global__ void __launch_bounds__(kThreads, 3) sketch_kernel(const SketchParams 
   // are in flight (the selection needs no data), then the CTA transforms and emits
   constexpr bool kEarly = LOGP >= 5;
   const bool async_load = has_x && std::is_same<T, float>::value && P.vec && !P.x_f64 && LOGP >= 2;
-  const bool sampling = P.mode != kNoSample;
+  const bool sampling = P.mode != kNoSample && P.mode != kGiven;
   for (int64_t tile = blockIdx.x; tile < P.num_tiles; tile += gridDim.x) {
     const int64_t row0 = tile * G::S;
     const int64_t rows_left = P.n - row0;
@@ -578,8 +580,183 @@ __global__ void __launch_bounds__(kThreads, 3) sketch_kernel(const SketchParams 
         const bool ok = kEarly ? (okbits >> k) & 1u : select_one<LOGP>(P, row0 + s, ck, cj, memk, hist, rm);
         emit_one<LOGP, T>(P, xs, s, row0 + s, rm, ok);
       }
+    } else if (P.mode == kGiven) {  // gather at supplied indices (coalesced per row)
+      for (int s = warp; s < G::S && s < rows_left; s += kWarps) {
+        const int64_t o = (row0 + s) * P.m;
+        for (int t = threadIdx.x & 31; t < P.m; t += 32)
+          store_val<T>(P.val_out, o + t, y_at<LOGP, T>(xs, s, __ldg(P.idx_in + o + t)), P.val_f64);
+      }
     }
   }
+}
+
+// ------------------------------------------------------------------------------------
+// kGiven with fp32 rows: K1 without the selection, double-buffered. Tile k+1's cp.async
+// copies are in flight while tile k is transformed and its values gathered, so the kernel
+// streams at HBM rate instead of exposing each tile's load latency.
+template <int LOGP>
+__global__ void __launch_bounds__(kThreads, 2) gather_kernel(const SketchParams P) {
+  using G = Geo<LOGP>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr size_t kTileBytes = sizeof(float) * ((G::WORDS + 3) & ~3);
+  float* xs0 = reinterpret_cast<float*>(smem);
+  constexpr int kSignWords = (G::P + 31) / 32;
+  uint32_t* sgn = reinterpret_cast<uint32_t*>(smem + 2 * kTileBytes);
+  const int warp = threadIdx.x >> 5;
+  if (P.use_signs) {  // D diagonal, _hash.py:38-43, regenerated per CTA
+    for (int w = threadIdx.x; w < kSignWords; w += kThreads) {
+      uint32_t bits = 0;
+      for (int b = 0; b < 32 && w * 32 + b < G::P; ++b)
+        bits |= (uint32_t)(mix64(P.sign_state + kGamma * (uint64_t)(w * 32 + b + 1)) >> 63) << b;
+      sgn[w] = bits;
+    }
+  }
+  const float scale = (float)(1.0 / sqrt((double)G::P));  // transform.py:170
+  constexpr int NV = kTileElems / 4 / kThreads;
+  const int f0 = threadIdx.x * 4;
+  const int s0 = f0 >> LOGP, i0 = f0 & (G::P - 1);
+  const uint32_t dst0 = (uint32_t)__cvta_generic_to_shared(smem);
+  auto issue = [&](int64_t tile, int buf) {
+    const int64_t row0 = tile * G::S;
+    const int64_t rows_left = P.n - row0;
+    const float* xb = reinterpret_cast<const float*>(P.X) + (row0 + s0) * P.ld + i0;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int f = f0 + k * kThreads * 4;
+      const int sk = f >> LOGP, ik = f & (G::P - 1);
+      const bool ok = sk < rows_left;
+      const float* src = ok ? xb + (sk - s0) * P.ld + (ik - i0) : reinterpret_cast<const float*>(P.X);
+      const uint32_t dst = dst0 + (uint32_t)(buf * kTileBytes) + 4u * (uint32_t)(sk * G::SP + G::addr(ik));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int64_t tile = blockIdx.x;
+  if (tile < P.num_tiles) issue(tile, 0);
+  for (int it = 0; tile < P.num_tiles; tile += gridDim.x, ++it) {
+    const int buf = it & 1;
+    const int64_t next = tile + gridDim.x;
+    if (next < P.num_tiles) {
+      issue(next, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_all;" ::: "memory");
+    }
+    __syncthreads();  // tile in buf visible to all; signs visible
+    float* xs = reinterpret_cast<float*>(smem + buf * kTileBytes);
+    wht_all_windows<LOGP, float, 0>(xs, P.use_signs ? sgn : nullptr, scale);
+    const int64_t row0 = tile * G::S;
+    const int64_t rows_left = P.n - row0;
+    if (P.y_out) {
+      for (int f = threadIdx.x; f < kTileElems; f += kThreads) {
+        const int s = f >> LOGP, i = f & (G::P - 1);
+        if (s < rows_left) P.y_out[(row0 + s) * G::P + i] = (double)xs[s * G::SP + G::addr(i)];
+      }
+    }
+    for (int s = warp; s < G::S && s < rows_left; s += kWarps) {
+      const int64_t o = (row0 + s) * P.m;
+      for (int t = threadIdx.x & 31; t < P.m; t += 32)
+        store_val<float>(P.val_out, o + t, y_at<LOGP, float>(xs, s, __ldg(P.idx_in + o + t)), P.val_f64);
+    }
+    __syncthreads();  // buf is refilled by the copies issued next iteration
+  }
+  (void)xs0;
+}
+
+template <int LOGP>
+static int launch_gather_t(SketchParams P, cudaStream_t st) {
+  using G = Geo<LOGP>;
+  const size_t smem = 2 * sizeof(float) * ((G::WORDS + 3) & ~3) + 4 * (((G::P + 31) / 32 + 3) & ~3);
+  auto kern = gather_kernel<LOGP>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return check_launch("gather smem attribute");
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
+  if (occ < 1) occ = 1;
+  P.num_tiles = (P.n + G::S - 1) / G::S;
+  int64_t grid = (int64_t)sm_count() * occ;
+  if (grid > P.num_tiles) grid = P.num_tiles;
+  if (grid < 1) return SKC_OK;
+  kern<<<(unsigned)grid, kThreads, smem, st>>>(P);
+  return check_launch("gather_kernel");
+}
+
+static int launch_gather_logp(int logp, const SketchParams& P, cudaStream_t st) {
+  switch (logp) {
+    case 2: return launch_gather_t<2>(P, st);
+    case 3: return launch_gather_t<3>(P, st);
+    case 4: return launch_gather_t<4>(P, st);
+    case 5: return launch_gather_t<5>(P, st);
+    case 6: return launch_gather_t<6>(P, st);
+    case 7: return launch_gather_t<7>(P, st);
+    case 8: return launch_gather_t<8>(P, st);
+    case 9: return launch_gather_t<9>(P, st);
+    case 10: return launch_gather_t<10>(P, st);
+    case 11: return launch_gather_t<11>(P, st);
+    case 12: return launch_gather_t<12>(P, st);
+  }
+  return fail(SKC_EPARAM, "gather kernel needs 4 <= p_pad <= 4096");
+}
+
+// ------------------------------------------------------------------------------------
+// Index-only sampler: the selection of K1 (phase 3) without the tile, one warp per sample,
+// grid-stride over samples. With no 37 KB tile per CTA it runs at full occupancy, and K1 in
+// kGiven mode then only loads, transforms and gathers (HBM-bound).
+constexpr int kIdxWarps = 8;
+template <int LOGP>
+__global__ void __launch_bounds__(kIdxWarps * 32, 4) indices_kernel(const SketchParams P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5;
+  constexpr int kRowWords = mask_words<LOGP>();
+  unsigned char* mine = smem + warp_bytes<LOGP>(P.cap) * warp;
+  uint64_t* ck = reinterpret_cast<uint64_t*>(mine);
+  uint64_t* memk = reinterpret_cast<uint64_t*>(mine + (size_t)P.cap * 8);
+  int* hist = reinterpret_cast<int*>(mine + (size_t)P.cap * 8 + 256);
+  uint32_t* rmask = reinterpret_cast<uint32_t*>(mine + (size_t)P.cap * 8 + 256 + 128);
+  uint16_t* cj = reinterpret_cast<uint16_t*>(mine + (size_t)P.cap * 8 + 256 + 128 + 4 * kRowWords);
+  for (int i = threadIdx.x & 31; i < kRowWords; i += 32) rmask[i] = 0;
+  __syncwarp();
+  const int64_t warps = (int64_t)gridDim.x * kIdxWarps;
+  for (int64_t row = blockIdx.x * (int64_t)kIdxWarps + warp; row < P.n; row += warps) {
+    const bool ok = select_one<LOGP>(P, row, ck, cj, memk, hist, rmask);
+    emit_one<LOGP, float>(P, nullptr, 0, row, rmask, ok);  // val_out == nullptr: indices only
+  }
+}
+
+template <int LOGP>
+static int launch_indices_t(SketchParams P, cudaStream_t st) {
+  const size_t smem = warp_bytes<LOGP>(P.cap) * kIdxWarps;
+  auto kern = indices_kernel<LOGP>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return check_launch("indices smem attribute");
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kIdxWarps * 32, smem);
+  if (occ < 1) occ = 1;
+  int64_t grid = (int64_t)sm_count() * occ;
+  const int64_t need = (P.n + kIdxWarps - 1) / kIdxWarps;
+  if (grid > need) grid = need;
+  if (grid < 1) return SKC_OK;
+  kern<<<(unsigned)grid, kIdxWarps * 32, smem, st>>>(P);
+  return check_launch("indices_kernel");
+}
+
+static int launch_indices_logp(int logp, const SketchParams& P, cudaStream_t st) {
+  switch (logp) {
+    case 0: return launch_indices_t<0>(P, st);
+    case 1: return launch_indices_t<1>(P, st);
+    case 2: return launch_indices_t<2>(P, st);
+    case 3: return launch_indices_t<3>(P, st);
+    case 4: return launch_indices_t<4>(P, st);
+    case 5: return launch_indices_t<5>(P, st);
+    case 6: return launch_indices_t<6>(P, st);
+    case 7: return launch_indices_t<7>(P, st);
+    case 8: return launch_indices_t<8>(P, st);
+    case 9: return launch_indices_t<9>(P, st);
+    case 10: return launch_indices_t<10>(P, st);
+    case 11: return launch_indices_t<11>(P, st);
+    case 12: return launch_indices_t<12>(P, st);
+  }
+  return fail(SKC_EPARAM, "p_pad exceeds the largest instantiated sampler (4096)");
 }
 
 // ------------------------------------------------------------------------------------
@@ -677,8 +854,25 @@ int sketch_launch(const void* X, int32_t x_dtype, int64_t ld, int64_t n, int32_t
     plan_select(p_pad, m, P);
   }
   if (kind == SKC_KIND_NONE && X != nullptr) return fail(SKC_EPARAM, "internal: kind none uses sketch_identity");
-  if (compute_dtype == SKC_F64) return launch_sketch_logp<double>(logp, P, st);
-  return launch_sketch_logp<float>(logp, P, st);
+  // Default: indices first (index-only sampler at full occupancy), then K1 gathers values at
+  // them. SKC_SKETCH_FUSED=1 selects the single fused kernel instead.
+  static const bool fused = getenv("SKC_SKETCH_FUSED") != nullptr;
+  if (X == nullptr || idx_out == nullptr || fused) {
+    if (X == nullptr && idx_out != nullptr && !fused) return launch_indices_logp(logp, P, st);
+    if (compute_dtype == SKC_F64) return launch_sketch_logp<double>(logp, P, st);
+    return launch_sketch_logp<float>(logp, P, st);
+  }
+  int rc = launch_indices_logp(logp, P, st);
+  if (rc) return rc;
+  SketchParams G = P;
+  G.mode = kGiven;
+  G.idx_in = idx_out;
+  G.idx_out = nullptr;
+  G.cap = 0;  // no selection scratch
+  if (val_out == nullptr) return SKC_OK;
+  if (compute_dtype == SKC_F64) return launch_sketch_logp<double>(logp, G, st);
+  if (G.vec && !G.x_f64 && logp >= 2) return launch_gather_logp(logp, G, st);
+  return launch_sketch_logp<float>(logp, G, st);
 }
 
 // kind == none: values are the raw coordinates (transform.py:225-227); the sampler runs
