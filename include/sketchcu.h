@@ -162,6 +162,21 @@ int skc_row_sqnorms(const void *val, int32_t val_dtype, int64_t n, int32_t m, do
 int skc_kmeans_d2_to_point(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m,
                            int32_t p_pad, int64_t c, const double *colsq, double *dense, double *out, void *stream);
 
+/* ---- Philox sampler and supplied-index sketching -----------------------------------
+ * north_star's counter-based alternative to the reference hash (not reference-identical;
+ * restated bit for bit by oracle/sketch_oracle.c:orc_philox_indices). Column g = col0 + i
+ * draws m of p_pad coordinates without replacement with Floyd's algorithm on a
+ * Philox4x32-10 stream keyed by mix64(master_seed ^ 0x50484C58); idx_out (n, m) int32,
+ * ascending per row. Same role as skc_indices (sketch.py:48-56). */
+int skc_indices_philox(uint64_t master_seed, int64_t col0, int64_t n, int32_t p_pad, int32_t m, int32_t *idx_out,
+                       void *stream);
+/* Sketch values at supplied indices: val_out[i][t] = precondition(x_i)[idx_in[i][t]].
+ * idx_in is (n, m) int32, each row strictly increasing (from skc_indices,
+ * skc_indices_philox, or the reference in oracle mode). Arguments as skc_sketch. */
+int skc_sketch_given(const void *X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, int32_t p_pad, int32_t kind,
+                     uint64_t sign_seed, int32_t m, int32_t compute_dtype, const int32_t *idx_in, void *val_out,
+                     int32_t val_dtype, void *stream);
+
 /* ---- SKCH1 file records (io.py:84-136) ---------------------------------------------
  * A record is the sample's m u32 indices followed by its m f64 values, 12 m bytes, no
  * padding; the file is a 61-byte header then n records. pack: (idx, val) -> out_words

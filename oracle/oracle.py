@@ -55,6 +55,8 @@ def lib():
         L.orc_signs.argtypes = [u64, i32, P]
         L.orc_column_keys.argtypes = [u64, i64, i64, i32, P]
         L.orc_indices_block.argtypes = [u64, i64, i64, i32, i32, P]
+        L.orc_philox_indices.argtypes = [u64, i64, i64, i32, i32, P]
+        L.orc_philox4x32_10.argtypes = [P, ctypes.c_uint32, ctypes.c_uint32]
         L.orc_fwht.argtypes = [P, i32]
         L.orc_precondition_rows.argtypes = [P, i64, i64, i32, i32, i32, u64, P]
         L.orc_unprecondition_rows.argtypes = [P, i64, i32, i32, u64, P]
@@ -107,6 +109,20 @@ def indices_block(master_seed: int, i0: int, i1: int, p: int, m: int) -> np.ndar
     """SamplingPlan.indices_block, sketch.py:48-56"""
     out = np.empty((i1 - i0, m), dtype=np.uint32)
     lib().orc_indices_block(_u64(master_seed), i0, i1 - i0, p, m, _p(out))
+    return out
+
+
+def philox4x32_10(ctr, key) -> np.ndarray:
+    """One Philox4x32-10 block (Salmon et al. SC'11): 4 x u32 counter, 2 x u32 key."""
+    c = np.array(ctr, dtype=np.uint32)
+    lib().orc_philox4x32_10(_p(c), int(key[0]), int(key[1]))
+    return c
+
+
+def philox_indices(master_seed: int, i0: int, i1: int, p: int, m: int) -> np.ndarray:
+    """The Philox sampler's kept sets (no reference counterpart; see sketch_oracle.c)."""
+    out = np.empty((i1 - i0, m), dtype=np.uint32)
+    lib().orc_philox_indices(_u64(master_seed), i0, i1 - i0, p, m, _p(out))
     return out
 
 

@@ -40,6 +40,9 @@ int sm_count() {
 }
 
 // kernels (sketch.cu, moments.cu, kmeans.cu, formats.cu)
+int philox_indices_launch(uint64_t, int64_t, int64_t, int32_t, int32_t, int32_t*, cudaStream_t);
+int sketch_given_launch(const void*, int32_t, int64_t, int64_t, int32_t, int32_t, int32_t, uint64_t, int32_t, int32_t,
+                        const int32_t*, void*, int32_t, cudaStream_t);
 int pack_records_launch(const int32_t*, const void*, int, int64_t, int32_t, uint32_t*, cudaStream_t);
 int unpack_records_launch(const uint32_t*, int64_t, int32_t, int32_t*, double*, cudaStream_t);
 size_t dense_sums_ws(int64_t, int32_t, int32_t);
@@ -160,6 +163,27 @@ int skc_indices(uint64_t master_seed, int64_t col0, int64_t n, int32_t p_pad, in
   if (n <= 0) return SKC_OK;
   return sketch_launch(nullptr, SKC_F32, 0, n, p_pad, p_pad, SKC_KIND_HADAMARD, 0, master_seed, col0, m, SKC_F32,
                        idx_out, nullptr, SKC_F32, nullptr, S(stream));
+}
+
+int skc_indices_philox(uint64_t master_seed, int64_t col0, int64_t n, int32_t p_pad, int32_t m, int32_t* idx_out,
+                       void* stream) {
+  int rc;
+  if ((rc = check_m(m, p_pad))) return rc;
+  if (p_pad < 1 || p_pad > kMaxPad) return fail(SKC_EPARAM, "p_pad out of range for the GPU sampler");
+  if (n <= 0) return SKC_OK;
+  return philox_indices_launch(master_seed, col0, n, p_pad, m, idx_out, S(stream));
+}
+
+int skc_sketch_given(const void* X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, int32_t p_pad, int32_t kind,
+                     uint64_t sign_seed, int32_t m, int32_t compute_dtype, const int32_t* idx_in, void* val_out,
+                     int32_t val_dtype, void* stream) {
+  int rc;
+  if ((rc = check_spec(kind, p, p_pad)) || (rc = check_m(m, p_pad)) || (rc = check_dtype(x_dtype)) ||
+      (rc = check_dtype(compute_dtype)) || (rc = check_dtype(val_dtype)))
+    return rc;
+  if (n < 0 || ld < p) return fail(SKC_EDIM, "expected a (n, p) row block with ld >= p");
+  return sketch_given_launch(X, x_dtype, ld, n, p, p_pad, kind, sign_seed, m, compute_dtype, idx_in, val_out,
+                             val_dtype, S(stream));
 }
 
 int skc_sketch(const void* X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, int32_t p_pad, int32_t kind,

@@ -14,12 +14,29 @@ constexpr uint64_t kMix1 = 0xBF58476D1CE4E5B9ULL;   // _hash.py:12
 constexpr uint64_t kMix2 = 0x94D049BB133111EBULL;   // _hash.py:13
 constexpr uint64_t kTagSign = 0x53494748ULL;        // _hash.py:16
 constexpr uint64_t kTagSample = 0x53414D50ULL;      // _hash.py:17
+constexpr uint64_t kTagPhilox = 0x50484C58ULL;      // "PHLX": Philox sampler key derivation
 
 // splitmix64 finalizer (_hash.py:20-26). 64-bit ops lower to 32-bit IMAD/SHF/LOP3.
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * kMix1;
   z = (z ^ (z >> 27)) * kMix2;
   return z ^ (z >> 31);
+}
+
+// Philox4x32-10 (Salmon et al., SC'11): counter (4 x u32) and key (2 x u32) -> 4 x u32.
+struct Philox4 {
+  uint32_t x, y, z, w;
+};
+__host__ __device__ __forceinline__ Philox4 philox4x32_10(Philox4 c, uint32_t k0, uint32_t k1) {
+  constexpr uint32_t kM0 = 0xD2511F53u, kM1 = 0xCD9E8D57u, kW0 = 0x9E3779B9u, kW1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)kM0 * c.x, p1 = (uint64_t)kM1 * c.z;
+    c = Philox4{(uint32_t)(p1 >> 32) ^ c.y ^ k0, (uint32_t)p1, (uint32_t)(p0 >> 32) ^ c.w ^ k1, (uint32_t)p0};
+    k0 += kW0;
+    k1 += kW1;
+  }
+  return c;
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {

@@ -900,6 +900,102 @@ __global__ void gather_identity_kernel(const void* X, int x_f64, int64_t ld, int
   }
 }
 
+// ------------------------------------------------------------------------------------
+// Philox sampler (north_star's counter-based alternative to the reference hash). Column g
+// (global) draws m of p coordinates without replacement by Floyd's algorithm:
+//   for s in 0..m-1: j = p - m + s; t = floor(r_s * (j + 1) / 2^32);
+//                    insert t unless already present, else insert j,
+// with r_s = component s % 4 of Philox4x32-10(counter {s / 4, g_lo, g_hi, "PHLX"},
+// key mix64(master ^ "PHLX")). The set is returned in ascending order. One lane per column;
+// the lane's p-bit set lives in shared memory as [word][lane], which is bank-conflict-free
+// for any word indices. ~45 warp-instructions per column at p=1024, m=51.
+constexpr int kPhxThreads = 128;
+
+__global__ void __launch_bounds__(kPhxThreads) philox_indices_kernel(uint64_t key, int64_t col0, int64_t n, int32_t p,
+                                                                    int32_t m, int32_t* __restrict__ idx_out) {
+  extern __shared__ uint32_t bm[];  // [W][kPhxThreads]
+  const int W = (p + 31) >> 5;
+  const int t = threadIdx.x;
+  const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+  for (int64_t row = blockIdx.x * (int64_t)kPhxThreads + t; row - t < n; row += (int64_t)gridDim.x * kPhxThreads) {
+    if (row >= n) continue;
+    for (int w = 0; w < W; ++w) bm[w * kPhxThreads + t] = 0u;
+    const uint64_t g = (uint64_t)(col0 + row);
+    for (int s0 = 0; s0 < m; s0 += 4) {
+      const Philox4 r4 = philox4x32_10(Philox4{(uint32_t)(s0 >> 2), (uint32_t)g, (uint32_t)(g >> 32), (uint32_t)kTagPhilox},
+                                       k0, k1);
+      const uint32_t rr[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int s = s0 + q;
+        if (s < m) {
+          const uint32_t j = (uint32_t)(p - m + s);
+          const uint32_t c = __umulhi(rr[q], j + 1u);
+          const uint32_t hit = (bm[(c >> 5) * kPhxThreads + t] >> (c & 31)) & 1u;
+          const uint32_t x = hit ? j : c;
+          bm[(x >> 5) * kPhxThreads + t] |= 1u << (x & 31);
+        }
+      }
+    }
+    int32_t* out = idx_out + row * m;
+    int k = 0;
+    for (int w = 0; w < W; ++w)
+      for (uint32_t b = bm[w * kPhxThreads + t]; b; b &= b - 1) out[k++] = 32 * w + __ffs(b) - 1;
+  }
+}
+
+int philox_indices_launch(uint64_t master_seed, int64_t col0, int64_t n, int32_t p, int32_t m, int32_t* idx_out,
+                          cudaStream_t st) {
+  if (n <= 0) return SKC_OK;
+  const size_t smem = (size_t)((p + 31) / 32) * kPhxThreads * 4;
+  if (cudaFuncSetAttribute(philox_indices_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return check_launch("philox smem attribute");
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, philox_indices_kernel, kPhxThreads, smem);
+  int64_t grid = (int64_t)sm_count() * (occ < 1 ? 1 : occ);
+  const int64_t need = (n + kPhxThreads - 1) / kPhxThreads;
+  if (grid > need) grid = need;
+  philox_indices_kernel<<<(unsigned)grid, kPhxThreads, smem, st>>>(mix64(master_seed ^ kTagPhilox), col0, n, p, m,
+                                                                   idx_out);
+  return check_launch("philox_indices_kernel");
+}
+
+// Values at supplied sorted indices (oracle mode with reference-supplied indices, or the
+// Philox sampler's): load + D + WHT + gather, no selection.
+int sketch_given_launch(const void* X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, int32_t p_pad, int32_t kind,
+                        uint64_t sign_seed, int32_t m, int32_t compute_dtype, const int32_t* idx_in, void* val_out,
+                        int32_t val_dtype, cudaStream_t st) {
+  if (n <= 0 || val_out == nullptr) return SKC_OK;
+  if (kind == SKC_KIND_NONE) {
+    const int64_t blocks = (n * (int64_t)m + 255) / 256;
+    gather_identity_kernel<<<(unsigned)blocks, 256, 0, st>>>(X, x_dtype == SKC_F64, ld, n, p, m, idx_in, val_out,
+                                                             val_dtype == SKC_F64, nullptr, p_pad);
+    return check_launch("gather_identity_kernel");
+  }
+  SketchParams P{};
+  P.X = X;
+  P.ld = ld;
+  P.n = n;
+  P.p = p;
+  P.m = m;
+  P.pk = p_pad;
+  P.x_f64 = x_dtype == SKC_F64;
+  P.use_signs = kind == SKC_KIND_HADAMARD;
+  P.sign_state = mix64(sign_seed ^ kTagSign);
+  P.val_out = val_out;
+  P.val_f64 = val_dtype == SKC_F64;
+  P.mode = kGiven;
+  P.idx_in = idx_in;
+  P.cap = 0;
+  int logp = 0;
+  while ((1 << logp) < p_pad) ++logp;
+  const uintptr_t xa = reinterpret_cast<uintptr_t>(X);
+  P.vec = p == p_pad && p_pad >= 4 && (ld % 4) == 0 && (xa % 16) == 0;
+  if (compute_dtype == SKC_F64) return launch_sketch_logp<double>(logp, P, st);
+  if (P.vec && !P.x_f64 && logp >= 2) return launch_gather_logp(logp, P, st);
+  return launch_sketch_logp<float>(logp, P, st);
+}
+
 int sketch_identity(const void* X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, int32_t p_pad,
                     uint64_t master_seed, int64_t col0, int32_t m, int32_t* idx_out, void* val_out,
                     int32_t val_dtype, double* y_out, cudaStream_t st) {

@@ -27,17 +27,30 @@ DEFAULT_CHUNK_COLS = 8192
 COMPUTE = {"f64": _lib.F64, "f32": _lib.F32}
 
 
+SAMPLERS = ("oracle", "philox")
+
+
 @dataclass(frozen=True)
 class SamplingPlan:
-    """Master seed plus (p, m); sketch.py:23-56. Indices are drawn on the GPU."""
+    """Master seed plus (p, m); sketch.py:23-56. Indices are drawn on the GPU.
+
+    ``sampler="oracle"`` (default) is the reference's keyed-hash rule, bit-exact.
+    ``sampler="philox"`` is north_star's counter-based alternative: Floyd's algorithm on a
+    Philox4x32-10 stream (``skc_indices_philox``). It draws from the same distribution
+    (uniform m-subsets), but not the reference's subsets. It is much cheaper on the GPU and
+    is pinned bit for bit against ``oracle/sketch_oracle.c:orc_philox_indices``.
+    """
 
     master_seed: int
     p: int
     m: int
+    sampler: str = "oracle"
 
     def __post_init__(self):
         if not 1 <= self.m <= self.p:
             raise ParameterError(f"need 1 <= m <= p, got m={self.m}, p={self.p}")
+        if self.sampler not in SAMPLERS:
+            raise ParameterError(f"sampler must be one of {SAMPLERS}, got {self.sampler!r}")
 
     @property
     def gamma(self) -> float:
@@ -52,8 +65,8 @@ class SamplingPlan:
         out = torch.empty((max(c, 0), self.m), dtype=torch.int32, device=device or default_device())
         if c > 0:
             with torch.cuda.device(out.device):
-                _lib.call("skc_indices", u64(self.master_seed), int(i0), c, self.p, self.m, out.data_ptr(),
-                          _lib.stream_ptr(out.device))
+                _lib.call("skc_indices" if self.sampler == "oracle" else "skc_indices_philox", u64(self.master_seed),
+                          int(i0), c, self.p, self.m, out.data_ptr(), _lib.stream_ptr(out.device))
         return out
 
     def indices_block(self, i0: int, i1: int) -> np.ndarray:
@@ -222,14 +235,14 @@ def as_source(data, chunk_cols: int = DEFAULT_CHUNK_COLS):
     return ArraySource(data, chunk_cols=chunk_cols)
 
 
-def plan_for(spec: PreconditionSpec, gamma: float, master_seed: int) -> SamplingPlan:
+def plan_for(spec: PreconditionSpec, gamma: float, master_seed: int, sampler: str = "oracle") -> SamplingPlan:
     """Keep round(gamma * p_pad) entries per column; sketch.py:177-184"""
     if not 0 < gamma <= 1:
         raise ParameterError(f"gamma must be in (0, 1], got {gamma}")
     m = int(round(gamma * spec.p_pad))
     if m < 1:
         raise ParameterError(f"gamma={gamma} keeps no entries at p_pad={spec.p_pad}")
-    return SamplingPlan(master_seed=int(master_seed), p=spec.p_pad, m=m)
+    return SamplingPlan(master_seed=int(master_seed), p=spec.p_pad, m=m, sampler=sampler)
 
 
 def _launch_rows(rows: torch.Tensor, spec: PreconditionSpec, plan: SamplingPlan, col0: int, compute: int,
@@ -241,9 +254,31 @@ def _launch_rows(rows: torch.Tensor, spec: PreconditionSpec, plan: SamplingPlan,
     if c == 0:
         return
     with torch.cuda.device(rows.device):
+        st = _lib.stream_ptr(rows.device)
+        if plan.sampler == "philox":
+            _lib.call("skc_indices_philox", u64(plan.master_seed), int(col0), c, plan.p, plan.m, idx_out.data_ptr(), st)
+            sketch_given_rows(rows, spec, plan.m, compute, idx_out, val_out)
+            return
         _lib.call("skc_sketch", rows.data_ptr(), _lib.dtype_code(rows), rows.stride(0), c, spec.p, spec.p_pad,
                   spec.gpu_kind(), u64(spec.sign_seed), u64(plan.master_seed), int(col0), plan.m, compute,
-                  idx_out.data_ptr(), val_out.data_ptr(), _lib.dtype_code(val_out), _lib.stream_ptr(rows.device))
+                  idx_out.data_ptr(), val_out.data_ptr(), _lib.dtype_code(val_out), st)
+
+
+def sketch_given_rows(rows: torch.Tensor, spec: PreconditionSpec, m: int, compute: int, idx_in: torch.Tensor,
+                      val_out: torch.Tensor) -> None:
+    """Values of CUDA rows (c, p) at supplied sorted indices (c, m) int32 (``skc_sketch_given``):
+    oracle mode with reference-supplied indices, or the Philox sampler's."""
+    if rows.stride(1) != 1:
+        rows = rows.contiguous()
+    c = rows.shape[0]
+    if c == 0:
+        return
+    if tuple(idx_in.shape) != (c, m) or idx_in.dtype != torch.int32 or not idx_in.is_contiguous():
+        raise DimensionError(f"indices must be contiguous int32 ({c}, {m})")
+    with torch.cuda.device(rows.device):
+        _lib.call("skc_sketch_given", rows.data_ptr(), _lib.dtype_code(rows), rows.stride(0), c, spec.p, spec.p_pad,
+                  spec.gpu_kind(), u64(spec.sign_seed), m, compute, idx_in.data_ptr(), val_out.data_ptr(),
+                  _lib.dtype_code(val_out), _lib.stream_ptr(rows.device))
 
 
 def device_row_chunks(row_iter, device) -> Iterator[torch.Tensor]:
@@ -294,12 +329,15 @@ def device_row_chunks(row_iter, device) -> Iterator[torch.Tensor]:
 
 
 def sketch_stream(source, spec: PreconditionSpec, plan: SamplingPlan, *, compute: str = "f64",
-                  values_dtype: Optional[torch.dtype] = None, device=None, col0: int = 0) -> SparseSketch:
+                  values_dtype: Optional[torch.dtype] = None, device=None, col0: int = 0,
+                  indices=None) -> SparseSketch:
     """Precondition and sample every column of ``source`` in one pass; sketch.py:196-223.
 
     compute="f64" reproduces the reference values bit for bit. compute="f32" is the
     fast path. Indices are bit-exact in both. ``col0`` offsets the global column index,
-    for a shard of a larger matrix.
+    for a shard of a larger matrix. ``indices`` (n, m), each row strictly increasing,
+    replaces sampling: the values are taken at those coordinates (oracle mode with
+    reference-supplied indices).
     """
     source = as_source(source)
     if source.p != spec.p:
@@ -313,7 +351,18 @@ def sketch_stream(source, spec: PreconditionSpec, plan: SamplingPlan, *, compute
     if values_dtype is None:
         values_dtype = torch.float64 if compute == "f64" else torch.float32
     n = source.n
-    indices = torch.empty((n, plan.m), dtype=torch.int32, device=device)
+    given = indices is not None
+    if given:
+        idx_t = indices if isinstance(indices, torch.Tensor) else torch.from_numpy(np.asarray(indices).astype(np.int64))
+        if tuple(idx_t.shape) != (n, plan.m):
+            raise DimensionError(f"indices must be ({n}, {plan.m}), got {tuple(idx_t.shape)}")
+        if n and (int(idx_t.min()) < 0 or int(idx_t.max()) >= spec.p_pad):
+            raise DimensionError(f"indices must lie in [0, {spec.p_pad})")
+        if n and plan.m > 1 and not bool((idx_t[:, 1:] > idx_t[:, :-1]).all()):
+            raise DimensionError("each row of indices must be strictly increasing")
+        indices = idx_t.to(device=device, dtype=torch.int32).contiguous()
+    else:
+        indices = torch.empty((n, plan.m), dtype=torch.int32, device=device)
     values = torch.empty((n, plan.m), dtype=values_dtype, device=device)
     row_iter = source.row_chunks() if hasattr(source, "row_chunks") else (ch.T for ch in source.chunks())
     j0 = 0
@@ -326,7 +375,10 @@ def sketch_stream(source, spec: PreconditionSpec, plan: SamplingPlan, *, compute
         c = rows.shape[0]
         if j0 + c > n:
             raise DimensionError(f"source yielded more than {n} columns")
-        _launch_rows(rows, spec, plan, col0 + j0, COMPUTE[compute], indices[j0 : j0 + c], values[j0 : j0 + c])
+        if given:
+            sketch_given_rows(rows, spec, plan.m, COMPUTE[compute], indices[j0 : j0 + c], values[j0 : j0 + c])
+        else:
+            _launch_rows(rows, spec, plan, col0 + j0, COMPUTE[compute], indices[j0 : j0 + c], values[j0 : j0 + c])
         j0 += c
     if j0 != n:
         raise DimensionError(f"source yielded {j0} columns, expected {n}")
