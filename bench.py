@@ -257,9 +257,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=None, help="override rows per GPU")
     ap.add_argument("--compute", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--sampler", default="oracle", choices=["oracle", "philox"],
+                    help="oracle: the reference's index rule (bit-exact, headline); philox: north_star's Philox sampler")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-kmeans", action="store_true")
+    ap.add_argument("--no-philox", action="store_true", help="skip the Philox-sampler secondary measurement")
     args = ap.parse_args()
     cfg = dict(WORKLOADS[args.workload])
     if args.n:
@@ -317,6 +320,16 @@ def main():
         st = _lib.stream_ptr(dev)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         stage_names = ["sketch", "moments", "covariance", "finalize"]
+        sampler = args.sampler
+
+        def sketch_call(which):
+            if which == "philox":  # Philox indices, then values at them
+                _lib.call("skc_indices_philox", plan.master_seed, col0, n, p, m, idx.data_ptr(), st)
+                _lib.call("skc_sketch_given", X.data_ptr(), _lib.F32, p, n, p, p, 0, spec.sign_seed, m, vcode,
+                          idx.data_ptr(), val.data_ptr(), vcode, st)
+            else:
+                _lib.call("skc_sketch", X.data_ptr(), _lib.F32, p, n, p, p, 0, spec.sign_seed, plan.master_seed, col0,
+                          m, vcode, idx.data_ptr(), val.data_ptr(), vcode, st)
 
         def step(record):
             acc.zero_()
@@ -324,8 +337,7 @@ def main():
             tri.zero_()
             if record:
                 ev[0].record()
-            _lib.call("skc_sketch", X.data_ptr(), _lib.F32, p, n, p, p, 0, spec.sign_seed, plan.master_seed, col0, m,
-                      vcode, idx.data_ptr(), val.data_ptr(), vcode, st)
+            sketch_call(sampler)
             if record:
                 ev[1].record()
             _lib.call("skc_moments", idx.data_ptr(), val.data_ptr(), vcode, n, m, p, acc.data_ptr(), stats.data_ptr(),
@@ -415,13 +427,13 @@ def main():
                 "algorithmic_bytes_per_launch": dom_bytes}
     if cfg["kind"] == "cov":
         # every stage, and the pass as a whole, against the HBM roofline; K3's own bound is the
-        # shared-memory ATOMS.ADD rate (tools/microbench: 1.23e12 updates/s on this pool's B200)
+        # shared-memory atomic rate (tools/microbench/mb_dsmem: 1.355e12 returning adds/s on this pool's B200)
         per_stage = {k: {"algorithmic_GBps": unit_bytes[k] * n / (stage_ms[k] * 1e-3) / 1e9,
                          "frac_hbm": unit_bytes[k] * n / (stage_ms[k] * 1e-3) / 1e9 / hbm_peak}
                      for k in stage_ms if stage_ms[k] > 0 and unit_bytes[k] > 0}
         upd = n * m * (m + 1) / 2 / (stage_ms["covariance"] * 1e-3)
         per_stage["covariance"]["smem_atomic_updates_per_s"] = upd
-        per_stage["covariance"]["frac_of_measured_atoms_peak"] = upd / 1.226e12
+        per_stage["covariance"]["frac_of_measured_atoms_peak"] = upd / 1.355e12  # mb_dsmem: returning atom.shared
         roofline["stages"] = per_stage
         roofline["pass_frac_hbm"] = (4 * p + 8 * m) * (n / (ms_step * 1e-3)) / 1e9 / hbm_peak
 
@@ -431,6 +443,7 @@ def main():
         "dtype": args.compute if cfg["kind"] == "cov" else "f64",
         "data": "synthetic (seeded, device-generated; BASELINE.json generator shapes)",
         "config": {"workload": args.workload, "desc": cfg["desc"], "p": p, "m": m, "rows_per_gpu": n,
+                   "sampler": args.sampler if cfg["kind"] == "cov" else "oracle",
                    "global_rows": total_samples, "parallelism": f"dp{world}",
                    "l2": "inputs larger than L2 (no flush needed)" if n * p * 4 > 126e6 else "inputs fit L2"},
         "stages_ms": stage_ms,
@@ -438,6 +451,35 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+
+    # secondary: the same pass with north_star's Philox sampler (not reference-identical
+    # indices; pinned to oracle/sketch_oracle.c:orc_philox_indices), same shapes and timing
+    if cfg["kind"] == "cov" and args.sampler == "oracle" and not args.no_philox:
+        sampler = "philox"
+        for _ in range(args.warmup):
+            step(False)
+        barrier()
+        psums = [0.0] * 4
+        ksteps = max(1, min(args.steps, 5))
+        p0 = torch.cuda.Event(enable_timing=True)
+        p1 = torch.cuda.Event(enable_timing=True)
+        p0.record()
+        for _ in range(ksteps):
+            step(True)
+            torch.cuda.synchronize()
+            for i in range(4):
+                psums[i] += ev[i].elapsed_time(ev[i + 1])
+        p1.record()
+        barrier()
+        pms = torch.tensor([p0.elapsed_time(p1) / ksteps], dtype=torch.float64, device=dev)
+        if world > 1:
+            tdist.all_reduce(pms, op=tdist.ReduceOp.MAX)
+        out["philox_mode"] = {
+            "value": n * world / (float(pms.item()) * 1e-3), "unit": unit, "ms_per_step": float(pms.item()),
+            "stages_ms": {k: psums[i] / ksteps for i, k in enumerate(stage_names)},
+            "sketch_frac_hbm": (4 * p + 8 * m) * n / (psums[0] / ksteps * 1e-3) / 1e9 / hbm_peak,
+            "note": "skc_indices_philox + skc_sketch_given; uniform m-subsets, not the reference's subsets"}
+        sampler = args.sampler
 
     # e2e through the public API with pinned host buffers
     if cfg["kind"] == "cov" and not args.no_e2e:

@@ -911,43 +911,69 @@ __global__ void gather_identity_kernel(const void* X, int x_f64, int64_t ld, int
 // for any word indices. ~45 warp-instructions per column at p=1024, m=51.
 constexpr int kPhxThreads = 128;
 
+constexpr int kPhxStageMaxM = 160;  // staged, coalesced output up to here (80 KB); direct stores above
+
 __global__ void __launch_bounds__(kPhxThreads) philox_indices_kernel(uint64_t key, int64_t col0, int64_t n, int32_t p,
                                                                     int32_t m, int32_t* __restrict__ idx_out) {
-  extern __shared__ uint32_t bm[];  // [W][kPhxThreads]
+  extern __shared__ uint32_t bm[];  // [W][kPhxThreads] sets, then [kPhxThreads][S] staged rows
   const int W = (p + 31) >> 5;
-  const int t = threadIdx.x;
+  const int S = m | 1;  // odd stride: conflict-free both when lanes write and when a row is read
+  const bool staged = m <= kPhxStageMaxM;
+  uint32_t* stage = bm + (size_t)W * kPhxThreads;
+  const int t = threadIdx.x, lane = t & 31, wbase = t & ~31;
   const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
-  for (int64_t row = blockIdx.x * (int64_t)kPhxThreads + t; row - t < n; row += (int64_t)gridDim.x * kPhxThreads) {
-    if (row >= n) continue;
-    for (int w = 0; w < W; ++w) bm[w * kPhxThreads + t] = 0u;
-    const uint64_t g = (uint64_t)(col0 + row);
-    for (int s0 = 0; s0 < m; s0 += 4) {
-      const Philox4 r4 = philox4x32_10(Philox4{(uint32_t)(s0 >> 2), (uint32_t)g, (uint32_t)(g >> 32), (uint32_t)kTagPhilox},
-                                       k0, k1);
-      const uint32_t rr[4] = {r4.x, r4.y, r4.z, r4.w};
+  for (int64_t base = blockIdx.x * (int64_t)kPhxThreads; base < n; base += (int64_t)gridDim.x * kPhxThreads) {
+    const int64_t row = base + t;
+    if (row < n) {
+      for (int w = 0; w < W; ++w) bm[w * kPhxThreads + t] = 0u;
+      const uint64_t g = (uint64_t)(col0 + row);
+      for (int s0 = 0; s0 < m; s0 += 4) {
+        const Philox4 r4 = philox4x32_10(
+            Philox4{(uint32_t)(s0 >> 2), (uint32_t)g, (uint32_t)(g >> 32), (uint32_t)kTagPhilox}, k0, k1);
+        const uint32_t rr[4] = {r4.x, r4.y, r4.z, r4.w};
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int s = s0 + q;
-        if (s < m) {
-          const uint32_t j = (uint32_t)(p - m + s);
-          const uint32_t c = __umulhi(rr[q], j + 1u);
-          const uint32_t hit = (bm[(c >> 5) * kPhxThreads + t] >> (c & 31)) & 1u;
-          const uint32_t x = hit ? j : c;
-          bm[(x >> 5) * kPhxThreads + t] |= 1u << (x & 31);
+        for (int q = 0; q < 4; ++q) {
+          const int s = s0 + q;
+          if (s < m) {
+            const uint32_t j = (uint32_t)(p - m + s);
+            const uint32_t c = __umulhi(rr[q], j + 1u);
+            const uint32_t hit = (bm[(c >> 5) * kPhxThreads + t] >> (c & 31)) & 1u;
+            const uint32_t x = hit ? j : c;
+            bm[(x >> 5) * kPhxThreads + t] |= 1u << (x & 31);
+          }
         }
       }
+      // ascending emit with a uniform trip count (m); the word advance is short
+      int w = 0;
+      uint32_t b = bm[t];
+      int32_t* mine = idx_out + row * m;
+      for (int k = 0; k < m; ++k) {
+        while (b == 0u) b = bm[++w * kPhxThreads + t];
+        const uint32_t j = 32u * w + __ffs(b) - 1;
+        if (staged) stage[t * S + k] = j;
+        else mine[k] = (int32_t)j;
+        b &= b - 1u;
+      }
     }
-    int32_t* out = idx_out + row * m;
-    int k = 0;
-    for (int w = 0; w < W; ++w)
-      for (uint32_t b = bm[w * kPhxThreads + t]; b; b &= b - 1) out[k++] = 32 * w + __ffs(b) - 1;
+    if (staged) {
+      __syncwarp();
+      // the warp's 32 rows are contiguous in idx_out: coalesced stores
+      const int64_t r0 = base + wbase;
+      const int64_t left = n - r0;
+      const int rows = left < 32 ? (int)left : 32;
+      int32_t* out = idx_out + r0 * m;
+      for (int r = 0; r < rows; ++r)
+        for (int q = lane; q < m; q += 32) out[r * m + q] = (int32_t)stage[(wbase + r) * S + q];
+      __syncwarp();
+    }
   }
 }
 
 int philox_indices_launch(uint64_t master_seed, int64_t col0, int64_t n, int32_t p, int32_t m, int32_t* idx_out,
                           cudaStream_t st) {
   if (n <= 0) return SKC_OK;
-  const size_t smem = (size_t)((p + 31) / 32) * kPhxThreads * 4;
+  const size_t smem =
+      ((size_t)((p + 31) / 32) * kPhxThreads + (m <= kPhxStageMaxM ? (size_t)kPhxThreads * (m | 1) : 0)) * 4;
   if (cudaFuncSetAttribute(philox_indices_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return check_launch("philox smem attribute");
   int occ = 0;
