@@ -151,6 +151,31 @@ int skc_kmeans_centers(const double *sums, const int64_t *counts, const int64_t 
 int skc_kmeans_reseed(const int32_t *idx_c, const void *val_c, int32_t val_dtype, int32_t m, const int32_t *empty,
                       int32_t p_pad, int32_t K, double *mu, void *stream);
 
+/* The same partial sums through a transposed sketch that is built once and reused every
+ * iteration: per-coordinate lists ascending in point index (a stable counting sort by
+ * coordinate). skc_kmeans_partials_csc then sums each (coordinate, cluster) chain
+ * sequentially in point order, exactly np.bincount's order in cluster.py:203-205, so sums
+ * are bit-identical to the reference. csc: skc_kmeans_csc_workspace bytes (device), kept
+ * alive between the calls; skc_kmeans_partials runs both steps in one call. Per
+ * iteration each coordinate's list is split into segments, labels are counted per
+ * segment, a scan makes every (coordinate, cluster) chain contiguous, values are scattered
+ * stably, and one thread adds each chain in order. */
+size_t skc_kmeans_csc_workspace(int64_t n, int32_t m, int32_t p_pad, int32_t val_dtype);
+int skc_kmeans_build_csc(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m, int32_t p_pad,
+                         void *csc, size_t csc_bytes, void *stream);
+/* seg: skc_kmeans_seg_workspace bytes of per-iteration scratch (labels per entry, the
+ * values in chain order, segment offsets). K <= 256. */
+size_t skc_kmeans_seg_workspace(int64_t n, int32_t m, int32_t p_pad, int32_t K, int32_t val_dtype);
+int skc_kmeans_partials_csc(const void *csc, int32_t val_dtype, int64_t n, int32_t m, int32_t p_pad,
+                            const int32_t *labels, int32_t K, double *sums, int64_t *counts, int64_t *sizes, void *seg,
+                            size_t seg_bytes, void *stream);
+
+/* skc_kmeans_reseed with the point given on the device: row = max(*row, 0) (the argmax that
+ * skc_kmeans_assign writes to out[1]), so a Lloyd iteration can be enqueued before the host
+ * reads its convergence flag. idx/val are the whole (n, m) sketch. */
+int skc_kmeans_reseed_at(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m,
+                         const int64_t *row, const int32_t *empty, int32_t p_pad, int32_t K, double *mu, void *stream);
+
 /* Row norms ||v_i||^2 of the sketch in numpy's pairwise order (the colsq of
  * cluster.py:148). out: (n) fp64 (=). */
 int skc_row_sqnorms(const void *val, int32_t val_dtype, int64_t n, int32_t m, double *out, void *stream);

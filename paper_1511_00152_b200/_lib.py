@@ -55,6 +55,11 @@ SIGNATURES = {
     "skc_kmeans_partials": (_c.c_int, [_P, _P, _I32, _I64, _I32, _P, _I32, _I32, _P, _P, _P, _P, _SZ, _P]),
     "skc_kmeans_centers": (_c.c_int, [_P, _P, _P, _P, _I32, _I32, _P, _P, _P]),
     "skc_kmeans_reseed": (_c.c_int, [_P, _P, _I32, _I32, _P, _I32, _I32, _P, _P]),
+    "skc_kmeans_csc_workspace": (_c.c_size_t, [_I64, _I32, _I32, _I32]),
+    "skc_kmeans_build_csc": (_c.c_int, [_P, _P, _I32, _I64, _I32, _I32, _P, _SZ, _P]),
+    "skc_kmeans_seg_workspace": (_c.c_size_t, [_I64, _I32, _I32, _I32, _I32]),
+    "skc_kmeans_partials_csc": (_c.c_int, [_P, _I32, _I64, _I32, _I32, _P, _I32, _P, _P, _P, _P, _SZ, _P]),
+    "skc_kmeans_reseed_at": (_c.c_int, [_P, _P, _I32, _I64, _I32, _P, _P, _I32, _I32, _P, _P]),
     "skc_indices_philox": (_c.c_int, [_U64, _I64, _I64, _I32, _I32, _P, _P]),
     "skc_sketch_given": (_c.c_int, [_P, _I32, _I64, _I64, _I32, _I32, _I32, _U64, _I32, _I32, _P, _P, _I32, _P]),
     "skc_sketch_pack_records": (_c.c_int, [_P, _P, _I32, _I64, _I32, _P, _P]),

@@ -129,16 +129,26 @@ class SketchKMeans:
                       self._st())
 
     def partials(self, labels: torch.Tensor, K: int):
-        """cluster.py:189-208 partial sums: (sums, counts, sizes) on the device."""
+        """cluster.py:189-208 partial sums: (sums, counts, sizes) on the device.
+
+        Sums follow the reference's sequential order exactly, through the transposed sketch
+        built on first use (``skc_kmeans_build_csc``)."""
         L = _lib.lib()
-        ws = self._workspace("partials", L.skc_kmeans_partials_workspace(self.n, self.m, self.p, K))
+        if "csc" not in self._ws:
+            csc = _lib.workspace(L.skc_kmeans_csc_workspace(self.n, self.m, self.p, self.vcode), self.dev)
+            with torch.cuda.device(self.dev):
+                _lib.call("skc_kmeans_build_csc", self.idx.data_ptr(), self.val.data_ptr(), self.vcode, self.n,
+                          self.m, self.p, csc.data_ptr(), csc.numel(), self._st())
+            self._ws["csc"] = csc
+        csc = self._ws["csc"]
+        seg = self._workspace(("seg", K), L.skc_kmeans_seg_workspace(self.n, self.m, self.p, K, self.vcode))
         sums = torch.empty((self.p, K), dtype=torch.float64, device=self.dev)
         counts = torch.empty((self.p, K), dtype=torch.int64, device=self.dev)
         sizes = torch.empty(K, dtype=torch.int64, device=self.dev)
         with torch.cuda.device(self.dev):
-            _lib.call("skc_kmeans_partials", self.idx.data_ptr(), self.val.data_ptr(), self.vcode, self.n, self.m,
-                      labels.data_ptr(), self.p, K, sums.data_ptr(), counts.data_ptr(), sizes.data_ptr(),
-                      ws.data_ptr(), ws.numel(), self._st())
+            _lib.call("skc_kmeans_partials_csc", csc.data_ptr(), self.vcode, self.n, self.m, self.p, labels.data_ptr(),
+                      K, sums.data_ptr(), counts.data_ptr(), sizes.data_ptr(), seg.data_ptr(), seg.numel(),
+                      self._st())
         return sums, counts, sizes
 
     def centers(self, sums, counts, sizes, mu_prev):
@@ -157,6 +167,13 @@ class SketchKMeans:
         with torch.cuda.device(self.dev):
             _lib.call("skc_kmeans_reseed", idx_row.data_ptr(), val_row.data_ptr(), self.vcode, self.m,
                       empty.data_ptr(), self.p, K, mu.data_ptr(), self._st())
+
+    def reseed_at(self, mu, empty, row: torch.Tensor) -> None:
+        """reseed with the farthest point's row taken from device memory (row: int64[1])."""
+        K = mu.shape[1]
+        with torch.cuda.device(self.dev):
+            _lib.call("skc_kmeans_reseed_at", self.idx.data_ptr(), self.val.data_ptr(), self.vcode, self.n, self.m,
+                      row.data_ptr(), empty.data_ptr(), self.p, K, mu.data_ptr(), self._st())
 
     def update(self, labels: torch.Tensor, mu_prev: torch.Tensor, group=None):
         sums, counts, sizes = self.partials(labels, mu_prev.shape[1])
@@ -179,6 +196,8 @@ def lloyd_loop(ops, mu0: torch.Tensor, max_iter: int, group=None):
     measured with CUDA events).
     """
     w = dist.world(group)
+    if w == 1 and getattr(ops, "dev", torch.device("cpu")).type == "cuda" and hasattr(ops, "reseed_at"):
+        return _lloyd_loop_device(ops, mu0, max_iter)
     mu = mu0.clone()
     n, dev = ops.n, ops.dev
     n_global = n
@@ -239,6 +258,50 @@ def lloyd_loop(ops, mu0: torch.Tensor, max_iter: int, group=None):
         e1.synchronize()
         secs = e0.elapsed_time(e1) * 1e-3
     return cur, mu, traj, iters, secs
+
+
+def _lloyd_loop_device(ops, mu0: torch.Tensor, max_iter: int):
+    """Single-GPU Lloyd loop with one host read per iteration, overlapped with the next step.
+
+    Each iteration enqueues assign + objective, a 32-byte device-to-host copy of
+    (changed, argmax row, objective, max d2), and then, speculatively, the update and the
+    reseed (which takes the argmax row from device memory). The host waits only for the
+    copy; on convergence the speculative centres are discarded. The arithmetic and the
+    trajectory equal lloyd_loop's (cluster.py:230-241).
+    """
+    n, dev = ops.n, ops.dev
+    mu = mu0.clone()
+    lab = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(2)]
+    d2min = torch.empty(n, dtype=torch.float64, device=dev)
+    raw = torch.zeros(32, dtype=torch.uint8, device=dev)
+    out, obj, d2max = raw[0:16].view(torch.int64), raw[16:24].view(torch.float64), raw[24:32].view(torch.float64)
+    host = torch.empty(32, dtype=torch.uint8, pin_memory=True)
+    h_out, h_obj = host[0:16].view(torch.int64), host[16:24].view(torch.float64)
+    ready = torch.cuda.Event()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    traj, iters, prev = [], 0, None
+    cur = lab[0]
+    e0.record()
+    for it in range(max_iter):
+        cur = lab[it % 2]
+        ops.assign(mu, prev, cur, d2min, out, d2max)
+        ops.objective(d2min, obj)
+        host.copy_(raw, non_blocking=True)
+        ready.record()
+        mu_next, _, empty = ops.update(cur, mu)
+        ops.reseed_at(mu_next, empty, out[1:2])
+        ready.synchronize()
+        changed, objective = int(h_out[0]), float(h_obj[0])
+        traj.append(objective)
+        iters += 1
+        if prev is not None and changed == 0:
+            break
+        prev = cur
+        mu = mu_next
+    e1.record()
+    e1.synchronize()
+    return cur, mu, traj, iters, e0.elapsed_time(e1) * 1e-3
 
 
 def _labels_to_device(labels, dev) -> torch.Tensor:

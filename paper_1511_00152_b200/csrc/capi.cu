@@ -43,6 +43,8 @@ int sm_count() {
 int philox_indices_launch(uint64_t, int64_t, int64_t, int32_t, int32_t, int32_t*, cudaStream_t);
 int sketch_given_launch(const void*, int32_t, int64_t, int64_t, int32_t, int32_t, int32_t, uint64_t, int32_t, int32_t,
                         const int32_t*, void*, int32_t, cudaStream_t);
+int reseed_at_launch(const int32_t*, const void*, int, int32_t, const long long*, const int32_t*, int32_t, int32_t,
+                     double*, cudaStream_t);
 int pack_records_launch(const int32_t*, const void*, int, int64_t, int32_t, uint32_t*, cudaStream_t);
 int unpack_records_launch(const uint32_t*, int64_t, int32_t, int32_t*, double*, cudaStream_t);
 size_t dense_sums_ws(int64_t, int32_t, int32_t);
@@ -71,7 +73,12 @@ int assign_launch(const int32_t*, const void*, int, int64_t, int32_t, const doub
                   int32_t*, double*, int64_t*, double*, void*, cudaStream_t);
 int pairwise_launch(const double*, int64_t, double*, void*, cudaStream_t);
 size_t pairwise_ws();
-size_t partials_ws(int64_t, int32_t, int32_t);
+size_t partials_ws(int64_t, int32_t, int32_t, int32_t);
+size_t csc_ws(int64_t, int32_t, int32_t, int);
+size_t seg_ws(int64_t, int32_t, int32_t, int32_t, int);
+int csc_build_launch(const int32_t*, const void*, int, int64_t, int32_t, int32_t, void*, cudaStream_t);
+int csc_partials_launch(const void*, int, int64_t, int32_t, int32_t, const int32_t*, int32_t, double*, int64_t*,
+                        int64_t*, void*, cudaStream_t);
 int partials_check(int32_t, int32_t);
 int partials_launch(const int32_t*, const void*, int, int64_t, int32_t, const int32_t*, int32_t, int32_t, double*,
                     int64_t*, int64_t*, void*, cudaStream_t);
@@ -283,7 +290,7 @@ int skc_pairwise_sum(const double* x, int64_t n, double* out, void* workspace, s
 
 size_t skc_kmeans_partials_workspace(int64_t n, int32_t m, int32_t p_pad, int32_t K) {
   (void)m;
-  return partials_ws(n, p_pad, K);
+  return partials_ws(n, m, p_pad, K);
 }
 
 int skc_kmeans_partials(const int32_t* idx, const void* val, int32_t val_dtype, int64_t n, int32_t m,
@@ -293,7 +300,7 @@ int skc_kmeans_partials(const int32_t* idx, const void* val, int32_t val_dtype, 
   if ((rc = check_dtype(val_dtype))) return rc;
   if (K < 1) return fail(SKC_EPARAM, "K must be >= 1");
   if ((rc = partials_check(p_pad, K))) return rc;
-  if (ws_bytes < partials_ws(n, p_pad, K)) return fail(SKC_EPARAM, "workspace too small");
+  if (ws_bytes < partials_ws(n, m, p_pad, K)) return fail(SKC_EPARAM, "workspace too small");
   return partials_launch(idx, val, val_dtype == SKC_F64, n, m, labels, p_pad, K, sums, counts, sizes, workspace,
                          S(stream));
 }
@@ -309,6 +316,42 @@ int skc_kmeans_reseed(const int32_t* idx_c, const void* val_c, int32_t val_dtype
   int rc;
   if ((rc = check_dtype(val_dtype))) return rc;
   return reseed_launch(idx_c, val_c, val_dtype == SKC_F64, m, empty, p_pad, K, mu, S(stream));
+}
+
+int skc_kmeans_reseed_at(const int32_t* idx, const void* val, int32_t val_dtype, int64_t n, int32_t m,
+                         const int64_t* row, const int32_t* empty, int32_t p_pad, int32_t K, double* mu, void* stream) {
+  int rc;
+  if ((rc = check_dtype(val_dtype))) return rc;
+  if (n < 1) return fail(SKC_EDIM, "empty sketch");
+  return reseed_at_launch(idx, val, val_dtype == SKC_F64, m, reinterpret_cast<const long long*>(row), empty, p_pad, K,
+                          mu, S(stream));
+}
+
+size_t skc_kmeans_csc_workspace(int64_t n, int32_t m, int32_t p_pad, int32_t val_dtype) {
+  return csc_ws(n, m, p_pad, val_dtype == SKC_F64);
+}
+
+int skc_kmeans_build_csc(const int32_t* idx, const void* val, int32_t val_dtype, int64_t n, int32_t m, int32_t p_pad,
+                         void* csc, size_t csc_bytes, void* stream) {
+  int rc;
+  if ((rc = check_dtype(val_dtype))) return rc;
+  if ((rc = partials_check(p_pad, 1))) return rc;
+  if (csc_bytes < csc_ws(n, m, p_pad, val_dtype == SKC_F64)) return fail(SKC_EPARAM, "workspace too small");
+  return csc_build_launch(idx, val, val_dtype == SKC_F64, n, m, p_pad, csc, S(stream));
+}
+
+size_t skc_kmeans_seg_workspace(int64_t n, int32_t m, int32_t p_pad, int32_t K, int32_t val_dtype) {
+  return seg_ws(n, m, p_pad, K, val_dtype == SKC_F64);
+}
+
+int skc_kmeans_partials_csc(const void* csc, int32_t val_dtype, int64_t n, int32_t m, int32_t p_pad,
+                            const int32_t* labels, int32_t K, double* sums, int64_t* counts, int64_t* sizes, void* seg,
+                            size_t seg_bytes, void* stream) {
+  int rc;
+  if ((rc = check_dtype(val_dtype))) return rc;
+  if ((rc = partials_check(p_pad, K))) return rc;
+  if (seg_bytes < seg_ws(n, m, p_pad, K, val_dtype == SKC_F64)) return fail(SKC_EPARAM, "workspace too small");
+  return csc_partials_launch(csc, val_dtype == SKC_F64, n, m, p_pad, labels, K, sums, counts, sizes, seg, S(stream));
 }
 
 int skc_row_sqnorms(const void* val, int32_t val_dtype, int64_t n, int32_t m, double* out, void* stream) {

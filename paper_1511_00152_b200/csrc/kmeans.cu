@@ -2,10 +2,13 @@
 //  assign   exact fp64 emulation of [values | ones] @ [-2 mu ; mu*mu] + colsq
 //           (cluster.py:181-187), so labels and d2min are bit-exact
 //  pairwise numpy pairwise summation of d2min (the objective, cluster.py:233)
-//  partials stable counting sort by label, then fixed-size chunks summed by
-//           warp-private shared-memory vectors; deterministic (cluster.py:189-208)
+//  partials bit-exact np.bincount sums (cluster.py:189-208): the sketch transposed once
+//           into per-coordinate lists; per iteration a segmented stable sort by label
+//           and one sequential add per (coordinate, cluster) chain
 //  centers  divide / keep-previous / empty flags (cluster.py:196-210)
 //  reseed   cluster.py:212-215;  init  cluster.py:175-179
+#include <cub/device/device_scan.cuh>
+
 #include "common.cuh"
 
 namespace skc {
@@ -399,315 +402,348 @@ int assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, i
 }
 
 // ---------------------------------------------------------------------------------
-// partials: stable counting sort by label + chunked warp-private accumulation
-constexpr int kSortBlock = 1024;  // points per histogram/scatter block
-constexpr int kPartWarps = 8;
+// partials (exact): see the transposed-sketch section below
+size_t csc_ws(int64_t n, int32_t m, int32_t p_pad, int val_f64);
+size_t seg_ws(int64_t n, int32_t m, int32_t p_pad, int32_t K, int val_f64);
+int csc_build_launch(const int32_t*, const void*, int, int64_t, int32_t, int32_t, void*, cudaStream_t);
+int csc_partials_launch(const void*, int, int64_t, int32_t, int32_t, const int32_t*, int32_t, double*, int64_t*,
+                        int64_t*, void*, cudaStream_t);
 
-struct PartLayout {
-  int64_t nblk, nchunk_max, ch;
-  size_t off_hist, off_base, off_perm, off_sizes, off_coff, off_cfirst, off_chunks, off_psum, off_pcnt, total;
+// skc_kmeans_partials: the exact path (transpose, then sequential per-chain sums)
+size_t partials_ws(int64_t n, int32_t m, int32_t p_pad, int32_t K) {
+  return ((csc_ws(n, m, p_pad, 1) + 255) & ~(size_t)255) + seg_ws(n, m, p_pad, K, 1);
+}
+int partials_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, const int32_t* labels,
+                    int32_t p_pad, int32_t K, double* sums, int64_t* counts, int64_t* sizes, void* ws,
+                    cudaStream_t st) {
+  int rc = csc_build_launch(idx, val, val_f64, n, m, p_pad, ws, st);
+  if (rc) return rc;
+  char* seg = static_cast<char*>(ws) + ((csc_ws(n, m, p_pad, 1) + 255) & ~(size_t)255);
+  return csc_partials_launch(ws, val_f64, n, m, p_pad, labels, K, sums, counts, sizes, seg, st);
+}
+
+int partials_check(int32_t p_pad, int32_t K) {
+  if ((size_t)p_pad * 8 > 96 * 1024) return fail(SKC_EPARAM, "p_pad too large for the K-means update kernel");
+  if (K > 256) return fail(SKC_EPARAM, "K > 256 is not supported by the exact K-means update (byte labels)");
+  return SKC_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// Exact partials (cluster.py:189-208). sums[j][k] is np.bincount's sum: sequential fp64 in
+// ascending point index over the points labelled k (the stable label sort), at coordinate j.
+// The sketch is transposed once (per sketch) into per-coordinate lists, ascending in point
+// index: a stable counting sort by coordinate, where a warp takes a range of kCscRange
+// points in order. Each iteration one warp walks one coordinate's list 32 entries at a time.
+// Lanes with equal labels (match_any) are folded by their lowest lane, in lane order
+// (= point order), into warp-private acc[k]. Every (j, k) sum is the reference's chain,
+// bit for bit, and the counts come with it.
+constexpr int kCscRange = 2048;
+
+struct CscLayout {
+  int64_t R, nnz;
+  int S;  // segments per coordinate list in the per-iteration label sort
+  size_t off_off, off_rows, off_vals, off_temp, temp_bytes, total;
+  size_t off_kbuf, off_sorted, off_seg, off_stemp, stemp_bytes;
 };
 
-static PartLayout part_layout(int64_t n, int32_t p_pad, int32_t K) {
-  PartLayout L{};
-  L.nblk = (n + kSortBlock - 1) / kSortBlock;
-  if (L.nblk < 1) L.nblk = 1;
-  int64_t ch = n / (2 * (int64_t)sm_count());
-  const int64_t minch = (int64_t)32 * p_pad / 8;  // per-chunk setup ~ W*p words vs ch*m/32 work
-  if (ch < minch) ch = minch;
-  if (ch < 512) ch = 512;
-  if (ch > 32768) ch = 32768;
-  L.ch = ch;
-  L.nchunk_max = (n + ch - 1) / ch + K;
+static CscLayout csc_layout(int64_t n, int32_t m, int32_t p_pad, int val_f64) {
+  CscLayout L{};
+  L.R = (n + kCscRange - 1) / kCscRange;
+  if (L.R < 1) L.R = 1;
+  L.nnz = n * (int64_t)m;
+  const int64_t cells = (int64_t)p_pad * L.R + 1;
+  cub::DeviceScan::ExclusiveSum(nullptr, L.temp_bytes, (int64_t*)nullptr, (int64_t*)nullptr, (int)cells);
   size_t o = 0;
   auto take = [&](size_t bytes) {
-    size_t r = o;
+    const size_t r = o;
     o += (bytes + 255) & ~(size_t)255;
     return r;
   };
-  L.off_hist = take((size_t)L.nblk * K * 4);
-  L.off_base = take((size_t)L.nblk * K * 8);
-  L.off_perm = take((size_t)(n > 0 ? n : 1) * 4);
-  L.off_sizes = take((size_t)K * 8);
-  L.off_coff = take((size_t)(K + 1) * 8);
-  L.off_cfirst = take((size_t)(K + 1) * 8);
-  L.off_chunks = take((size_t)L.nchunk_max * 16);
-  L.off_psum = take((size_t)L.nchunk_max * p_pad * 8);
-  L.off_pcnt = take((size_t)L.nchunk_max * p_pad * 4);
+  L.off_off = take((size_t)cells * 8);
+  L.off_rows = take((size_t)(L.nnz > 0 ? L.nnz : 1) * 4);
+  L.off_vals = take((size_t)(L.nnz > 0 ? L.nnz : 1) * (val_f64 ? 8 : 4));
+  L.off_temp = take(L.temp_bytes);
   L.total = o;
   return L;
 }
 
-size_t partials_ws(int64_t n, int32_t p_pad, int32_t K) { return part_layout(n, p_pad, K).total; }
-
-// hist[k][b] = # points of block b with label k
-__global__ void km_hist_kernel(const int32_t* __restrict__ labels, int64_t n, int K, int64_t nblk,
-                               int32_t* __restrict__ hist) {
-  extern __shared__ int h[];
-  for (int k = threadIdx.x; k < K; k += blockDim.x) h[k] = 0;
-  __syncthreads();
-  const int64_t b = blockIdx.x;
-  for (int64_t i = b * kSortBlock + threadIdx.x; i < min(n, (b + 1) * (int64_t)kSortBlock); i += blockDim.x)
-    atomicAdd(&h[labels[i]], 1);
-  __syncthreads();
-  for (int k = threadIdx.x; k < K; k += blockDim.x) hist[(int64_t)k * nblk + b] = h[k];
+// per-iteration scratch of the exact partials for K clusters (separate from the transpose)
+struct SegLayout {
+  int S;
+  size_t off_kbuf, off_sorted, off_seg, off_temp, temp_bytes, total;
+};
+static SegLayout seg_layout(int64_t n, int32_t m, int32_t p_pad, int32_t K, int val_f64) {
+  SegLayout L{};
+  const int64_t nnz = n * (int64_t)m;
+  const int64_t avg = nnz / (p_pad > 0 ? p_pad : 1);
+  int64_t S = (avg + 1023) / 1024;
+  const int64_t smax = (int64_t)(4 << 20) / ((int64_t)p_pad * K);  // keep p*K*S counters <= 4M
+  if (S > smax) S = smax;
+  if (S < 1) S = 1;
+  L.S = (int)S;
+  const int64_t cells = (int64_t)p_pad * K * S + 1;
+  cub::DeviceScan::ExclusiveSum(nullptr, L.temp_bytes, (int64_t*)nullptr, (int64_t*)nullptr, (int)cells);
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t r = o;
+    o += (bytes + 255) & ~(size_t)255;
+    return r;
+  };
+  L.off_kbuf = take((size_t)(nnz > 0 ? nnz : 1));
+  L.off_sorted = take((size_t)(nnz > 0 ? nnz : 1) * (val_f64 ? 8 : 4));
+  L.off_seg = take((size_t)cells * 8);
+  L.off_temp = take(L.temp_bytes);
+  L.total = o;
+  return L;
 }
 
-// per k: exclusive scan over blocks -> base[k][b]; sizes[k]
-__global__ void km_scan_kernel(const int32_t* __restrict__ hist, int64_t nblk, int64_t* __restrict__ base,
-                               int64_t* __restrict__ sizes) {
-  const int k = blockIdx.x;
-  __shared__ int64_t carry;
-  __shared__ int64_t wsum[32];
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  for (int64_t b0 = 0; b0 < nblk; b0 += blockDim.x) {
-    const int64_t b = b0 + threadIdx.x;
-    int64_t v = b < nblk ? hist[(int64_t)k * nblk + b] : 0;
-    int64_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t y = __shfl_up_sync(kFM, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) wsum[warp] = x;
-    __syncthreads();
-    int64_t before = carry;
-    for (int w = 0; w < warp; ++w) before += wsum[w];
-    if (b < nblk) base[(int64_t)k * nblk + b] = before + x - v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int64_t s = 0;
-      for (int w = 0; w < nwarp; ++w) s += wsum[w];
-      carry += s;
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) sizes[k] = carry;
-}
-
-// cluster offsets, first chunk of each cluster, and the chunk table (cluster-major, fixed
-// chunk length). One block: a warp-cooperative scan over K, then every thread fills the
-// entries of its own clusters.
-__global__ void km_offsets_kernel(const int64_t* __restrict__ sizes, int K, int64_t ch, int64_t nchunk_max,
-                                  int64_t* __restrict__ coff, int64_t* __restrict__ cfirst,
-                                  int64_t* __restrict__ chunks) {
-  __shared__ int64_t carry_s, carry_c;
-  if (threadIdx.x == 0) {
-    carry_s = 0;
-    carry_c = 0;
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  if (threadIdx.x < 32) {
-    for (int k0 = 0; k0 < K; k0 += 32) {
-      const int k = k0 + lane;
-      const int64_t sz = k < K ? sizes[k] : 0;
-      const int64_t nc = (sz + ch - 1) / ch;
-      int64_t is = sz, ic = nc;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t ys = __shfl_up_sync(kFM, is, o), yc = __shfl_up_sync(kFM, ic, o);
-        if (lane >= o) {
-          is += ys;
-          ic += yc;
-        }
-      }
-      if (k < K) {
-        coff[k] = carry_s + is - sz;
-        cfirst[k] = carry_c + ic - nc;
-      }
-      __syncwarp();
-      if (lane == 31) {
-        carry_s += is;
-        carry_c += ic;
-      }
-      __syncwarp();
-    }
-    if (lane == 0) {
-      coff[K] = carry_s;
-      cfirst[K] = carry_c;
-    }
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
-    int64_t c = cfirst[k];
-    for (int64_t s0 = 0; s0 < sizes[k]; s0 += ch, ++c) {
-      chunks[2 * c] = coff[k] + s0;                                             // start in perm
-      chunks[2 * c + 1] = ((int64_t)k << 32) | (uint32_t)min(ch, sizes[k] - s0);  // k | len
-    }
-  }
-  for (int64_t c = cfirst[K] + threadIdx.x; c < nchunk_max; c += blockDim.x) {
-    chunks[2 * c] = 0;
-    chunks[2 * c + 1] = -1;
-  }
-}
-
-// stable scatter: one warp per block walks its points in order
-__global__ void km_scatter_kernel(const int32_t* __restrict__ labels, int64_t n, int K, int64_t nblk,
-                                  const int64_t* __restrict__ base, const int64_t* __restrict__ coff,
-                                  int32_t* __restrict__ perm) {
-  extern __shared__ int64_t run[];
-  const int lane = threadIdx.x;
-  const int64_t b = blockIdx.x;
-  for (int k = lane; k < K; k += 32) run[k] = coff[k] + base[(int64_t)k * nblk + b];
+// counts of range r at coordinate j -> off[j * R + r] (int64, scanned in place afterwards)
+__global__ void km_csc_count_kernel(const int32_t* __restrict__ idx, int64_t n, int m, int32_t p_pad, int64_t R,
+                                    int64_t* __restrict__ off) {
+  extern __shared__ int ccnt[];  // [warps][p_pad]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  int* c = ccnt + (size_t)warp * p_pad;
+  const int64_t r = blockIdx.x * (int64_t)nw + warp;
+  for (int j = lane; j < p_pad; j += 32) c[j] = 0;
   __syncwarp();
-  const int64_t end = min(n, (b + 1) * (int64_t)kSortBlock);
-  for (int64_t i0 = b * kSortBlock; i0 < end; i0 += 32) {
-    const int64_t i = i0 + lane;
-    const bool ok = i < end;
-    const int k = ok ? labels[i] : -1 - lane;
-    const uint32_t same = __match_any_sync(kFM, k);
-    if (ok) {
-      const int rank = __popc(same & lanemask_lt());
-      perm[run[k] + rank] = (int32_t)i;
+  if (r < R) {
+    const int64_t i1 = min(n, (r + 1) * (int64_t)kCscRange);
+    for (int64_t i = r * (int64_t)kCscRange; i < i1; ++i)
+      for (int t = lane; t < m; t += 32) atomicAdd(&c[__ldg(idx + i * m + t)], 1);
+    __syncwarp();
+    for (int j = lane; j < p_pad; j += 32) off[(int64_t)j * R + r] = c[j];
+  }
+}
+
+// stable scatter: range r's entries of coordinate j go to off[j * R + r] ... in point order
+template <typename V>
+__global__ void km_csc_scatter_kernel(const int32_t* __restrict__ idx, const V* __restrict__ val, int64_t n, int m,
+                                      int32_t p_pad, int64_t R, const int64_t* __restrict__ off,
+                                      int32_t* __restrict__ rows, V* __restrict__ vals) {
+  extern __shared__ int64_t cpos[];  // [warps][p_pad]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  int64_t* q = cpos + (size_t)warp * p_pad;
+  const int64_t r = blockIdx.x * (int64_t)nw + warp;
+  if (r >= R) return;
+  for (int j = lane; j < p_pad; j += 32) q[j] = off[(int64_t)j * R + r];
+  __syncwarp();
+  const int64_t i1 = min(n, (r + 1) * (int64_t)kCscRange);
+  for (int64_t i = r * (int64_t)kCscRange; i < i1; ++i) {
+    for (int t = lane; t < m; t += 32) {
+      const int j = __ldg(idx + i * m + t);
+      const int64_t pos = q[j]++;
+      rows[pos] = (int32_t)i;
+      vals[pos] = __ldg(val + i * m + t);
     }
     __syncwarp();
-    if (ok && (same & lanemask_lt()) == 0) run[k] += __popc(same);
-    __syncwarp();
   }
+}
+
+// Per iteration, with each coordinate's list cut into S segments (equal parts per
+// coordinate): (A) a warp per segment gathers the labels (kept per entry) and counts them
+// per cluster; (B) an exclusive scan over [coordinate][cluster][segment] makes every
+// (coordinate, cluster) chain contiguous, in point order; (C) a warp per segment scatters
+// its values stably (match_any ranks); (D) a thread per chain adds it sequentially. The
+// order is np.bincount's, so sums are bit-identical, and thousands of segments / chains
+// keep the GPU busy even at p = 512.
+__device__ __forceinline__ void seg_bounds(const int64_t* __restrict__ off, int64_t R, int64_t j, int S, int s,
+                                           int64_t* a, int64_t* b) {
+  const int64_t e0 = off[j * R], e1 = off[(j + 1) * R];
+  const int64_t len = e1 - e0, seg = (len + S - 1) / S;
+  *a = min(e1, e0 + seg * s);
+  *b = min(e1, e0 + seg * (s + 1));
+}
+
+__global__ void km_seg_hist_kernel(const int64_t* __restrict__ off, int64_t R, const int32_t* __restrict__ rows,
+                                   const int32_t* __restrict__ labels, int32_t p_pad, int K, int S,
+                                   uint8_t* __restrict__ kbuf, int64_t* __restrict__ cnt) {
+  extern __shared__ int hcnt[];  // [warps][K]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  int* h = hcnt + (size_t)warp * K;
+  const int64_t w = blockIdx.x * (int64_t)nw + warp;
+  if (w >= (int64_t)p_pad * S) return;
+  const int64_t j = w / S;
+  const int sg = (int)(w - j * S);
+  for (int k = lane; k < K; k += 32) h[k] = 0;
+  __syncwarp();
+  int64_t a, b;
+  seg_bounds(off, R, j, S, sg, &a, &b);
+  for (int64_t e = a + lane; e < b; e += 32) {
+    const int k = __ldg(labels + __ldg(rows + e));
+    kbuf[e] = (uint8_t)k;
+    atomicAdd(&h[k], 1);
+  }
+  __syncwarp();
+  for (int k = lane; k < K; k += 32) cnt[(j * K + k) * S + sg] = h[k];
 }
 
 template <typename V>
-__global__ void __launch_bounds__(kPartWarps * 32)
-    km_chunk_kernel(const int32_t* __restrict__ idx, const void* __restrict__ val, int m, int32_t p_pad,
-                    const int32_t* __restrict__ perm, const int64_t* __restrict__ chunks, double* __restrict__ psum,
-                    int32_t* __restrict__ pcnt) {
-  extern __shared__ unsigned char sm[];
-  const int c = blockIdx.x;
-  const int64_t meta = chunks[2 * c + 1];
-  if (meta < 0) return;
-  const int64_t start = chunks[2 * c];
-  const int len = (int)(meta & 0xFFFFFFFF);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* ws = reinterpret_cast<double*>(sm) + (size_t)warp * p_pad;
-  int* wc = reinterpret_cast<int*>(sm + (size_t)kPartWarps * p_pad * 8) + (size_t)warp * p_pad;
-  for (int j = lane; j < p_pad; j += 32) {
-    ws[j] = 0.0;
-    wc[j] = 0;
-  }
+__global__ void km_seg_scatter_kernel(const int64_t* __restrict__ off, int64_t R, const V* __restrict__ vals,
+                                      const uint8_t* __restrict__ kbuf, int32_t p_pad, int K, int S,
+                                      const int64_t* __restrict__ pos0, V* __restrict__ sorted) {
+  extern __shared__ int64_t run[];  // [warps][K]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  int64_t* q = run + (size_t)warp * K;
+  const int64_t w = blockIdx.x * (int64_t)nw + warp;
+  if (w >= (int64_t)p_pad * S) return;
+  const int64_t j = w / S;
+  const int sg = (int)(w - j * S);
+  for (int k = lane; k < K; k += 32) q[k] = pos0[(j * K + k) * S + sg];
   __syncwarp();
-  const int q0 = len * warp / kPartWarps, q1 = len * (warp + 1) / kPartWarps;
-  int q = q0;
-  if (m <= 64) {  // batches of 4 points: perm and row loads issued before the updates
-    for (; q + 4 <= q1; q += 4) {
-      int64_t pi[4];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) pi[b] = perm[start + q + b];
-      int jj[4][2];
-      double vv[4][2];
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int c2 = 0; c2 < 2; ++c2) {
-          const int t = lane + 32 * c2;
-          jj[b][c2] = -1;
-          if (t < m) {
-            jj[b][c2] = __ldg(idx + pi[b] * m + t);
-            vv[b][c2] = ldd<V>(val, pi[b] * m + t);
-          }
-        }
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-#pragma unroll
-        for (int c2 = 0; c2 < 2; ++c2)
-          if (jj[b][c2] >= 0) {
-            ws[jj[b][c2]] = dadd(ws[jj[b][c2]], vv[b][c2]);
-            wc[jj[b][c2]] += 1;
-          }
-        __syncwarp();
-      }
-    }
-  }
-  for (; q < q1; ++q) {
-    const int64_t i = perm[start + q];
-    for (int t = lane; t < m; t += 32) {
-      const int j = __ldg(idx + i * m + t);
-      ws[j] = dadd(ws[j], ldd<V>(val, i * m + t));
-      wc[j] += 1;
+  int64_t a, b;
+  seg_bounds(off, R, j, S, sg, &a, &b);
+  for (int64_t base = a; base < b; base += 32) {
+    const int64_t e = base + lane;
+    const int k = e < b ? (int)kbuf[e] : -1;
+    const uint32_t peers = __match_any_sync(kFM, k);
+    if (k >= 0) {
+      const int64_t at = q[k] + __popc(peers & lanemask_lt());
+      sorted[at] = vals[e];
     }
     __syncwarp();
+    if (k >= 0 && (peers & lanemask_lt()) == 0) q[k] += __popc(peers);
+    __syncwarp();
   }
+}
+
+// A thread adds one chain in order. Loads run one 16-value block ahead of the adds
+// (software pipeline). One warp per CTA spreads the few chains of a small problem over
+// every SM.
+template <typename V>
+__global__ void km_chain_sum_kernel(const int64_t* __restrict__ pos0, const V* __restrict__ sorted, int32_t p_pad,
+                                    int K, int S, double* __restrict__ sums, int64_t* __restrict__ counts) {
+  constexpr int B = 16;
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // chain = j * K + k
+  if (c >= (int64_t)p_pad * K) return;
+  const int64_t a = pos0[c * S], b = pos0[(c + 1) * S];
+  double acc = 0.0;
+  double cur[B], nxt[B];
+#pragma unroll
+  for (int u = 0; u < B; ++u) cur[u] = a + u < b ? (double)__ldg(sorted + a + u) : 0.0;
+  for (int64_t e = a; e < b; e += B) {
+#pragma unroll
+    for (int u = 0; u < B; ++u) nxt[u] = e + B + u < b ? (double)__ldg(sorted + e + B + u) : 0.0;
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+      if (e + u < b) acc = dadd(acc, cur[u]);
+#pragma unroll
+    for (int u = 0; u < B; ++u) cur[u] = nxt[u];
+  }
+  sums[c] = acc;
+  counts[c] = b - a;
+}
+
+// cluster sizes: bincount(labels), exact
+__global__ void km_sizes_kernel(const int32_t* __restrict__ labels, int64_t n, int K, int64_t* __restrict__ sizes) {
+  extern __shared__ int hs[];
+  for (int k = threadIdx.x; k < K; k += blockDim.x) hs[k] = 0;
   __syncthreads();
-  double* os = psum + (size_t)c * p_pad;
-  int32_t* oc = pcnt + (size_t)c * p_pad;
-  for (int j = threadIdx.x; j < p_pad; j += blockDim.x) {
-    double s = 0.0;
-    int cnt = 0;
-    for (int w = 0; w < kPartWarps; ++w) {
-      s = dadd(s, reinterpret_cast<double*>(sm)[(size_t)w * p_pad + j]);
-      cnt += reinterpret_cast<int*>(sm + (size_t)kPartWarps * p_pad * 8)[(size_t)w * p_pad + j];
-    }
-    os[j] = s;
-    oc[j] = cnt;
-  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&hs[labels[i]], 1);
+  __syncthreads();
+  for (int k = threadIdx.x; k < K; k += blockDim.x)
+    if (hs[k]) atomicAdd(reinterpret_cast<unsigned long long*>(sizes) + k, (unsigned long long)hs[k]);
 }
 
-// sums[j][k] / counts[j][k]: chunks of cluster k added in order
-__global__ void km_chunk_reduce_kernel(const double* __restrict__ psum, const int32_t* __restrict__ pcnt,
-                                       const int64_t* __restrict__ cfirst, int32_t p_pad, int K,
-                                       double* __restrict__ sums, int64_t* __restrict__ counts) {
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= (int64_t)p_pad * K) return;
-  const int j = (int)(e / K), k = (int)(e % K);
-  double s = 0.0;
-  int64_t cnt = 0;
-  for (int64_t c = cfirst[k]; c < cfirst[k + 1]; ++c) {
-    s = dadd(s, psum[(size_t)c * p_pad + j]);
-    cnt += pcnt[(size_t)c * p_pad + j];
-  }
-  sums[e] = s;
-  counts[e] = cnt;
+size_t csc_ws(int64_t n, int32_t m, int32_t p_pad, int val_f64) { return csc_layout(n, m, p_pad, val_f64).total; }
+
+static int csc_warps_for(int32_t p_pad, size_t bytes_per) {
+  int w = 4;
+  while (w > 1 && (size_t)w * p_pad * bytes_per > 96 * 1024) w >>= 1;
+  return w;
 }
 
-int partials_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, const int32_t* labels,
-                    int32_t p_pad, int32_t K, double* sums, int64_t* counts, int64_t* sizes, void* ws,
-                    cudaStream_t st) {
-  const PartLayout L = part_layout(n, p_pad, K);
+int csc_build_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, int32_t p_pad, void* ws,
+                     cudaStream_t st) {
+  const CscLayout L = csc_layout(n, m, p_pad, val_f64);
   char* w = reinterpret_cast<char*>(ws);
-  int32_t* hist = reinterpret_cast<int32_t*>(w + L.off_hist);
-  int64_t* base = reinterpret_cast<int64_t*>(w + L.off_base);
-  int32_t* perm = reinterpret_cast<int32_t*>(w + L.off_perm);
-  int64_t* coff = reinterpret_cast<int64_t*>(w + L.off_coff);
-  int64_t* cfirst = reinterpret_cast<int64_t*>(w + L.off_cfirst);
-  int64_t* chunks = reinterpret_cast<int64_t*>(w + L.off_chunks);
-  double* psum = reinterpret_cast<double*>(w + L.off_psum);
-  int32_t* pcnt = reinterpret_cast<int32_t*>(w + L.off_pcnt);
+  int64_t* off = reinterpret_cast<int64_t*>(w + L.off_off);
+  const int64_t cells = (int64_t)p_pad * L.R + 1;
+  cudaMemsetAsync(off, 0, (size_t)cells * 8, st);
   int rc;
-  const size_t hsm = (size_t)K * 4;
-  cudaFuncSetAttribute(km_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
   if (n > 0) {
-    km_hist_kernel<<<(unsigned)L.nblk, 256, hsm, st>>>(labels, n, K, L.nblk, hist);
-    if ((rc = check_launch("km_hist_kernel"))) return rc;
-  } else {
-    cudaMemsetAsync(hist, 0, (size_t)L.nblk * K * 4, st);
+    const int wc = csc_warps_for(p_pad, 4);
+    const size_t smc = (size_t)wc * p_pad * 4;
+    cudaFuncSetAttribute(km_csc_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
+    km_csc_count_kernel<<<(unsigned)((L.R + wc - 1) / wc), wc * 32, smc, st>>>(idx, n, m, p_pad, L.R, off);
+    if ((rc = check_launch("km_csc_count_kernel"))) return rc;
   }
-  km_scan_kernel<<<K, 256, 0, st>>>(hist, L.nblk, base, sizes);
-  if ((rc = check_launch("km_scan_kernel"))) return rc;
-  km_offsets_kernel<<<1, 1024, 0, st>>>(sizes, K, L.ch, L.nchunk_max, coff, cfirst, chunks);
-  if ((rc = check_launch("km_offsets_kernel"))) return rc;
+  size_t tb = L.temp_bytes;
+  if (cub::DeviceScan::ExclusiveSum(w + L.off_temp, tb, off, off, (int)cells, st) != cudaSuccess)
+    return check_launch("csc offsets scan");
   if (n > 0) {
-    const size_t ssm = (size_t)K * 8;
-    cudaFuncSetAttribute(km_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
-    km_scatter_kernel<<<(unsigned)L.nblk, 32, ssm, st>>>(labels, n, K, L.nblk, base, coff, perm);
-    if ((rc = check_launch("km_scatter_kernel"))) return rc;
-    const size_t csm = (size_t)kPartWarps * p_pad * 12;
-    auto kk = val_f64 ? km_chunk_kernel<double> : km_chunk_kernel<float>;
-    cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
-    kk<<<(unsigned)L.nchunk_max, kPartWarps * 32, csm, st>>>(idx, val, m, p_pad, perm, chunks, psum, pcnt);
-    if ((rc = check_launch("km_chunk_kernel"))) return rc;
+    const int ws_ = csc_warps_for(p_pad, 8);
+    const size_t sms = (size_t)ws_ * p_pad * 8;
+    const unsigned grid = (unsigned)((L.R + ws_ - 1) / ws_);
+    if (val_f64) {
+      cudaFuncSetAttribute(km_csc_scatter_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms);
+      km_csc_scatter_kernel<double><<<grid, ws_ * 32, sms, st>>>(idx, (const double*)val, n, m, p_pad, L.R, off,
+                                                                  reinterpret_cast<int32_t*>(w + L.off_rows),
+                                                                  reinterpret_cast<double*>(w + L.off_vals));
+    } else {
+      cudaFuncSetAttribute(km_csc_scatter_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms);
+      km_csc_scatter_kernel<float><<<grid, ws_ * 32, sms, st>>>(idx, (const float*)val, n, m, p_pad, L.R, off,
+                                                                reinterpret_cast<int32_t*>(w + L.off_rows),
+                                                                reinterpret_cast<float*>(w + L.off_vals));
+    }
+    if ((rc = check_launch("km_csc_scatter_kernel"))) return rc;
   }
-  const int64_t tot = (int64_t)p_pad * K;
-  km_chunk_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(psum, pcnt, cfirst, p_pad, K, sums,
-                                                                          counts);
-  return check_launch("km_chunk_reduce_kernel");
+  return SKC_OK;
 }
 
-int partials_check(int32_t p_pad, int32_t K) {
-  if ((size_t)kPartWarps * p_pad * 12 > 227 * 1024)
-    return fail(SKC_EPARAM, "p_pad too large for the K-means update kernel");
-  if ((size_t)K * 8 > 227 * 1024) return fail(SKC_EPARAM, "K too large for the K-means update kernel");
+size_t seg_ws(int64_t n, int32_t m, int32_t p_pad, int32_t K, int val_f64) {
+  return seg_layout(n, m, p_pad, K, val_f64).total;
+}
+
+int csc_partials_launch(const void* ws, int val_f64, int64_t n, int32_t m, int32_t p_pad, const int32_t* labels,
+                        int32_t K, double* sums, int64_t* counts, int64_t* sizes, void* seg_ws_ptr, cudaStream_t st) {
+  const CscLayout L = csc_layout(n, m, p_pad, val_f64);
+  const SegLayout G = seg_layout(n, m, p_pad, K, val_f64);
+  const char* w = reinterpret_cast<const char*>(ws);
+  char* g = reinterpret_cast<char*>(seg_ws_ptr);
+  const int64_t* off = reinterpret_cast<const int64_t*>(w + L.off_off);
+  const int32_t* rows = reinterpret_cast<const int32_t*>(w + L.off_rows);
+  uint8_t* kbuf = reinterpret_cast<uint8_t*>(g + G.off_kbuf);
+  int64_t* seg = reinterpret_cast<int64_t*>(g + G.off_seg);
+  const int S = G.S;
+  const int64_t items = (int64_t)p_pad * S;
+  const int64_t cells = (int64_t)p_pad * K * S + 1;
+  constexpr int kW = 4;  // warps per CTA (one segment each)
+  const unsigned grid = (unsigned)((items + kW - 1) / kW);
+  int rc;
+  cudaMemsetAsync(seg + cells - 1, 0, 8, st);
+  cudaFuncSetAttribute(km_seg_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kW * K * 4));
+  km_seg_hist_kernel<<<grid, kW * 32, (size_t)kW * K * 4, st>>>(off, L.R, rows, labels, p_pad, K, S, kbuf, seg);
+  if ((rc = check_launch("km_seg_hist_kernel"))) return rc;
+  size_t tb = G.temp_bytes;
+  if (cub::DeviceScan::ExclusiveSum(g + G.off_temp, tb, seg, seg, (int)cells, st) != cudaSuccess)
+    return check_launch("segment offsets scan");
+  const size_t ssm = (size_t)kW * K * 8;
+  const unsigned cgrid = (unsigned)(((int64_t)p_pad * K + 31) / 32);  // one warp (32 chains) per CTA
+  if (val_f64) {
+    const double* vals = reinterpret_cast<const double*>(w + L.off_vals);
+    double* sorted = reinterpret_cast<double*>(g + G.off_sorted);
+    cudaFuncSetAttribute(km_seg_scatter_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+    km_seg_scatter_kernel<double><<<grid, kW * 32, ssm, st>>>(off, L.R, vals, kbuf, p_pad, K, S, seg, sorted);
+    if ((rc = check_launch("km_seg_scatter_kernel"))) return rc;
+    km_chain_sum_kernel<double><<<cgrid, 32, 0, st>>>(seg, sorted, p_pad, K, S, sums, counts);
+  } else {
+    const float* vals = reinterpret_cast<const float*>(w + L.off_vals);
+    float* sorted = reinterpret_cast<float*>(g + G.off_sorted);
+    cudaFuncSetAttribute(km_seg_scatter_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+    km_seg_scatter_kernel<float><<<grid, kW * 32, ssm, st>>>(off, L.R, vals, kbuf, p_pad, K, S, seg, sorted);
+    if ((rc = check_launch("km_seg_scatter_kernel"))) return rc;
+    km_chain_sum_kernel<float><<<cgrid, 32, 0, st>>>(seg, sorted, p_pad, K, S, sums, counts);
+  }
+  if ((rc = check_launch("km_chain_sum_kernel"))) return rc;
+  cudaMemsetAsync(sizes, 0, (size_t)K * 8, st);
+  if (n > 0) {
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 4LL * sm_count()) blocks = 4LL * sm_count();
+    cudaFuncSetAttribute(km_sizes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(K * 4));
+    km_sizes_kernel<<<(unsigned)blocks, 256, (size_t)K * 4, st>>>(labels, n, K, sizes);
+    if ((rc = check_launch("km_sizes_kernel"))) return rc;
+  }
   return SKC_OK;
 }
 
@@ -740,6 +776,27 @@ __global__ void km_reseed_kernel(const int32_t* __restrict__ idx_c, const void* 
   for (int j = threadIdx.x; j < p_pad; j += blockDim.x) mu[(int64_t)j * K + k] = 0.0;
   __syncthreads();
   for (int t = threadIdx.x; t < m; t += blockDim.x) mu[(int64_t)idx_c[t] * K + k] = ldd<V>(val_c, t);
+}
+
+// the same with the farthest point's row read from device memory (*row, clamped at 0),
+// so the Lloyd loop can enqueue the reseed before the host has read the argmax
+template <typename V>
+__global__ void km_reseed_at_kernel(const int32_t* __restrict__ idx, const void* __restrict__ val, int m,
+                                    const long long* __restrict__ row, const int32_t* __restrict__ empty,
+                                    int32_t p_pad, int K, double* __restrict__ mu) {
+  const int k = blockIdx.x;
+  if (!empty[k]) return;
+  const long long r = *row > 0 ? *row : 0;
+  for (int j = threadIdx.x; j < p_pad; j += blockDim.x) mu[(int64_t)j * K + k] = 0.0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < m; t += blockDim.x) mu[(int64_t)idx[r * m + t] * K + k] = ldd<V>(val, r * m + t);
+}
+
+int reseed_at_launch(const int32_t* idx, const void* val, int val_f64, int32_t m, const long long* row,
+                     const int32_t* empty, int32_t p_pad, int32_t K, double* mu, cudaStream_t st) {
+  if (val_f64) km_reseed_at_kernel<double><<<K, 256, 0, st>>>(idx, val, m, row, empty, p_pad, K, mu);
+  else km_reseed_at_kernel<float><<<K, 256, 0, st>>>(idx, val, m, row, empty, p_pad, K, mu);
+  return check_launch("km_reseed_at_kernel");
 }
 
 int reseed_launch(const int32_t* idx_c, const void* val_c, int val_f64, int32_t m, const int32_t* empty,
