@@ -642,11 +642,19 @@ __global__ void __launch_bounds__(kThreads, 2) gather_kernel(const SketchParams 
     } else {
       asm volatile("cp.async.wait_all;" ::: "memory");
     }
+    const int64_t row0 = tile * G::S;
+    const int64_t rows_left = P.n - row0;
+    // this warp's first sample's indices load during the transform (m <= 64 in registers)
+    int pj0 = 0, pj1 = 0;
+    if (warp < G::S && warp < rows_left && P.m <= 64) {
+      const int64_t o = (row0 + warp) * P.m;
+      const int lane = threadIdx.x & 31;
+      if (lane < P.m) pj0 = __ldg(P.idx_in + o + lane);
+      if (lane + 32 < P.m) pj1 = __ldg(P.idx_in + o + lane + 32);
+    }
     __syncthreads();  // tile in buf visible to all; signs visible
     float* xs = reinterpret_cast<float*>(smem + buf * kTileBytes);
     wht_all_windows<LOGP, float, 0>(xs, P.use_signs ? sgn : nullptr, scale);
-    const int64_t row0 = tile * G::S;
-    const int64_t rows_left = P.n - row0;
     if (P.y_out) {
       for (int f = threadIdx.x; f < kTileElems; f += kThreads) {
         const int s = f >> LOGP, i = f & (G::P - 1);
@@ -655,8 +663,14 @@ __global__ void __launch_bounds__(kThreads, 2) gather_kernel(const SketchParams 
     }
     for (int s = warp; s < G::S && s < rows_left; s += kWarps) {
       const int64_t o = (row0 + s) * P.m;
-      for (int t = threadIdx.x & 31; t < P.m; t += 32)
-        store_val<float>(P.val_out, o + t, y_at<LOGP, float>(xs, s, __ldg(P.idx_in + o + t)), P.val_f64);
+      const int lane = threadIdx.x & 31;
+      if (s == warp && P.m <= 64) {
+        if (lane < P.m) store_val<float>(P.val_out, o + lane, y_at<LOGP, float>(xs, s, pj0), P.val_f64);
+        if (lane + 32 < P.m) store_val<float>(P.val_out, o + lane + 32, y_at<LOGP, float>(xs, s, pj1), P.val_f64);
+      } else {
+        for (int t = lane; t < P.m; t += 32)
+          store_val<float>(P.val_out, o + t, y_at<LOGP, float>(xs, s, __ldg(P.idx_in + o + t)), P.val_f64);
+      }
     }
     __syncthreads();  // buf is refilled by the copies issued next iteration
   }
