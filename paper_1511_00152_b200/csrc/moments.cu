@@ -423,6 +423,101 @@ __global__ void cov_reduce_kernel(const unsigned long long* __restrict__ part, i
   tri[e] = dadd(tri[e], (double)s * ldexp(1.0, -S));
 }
 
+// ======================================================================================
+// K3g: no bands. The triangle is an L2-resident int64 fixed-point array (p = 4096: 67 MB),
+// and each product goes in with one red.global.add.u64: no carry logic, still exact and
+// order-independent. A row is visited once: one warp per row enumerates all m(m+1)/2 pairs
+// flatly (row x folded with row m-1-x into width m+1). For large p_pad the banded kernel's
+// per-visit overhead dominates (p = 4096: 153 bands, ~22 products per visit), and this
+// path replaces it (cov_launch chooses by band count).
+// ======================================================================================
+constexpr int kCovGWarps = 8;
+constexpr int kCovGlobalBands = 24;  // more bands than this: the global path (tools/cov_probe.py crossover)
+
+template <typename V>
+__global__ void __launch_bounds__(kCovGWarps * 32) cov_global_kernel(const int32_t* __restrict__ idx,
+                                                                    const V* __restrict__ val, int64_t n, int m,
+                                                                    int32_t p_pad, const double* __restrict__ stats,
+                                                                    unsigned long long* __restrict__ acc) {
+  extern __shared__ int2 gst[];  // per warp: T[m] = (tri_off(j) - j, w * 2^S), U[m] = (j, w)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int2* T = gst + (size_t)warp * 2 * m;
+  int2* U = T + m;
+  double tau;
+  const int S = cov_scale(stats, m, &tau);
+  const float scale_a = (float)ldexp(1.0, S);
+  const double full_s = ldexp(1.0, S);
+  const float ftau = (float)tau;
+  const int Lp = m + 1;
+  const int F = m * (m + 1) / 2;
+  float inv;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"((float)Lp));
+  const int64_t warps = (int64_t)gridDim.x * kCovGWarps;
+  for (int64_t r = blockIdx.x * (int64_t)kCovGWarps + warp; r < n; r += warps) {
+    const int32_t* ir = idx + r * m;
+    const V* vr = val + r * m;
+    bool big = false;
+    for (int t = lane; t < m; t += 32) {
+      const int j = __ldg(ir + t);
+      const float w = (float)__ldg(vr + t);
+      big |= fabsf(w) > ftau;
+      U[t] = make_int2(j, __float_as_int(w));
+      T[t] = make_int2((int)(tri_off(j, p_pad) - j), __float_as_int(w * scale_a));
+    }
+    const bool any_big = __any_sync(kFullMask, big);
+    __syncwarp();
+    if (!any_big) {
+      float ff = (float)lane + 0.5f;
+      for (int f = lane; f < F; f += 32, ff += 32.0f) {
+        int rr = (int)(ff * inv);
+        int c = f - rr * Lp;
+        if (c < 0) c += Lp, --rr;  // guard the approximate reciprocal
+        if (c >= Lp) c -= Lp, ++rr;
+        const bool first = c < m - rr;
+        const int t = first ? rr : m - 1 - rr;
+        const int u = first ? rr + c : c - 1;
+        const int2 tt = T[t], uu = U[u];
+        const long long q = __float2ll_rn(__int_as_float(tt.y) * __int_as_float(uu.y));
+        asm volatile("red.global.add.u64 [%0], %1;" ::"l"(acc + (tt.x + uu.x)), "l"(q) : "memory");
+      }
+    } else {  // a value above tau: exact fp64 products
+      for (int t = 0; t < m; ++t) {
+        const double va = (double)__ldg(vr + t);
+        const int base = T[t].x;
+        for (int u = t + lane; u < m; u += 32) {
+          const long long q = __double2ll_rn(dmul(dmul(va, (double)__ldg(vr + u)), full_s));
+          asm volatile("red.global.add.u64 [%0], %1;" ::"l"(acc + (base + U[u].x)), "l"(q) : "memory");
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+static int cov_launch_global(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, int32_t p_pad,
+                             const double* stats, double* tri, void* ws, cudaStream_t st) {
+  const int64_t total = tri_off(p_pad, p_pad);
+  unsigned long long* acc = reinterpret_cast<unsigned long long*>(ws);
+  cudaMemsetAsync(acc, 0, (size_t)total * 8, st);
+  const size_t smem = (size_t)kCovGWarps * 2 * m * sizeof(int2);
+  int64_t grid = (n + kCovGWarps - 1) / kCovGWarps;
+  const int64_t cap = 8LL * sm_count();
+  if (grid > cap) grid = cap;
+  int rc;
+  if (val_f64) {
+    cudaFuncSetAttribute(cov_global_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cov_global_kernel<double><<<(unsigned)grid, kCovGWarps * 32, smem, st>>>(idx, (const double*)val, n, m, p_pad,
+                                                                              stats, acc);
+  } else {
+    cudaFuncSetAttribute(cov_global_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cov_global_kernel<float><<<(unsigned)grid, kCovGWarps * 32, smem, st>>>(idx, (const float*)val, n, m, p_pad,
+                                                                            stats, acc);
+  }
+  if ((rc = check_launch("cov_global_kernel"))) return rc;
+  cov_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(acc, 1, total, m, stats, tri);
+  return check_launch("cov_reduce_kernel");
+}
+
 static int cov_groups(int nbands, int64_t n) {
   int g = sm_count() / nbands;
   if (g < 1) g = 1;
@@ -478,6 +573,12 @@ static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int
 
 int cov_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, int32_t p_pad,
                const double* stats, double* tri, void* ws, cudaStream_t st) {
+  if (n == 0) return SKC_OK;
+  // path: banded shared-memory accumulation, or (many bands) the L2-resident global path
+  const int nbands = make_bands(p_pad, band_capacity(m, p_pad), nullptr);
+  const char* force = getenv("SKC_COV_PATH");
+  const bool global = force ? force[0] == 'g' : nbands > kCovGlobalBands;
+  if (global) return cov_launch_global(idx, val, val_f64, n, m, p_pad, stats, tri, ws, st);
   // the kernel addresses a group's rows with 32-bit element offsets: split huge inputs
   const int groups = cov_groups(make_bands(p_pad, band_capacity(m, p_pad), nullptr), n);
   int64_t max_rows = (int64_t)groups * ((((int64_t)1 << 31) / m) - kCovWarps);

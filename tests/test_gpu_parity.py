@@ -257,6 +257,25 @@ def test_covariance_heavy_tails_and_determinism(skc):
     assert rel_fro(C1, Co) < 1e-6
 
 
+@pytest.mark.parametrize("p,m", [(512, 26), (2048, 40)])
+def test_covariance_paths_bit_identical(skc, monkeypatch, p, m):
+    # banded shared-memory accumulation and the L2-resident global path sum the same
+    # fixed-point integers: the results are bit-identical, including the outlier path
+    rng = np.random.default_rng(p)
+    n = 6000
+    X = (rng.standard_t(3, size=(p, n)) / np.sqrt(3.0)).astype(np.float32)
+    X[:, 7] *= 1e3
+    spec = skc.PreconditionSpec.create("hadamard", p, 1)
+    sk = skc.sketch_stream(X, spec, skc.SamplingPlan(2, p, m), compute="f32")
+    monkeypatch.setenv("SKC_COV_PATH", "band")
+    Cb = skc.estimate_covariance(sk).matrix
+    monkeypatch.setenv("SKC_COV_PATH", "global")
+    Cg = skc.estimate_covariance(sk).matrix
+    assert np.array_equal(Cb, Cg)
+    Co = O.estimate_covariance(sk.host_indices(), sk.host_values().astype(np.float64), p, nthreads=8)
+    assert rel_fro(Cg, Co) < 1e-6
+
+
 def test_covariance_split_launches(skc, monkeypatch):
     # inputs beyond 2^31 elements per row group run as several launches; force the split
     # on a small input (fixed-point sums per launch, fp64 sum of launches: 1e-12)
