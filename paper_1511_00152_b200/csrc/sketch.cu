@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 3) sketch_kernel(const SketchParams 
 // copies are in flight while tile k is transformed and its values gathered, so the kernel
 // streams at HBM rate instead of exposing each tile's load latency.
 template <int LOGP>
-__global__ void __launch_bounds__(kThreads, 2) gather_kernel(const SketchParams P) {
+__global__ void __launch_bounds__(kThreads, 3) gather_kernel(const SketchParams P) {
   using G = Geo<LOGP>;
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr size_t kTileBytes = sizeof(float) * ((G::WORDS + 3) & ~3);
