@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import ParameterError
+from .errors import DimensionError, ParameterError
 from .sketch import SparseSketch
 from .transform import default_device, u64, unprecondition
 
@@ -72,6 +72,45 @@ def accumulate_moments(sketch: SparseSketch, covariance: bool = True, into: Opti
             _lib.call("skc_cov_accumulate", idx.data_ptr(), val.data_ptr(), vcode, n, m, p, into.stats.data_ptr(),
                       into.tri.data_ptr(), ws2.data_ptr(), ws2.numel(), st)
     into.n += n
+    return into
+
+
+def stream_moments(source, spec, plan, *, covariance: bool = True, compute: str = "f32", device=None,
+                   col0: int = 0, into: Optional[Moments] = None) -> Moments:
+    """Sketch and accumulate the estimators' partial sums chunk by chunk, without keeping the
+    sketch (sketch.py:196-223 then estimators.py:30-66).
+
+    Host chunks reach the device through pinned, double-buffered copies on a copy stream
+    (``sketch.device_row_chunks``). Each chunk's K1 / K2 / K3 run on the compute stream while
+    the next chunk is in flight, so an end-to-end covariance from host data runs at the
+    PCIe rate. K3's fixed-point scale follows the statistics accumulated so far; every
+    chunk's sum is exact in its own quantum and the chunks add in fp64.
+    """
+    from .sketch import COMPUTE, _launch_rows, as_source, device_row_chunks
+
+    source = as_source(source)
+    if source.p != spec.p:
+        raise DimensionError(f"source has p={source.p}, spec expects {spec.p}")
+    if compute not in COMPUTE:
+        raise ParameterError(f"compute must be 'f64' or 'f32', got {compute!r}")
+    device = torch.device(device) if device is not None else default_device()
+    vdt = torch.float64 if compute == "f64" else torch.float32
+    row_iter = source.row_chunks() if hasattr(source, "row_chunks") else (ch.T for ch in source.chunks())
+    j0 = 0
+    for rows in device_row_chunks(row_iter, device):
+        if rows.ndim != 2 or rows.shape[1] != spec.p:
+            raise DimensionError(f"bad chunk at column offset {j0}: expected ({spec.p}, c)")
+        c = rows.shape[0]
+        idx = torch.empty((c, plan.m), dtype=torch.int32, device=device)
+        val = torch.empty((c, plan.m), dtype=vdt, device=device)
+        _launch_rows(rows, spec, plan, col0 + j0, COMPUTE[compute], idx, val)
+        sk = SparseSketch(spec=spec, n=c, indices=idx, values=val, plan=plan, col0=col0 + j0)
+        into = accumulate_moments(sk, covariance=covariance, into=into)
+        j0 += c
+    if j0 != source.n:
+        raise DimensionError(f"source yielded {j0} columns, expected {source.n}")
+    if into is None:
+        raise ParameterError("empty source")
     return into
 
 
@@ -168,6 +207,7 @@ def principal_components(sketch: SparseSketch, k: int, solver: str = "host") -> 
 
 __all__ = [
     "CovarianceEstimate", "Moments", "SYMMETRY_RTOL", "accumulate_moments", "covariance_from_moments",
+    "stream_moments",
     "estimate_covariance", "estimate_mean", "mean_from_moments", "principal_components", "top_eigenvectors",
     "unprecondition",
 ]

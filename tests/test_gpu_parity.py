@@ -382,3 +382,23 @@ def test_kmeanspp_matches_oracle_choice(skc):
     res = skc.sparsified_kmeans(X, 4, 12 / 32, n_init=2, seed=5)
     curve = res.diagnostics["objective_curve"]
     assert all(b <= a * (1 + 1e-9) for a, b in zip(curve, curve[1:]))
+
+
+def test_stream_moments_matches_one_shot(skc):
+    # streamed estimators (no stored sketch, copies overlapped) agree with the one-shot
+    # sketch: same mean accumulator order per chunk (1e-12), covariance per-chunk fixed point
+    rng = np.random.default_rng(21)
+    p, n = 512, 30000
+    X = rng.standard_normal((p, n)).astype(np.float32)
+    spec = skc.PreconditionSpec.create("hadamard", p, 8)
+    plan = skc.SamplingPlan(9, p, 26)
+    sk = skc.sketch_stream(X, spec, plan, compute="f32")
+    C1 = skc.estimate_covariance(sk).matrix
+    host = torch.from_numpy(np.ascontiguousarray(X.T)).pin_memory()
+    for src in (skc.RowSource(host, chunk_cols=7000), skc.ArraySource(X, chunk_cols=4096)):
+        mom = skc.stream_moments(src, spec, plan, compute="f32")
+        assert mom.n == n
+        C2 = skc.covariance_from_moments(mom, p, plan.m, n).cpu().numpy()
+        assert rel_fro(C2, C1) < 1e-7
+        mean = skc.mean_from_moments(mom, spec, plan.m, n).cpu().numpy()
+        assert np.abs(mean - skc.estimate_mean(sk)).max() < 1e-12 * max(1.0, np.abs(mean).max())
