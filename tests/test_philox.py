@@ -87,3 +87,22 @@ def test_sketch_stream_philox_and_supplied_indices(skc):
         skc.sketch_stream(X, spec, orc, indices=ref.host_indices()[:, ::-1].copy())
     with pytest.raises(skc.DimensionError):
         skc.sketch_stream(X, spec, orc, indices=ref.host_indices()[:10])
+
+
+@pytest.mark.gpu
+def test_philox_edges_and_identity_kind(skc):
+    for p, m in ((1, 1), (5, 5), (4096, 4096), (3, 1)):
+        plan = skc.SamplingPlan(master_seed=p * 31, p=p, m=m, sampler="philox")
+        got = plan.device_indices(0, 40).cpu().numpy().astype(np.uint32)
+        assert np.array_equal(got, O.philox_indices(p * 31, 0, 40, p, m))
+        if m == p:
+            assert np.array_equal(got, np.tile(np.arange(p, dtype=np.uint32), (40, 1)))
+    # kind "none": values are the raw coordinates at the sampled indices (transform.py:225-227)
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((37, 300))
+    spec = skc.PreconditionSpec.create("none", 37)
+    plan = skc.SamplingPlan(3, 37, 6, sampler="philox")
+    sk = skc.sketch_stream(X, spec, plan, compute="f64")
+    idx = O.philox_indices(3, 0, 300, 37, 6)
+    assert np.array_equal(sk.host_indices(), idx)
+    assert np.array_equal(sk.host_values(), np.take_along_axis(X.T, idx.astype(np.int64), axis=1))

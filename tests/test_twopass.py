@@ -79,3 +79,40 @@ def test_two_pass_from_dense_file_fp32_rows(skc, tmp_path):
     rows32 = torch.as_tensor(X.T.astype(np.float32), device="cuda")
     c = skc.sparsified_kmeans_two_pass(skc.RowSource(rows32), 6, 0.25, n_init=2, seed=4, compute="f32")
     assert (c.assignments.labels == b.assignments.labels).mean() > 0.99
+
+
+@pytest.mark.parametrize("K,p,n,dt", [(100, 130, 4000, np.float32), (70, 64, 3000, np.float64), (17, 200, 2500, np.float32)])
+def test_dense_kernels_many_centres(skc, K, p, n, dt):
+    # K > 16 runs several 16-centre passes in K8, K > 64 several 64-cluster passes in K9;
+    # checked against numpy in fp64: labels exact (separated points), sums to 1e-12
+    from paper_1511_00152_b200 import _lib
+
+    rng = np.random.default_rng(K + p)
+    C = rng.standard_normal((K, p)) * 6.0
+    lab_true = rng.integers(0, K, n)
+    X = (C[lab_true] + rng.standard_normal((n, p))).astype(dt)
+    mu = C + 0.01 * rng.standard_normal((K, p))
+    dev = torch.device("cuda")
+    Xd = torch.as_tensor(X, device=dev)
+    mud = torch.as_tensor(mu, device=dev)
+    L = _lib.lib()
+    ws = _lib.workspace(L.skc_dense_assign_workspace(p, K), dev)
+    labels = torch.empty(n, dtype=torch.int32, device=dev)
+    d2 = torch.empty(n, dtype=torch.float64, device=dev)
+    st = _lib.stream_ptr(dev)
+    _lib.call("skc_dense_assign", Xd.data_ptr(), _lib.dtype_code(Xd), p, n, p, mud.data_ptr(), K, ws.data_ptr(),
+              labels.data_ptr(), d2.data_ptr(), st)
+    Xf = X.astype(np.float64)
+    D = (Xf * Xf).sum(1)[:, None] - 2.0 * Xf @ mu.T + (mu * mu).sum(1)[None, :]
+    assert np.array_equal(labels.cpu().numpy(), np.argmin(D, axis=1))
+    assert np.allclose(d2.cpu().numpy(), np.clip(D.min(axis=1), 0, None), rtol=1e-10, atol=1e-8)
+    lab = torch.as_tensor(lab_true.astype(np.int32), device=dev)
+    sums = torch.zeros((K, p), dtype=torch.float64, device=dev)
+    counts = torch.zeros(K, dtype=torch.int64, device=dev)
+    ws2 = _lib.workspace(L.skc_dense_sums_workspace(n, p, K), dev)
+    _lib.call("skc_dense_sums", Xd.data_ptr(), _lib.dtype_code(Xd), p, n, p, lab.data_ptr(), K, sums.data_ptr(),
+              counts.data_ptr(), ws2.data_ptr(), st)
+    ref = np.zeros((K, p))
+    np.add.at(ref, lab_true, Xf)
+    assert np.array_equal(counts.cpu().numpy(), np.bincount(lab_true, minlength=K))
+    assert np.abs(sums.cpu().numpy() - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
