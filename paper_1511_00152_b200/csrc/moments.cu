@@ -240,7 +240,7 @@ __device__ __forceinline__ int cov_scale(const double* stats, int m, double* tau
 // needs a drift of 2^31 quanta and is rare even for entries whose sum hovers around zero.
 constexpr uint32_t kBias = 0x80000000u;
 
-template <typename V>
+template <typename V, bool WIDE>  // WIDE: m > 64 (columns beyond the two register chunks)
 __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __grid_constant__ CovParams P) {
   extern __shared__ int smem_i[];
   const int m = P.m;
@@ -290,21 +290,21 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
   int2* T = reinterpret_cast<int2*>(sidx);
   int2* U = T + m;
   auto visit = [&](const int64_t r, const int j0, const int j1, const float v0, const float v1) {
-    const int32_t* ir = P.idx + r * m;  // the row, for columns >= 64 and the general path
-    const V* vr = val + r * m;
     int nlo = __popc(__ballot_sync(kFullMask, j0 < r0)) + __popc(__ballot_sync(kFullMask, j1 < r0));
     int nhi = __popc(__ballot_sync(kFullMask, j0 < r1)) + __popc(__ballot_sync(kFullMask, j1 < r1));
     bool big = fabsf(v0) > ftau || fabsf(v1) > ftau;  // lanes past m hold 0
-    for (int t0 = 64; t0 < m; t0 += 32) {  // columns beyond the two register chunks
-      const int t = t0 + lane;
-      const int j = t < m ? __ldg(ir + t) : 0x7FFFFFFF;
-      if (t < m) big |= fabsf((float)__ldg(vr + t)) > ftau;
-      nlo += __popc(__ballot_sync(kFullMask, j < r0));
-      nhi += __popc(__ballot_sync(kFullMask, j < r1));
+    if constexpr (WIDE) {
+      for (int t0 = 64; t0 < m; t0 += 32) {  // columns beyond the two register chunks
+        const int t = t0 + lane;
+        const int j = t < m ? __ldg(P.idx + r * m + t) : 0x7FFFFFFF;
+        if (t < m) big |= fabsf((float)__ldg(val + r * m + t)) > ftau;
+        nlo += __popc(__ballot_sync(kFullMask, j < r0));
+        nhi += __popc(__ballot_sync(kFullMask, j < r1));
+      }
     }
     if (nlo == nhi) return;  // none of this row's indices fall in the band
     const bool any_big = __any_sync(kFullMask, big);
-    if (!any_big && m <= 64) {
+    if (!WIDE && !any_big) {
       // flat enumeration of the visit's pairs {(t, u): nlo <= t < nhi, t <= u < m}. Row x of
       // the trapezoid (t = nlo + x) has length mn - x; folding row x with row h-1-x gives a
       // rectangle of floor(h/2) rows of Lp = 2 mn - h + 1 (plus a half row when h is odd).
@@ -346,6 +346,8 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
       return;
     }
     // general path (m > 64, or a value above tau): stage the row in shared memory
+    const int32_t* ir = P.idx + r * m;
+    const V* vr = val + r * m;
     if (has0) {
       sidx[lane] = j0;
       sval[lane] = v0 * scale_a;
@@ -562,7 +564,8 @@ static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int
     if (H.band_rows[b + 1] - H.band_rows[b] > maxr) maxr = H.band_rows[b + 1] - H.band_rows[b];
   }
   const size_t smem = (size_t)((maxe + 1) & ~1) * 4 + (size_t)((maxr + 1) & ~1) * 4 + (size_t)kCovWarps * m * 16;
-  auto k = val_f64 ? cov_band_kernel<double> : cov_band_kernel<float>;
+  auto k = val_f64 ? (m > 64 ? cov_band_kernel<double, true> : cov_band_kernel<double, false>)
+                   : (m > 64 ? cov_band_kernel<float, true> : cov_band_kernel<float, false>);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<H.nbands * H.groups, kCovWarps * 32, smem, st>>>(H);
   int rc = check_launch("cov_band_kernel");
