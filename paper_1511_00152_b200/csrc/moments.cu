@@ -30,7 +30,7 @@ static int moments_warps(int32_t p_pad) {
   return w;
 }
 
-template <typename V>
+template <typename V, int MAXC>  // MAXC lane-chunks per row cover m <= 32 * MAXC from registers
 __global__ void moments_kernel(const int32_t* __restrict__ idx, const V* __restrict__ val, int64_t n, int32_t m,
                                int32_t p_pad, double* __restrict__ part) {
   extern __shared__ double wvec[];  // [warps][p_pad]
@@ -40,18 +40,20 @@ __global__ void moments_kernel(const int32_t* __restrict__ idx, const V* __restr
   __syncwarp();
   const int64_t c0 = n * blockIdx.x / gridDim.x, c1 = n * (blockIdx.x + 1) / gridDim.x;
   const int64_t r0 = c0 + (c1 - c0) * warp / warps, r1 = c0 + (c1 - c0) * (warp + 1) / warps;
-  double sq = 0.0, mx = 0.0;
-  // rows in batches of 4: all loads of a batch are issued before the shared-memory updates
-  constexpr int kB = 4, kMaxC = 4;  // kMaxC lane-chunks per row cover m <= 128 from registers
+  double sqc[MAXC], mx = 0.0;  // one square-sum chain per lane-chunk (they only feed K3's scale)
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) sqc[c] = 0.0;
+  // rows in batches of kB: all loads of a batch are issued before the shared-memory updates
+  constexpr int kB = 8;
   int64_t r = r0;
-  if (m <= 32 * kMaxC) {
+  if (m <= 32 * MAXC) {
     for (; r + kB <= r1; r += kB) {
-      int jj[kB][kMaxC];
-      double vv[kB][kMaxC];
+      int jj[kB][MAXC];
+      double vv[kB][MAXC];
 #pragma unroll
       for (int b = 0; b < kB; ++b)
 #pragma unroll
-        for (int c = 0; c < kMaxC; ++c) {
+        for (int c = 0; c < MAXC; ++c) {
           const int t = lane + 32 * c;
           jj[b][c] = -1;
           vv[b][c] = 0.0;
@@ -63,11 +65,11 @@ __global__ void moments_kernel(const int32_t* __restrict__ idx, const V* __restr
 #pragma unroll
       for (int b = 0; b < kB; ++b) {
 #pragma unroll
-        for (int c = 0; c < kMaxC; ++c) {
+        for (int c = 0; c < MAXC; ++c) {
           if (jj[b][c] >= 0) {
             const double v = vv[b][c];
             mine[jj[b][c]] = dadd(mine[jj[b][c]], v);
-            sq = dadd(sq, dmul(v, v));
+            sqc[c] = dadd(sqc[c], dmul(v, v));
             mx = fmax(mx, fabs(v));
           }
         }
@@ -80,11 +82,14 @@ __global__ void moments_kernel(const int32_t* __restrict__ idx, const V* __restr
       const int j = __ldg(idx + r * m + t);
       const double v = (double)__ldg(val + r * m + t);
       mine[j] = dadd(mine[j], v);
-      sq = dadd(sq, dmul(v, v));
+      sqc[0] = dadd(sqc[0], dmul(v, v));
       mx = fmax(mx, fabs(v));
     }
     __syncwarp();
   }
+  double sq = sqc[0];
+#pragma unroll
+  for (int c = 1; c < MAXC; ++c) sq = dadd(sq, sqc[c]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     sq = dadd(sq, __shfl_xor_sync(kFullMask, sq, o));
@@ -142,11 +147,21 @@ int moments_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, 
   double* part = reinterpret_cast<double*>(ws);
   if (n > 0) {
     if (val_f64) {
-      cudaFuncSetAttribute(moments_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      moments_kernel<double><<<G, W * 32, smem, st>>>(idx, (const double*)val, n, m, p_pad, part);
+      if (m <= 64) {
+        cudaFuncSetAttribute(moments_kernel<double, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        moments_kernel<double, 2><<<G, W * 32, smem, st>>>(idx, (const double*)val, n, m, p_pad, part);
+      } else {
+        cudaFuncSetAttribute(moments_kernel<double, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        moments_kernel<double, 4><<<G, W * 32, smem, st>>>(idx, (const double*)val, n, m, p_pad, part);
+      }
     } else {
-      cudaFuncSetAttribute(moments_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      moments_kernel<float><<<G, W * 32, smem, st>>>(idx, (const float*)val, n, m, p_pad, part);
+      if (m <= 64) {
+        cudaFuncSetAttribute(moments_kernel<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        moments_kernel<float, 2><<<G, W * 32, smem, st>>>(idx, (const float*)val, n, m, p_pad, part);
+      } else {
+        cudaFuncSetAttribute(moments_kernel<float, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        moments_kernel<float, 4><<<G, W * 32, smem, st>>>(idx, (const float*)val, n, m, p_pad, part);
+      }
     }
     int rc = check_launch("moments_kernel");
     if (rc) return rc;
