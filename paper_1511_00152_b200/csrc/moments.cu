@@ -19,7 +19,7 @@ constexpr uint32_t kFullMask = 0xFFFFFFFFu;
 // ======================================================================================
 int moments_grid(int64_t n) {
   int64_t g = (n + 255) / 256;
-  const int64_t cap = 2 * (int64_t)sm_count();
+  const int64_t cap = 3 * (int64_t)sm_count();  // 3 CTAs (24 warps) per SM at p_pad <= 1024
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (int)g;
