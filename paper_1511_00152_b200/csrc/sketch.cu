@@ -718,7 +718,10 @@ static int launch_gather_logp(int logp, const SketchParams& P, cudaStream_t st) 
 // kGiven mode then only loads, transforms and gathers (HBM-bound).
 constexpr int kIdxWarps = 8;
 template <int LOGP>
-__global__ void __launch_bounds__(kIdxWarps * 32, 4) indices_kernel(const SketchParams P) {
+#ifndef SKC_IDX_MINB
+#define SKC_IDX_MINB 8  // 32 registers: 8 CTAs (64 warps) per SM, no spills (measured best)
+#endif
+__global__ void __launch_bounds__(kIdxWarps * 32, SKC_IDX_MINB) indices_kernel(const SketchParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
   constexpr int kRowWords = mask_words<LOGP>();
