@@ -202,6 +202,21 @@ int skc_sketch_given(const void *X, int32_t x_dtype, int64_t ld, int64_t n, int3
                      uint64_t sign_seed, int32_t m, int32_t compute_dtype, const int32_t *idx_in, void *val_out,
                      int32_t val_dtype, void *stream);
 
+/* ---- native streaming runtime ---------------------------------------------------------
+ * sketch_stream + estimators.py:30-66 over host rows without keeping the sketch (the loop of
+ * stream_moments, in C++). host_X: (n, p) rows, row stride ld, fp32 or fp64; pinned host
+ * memory gives asynchronous copies. Chunks of chunk_rows are copied on a private stream into
+ * two device buffers while the previous chunk's sketch, moments and covariance run on
+ * `stream`; events gate buffer reuse. acc / stats / tri accumulate (+=) as in skc_moments /
+ * skc_cov_accumulate; tri may be NULL (mean only). sampler: 0 oracle, 1 philox.
+ * ws: skc_stream_workspace bytes (device). */
+size_t skc_stream_workspace(int64_t chunk_rows, int32_t p, int32_t p_pad, int32_t m, int32_t x_dtype,
+                            int32_t compute_dtype, int32_t covariance);
+int skc_stream_moments(const void *host_X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, int32_t p_pad,
+                       int32_t kind, uint64_t sign_seed, uint64_t master_seed, int64_t col0, int32_t m,
+                       int32_t compute_dtype, int32_t sampler, int64_t chunk_rows, double *acc, double *stats,
+                       double *tri, void *ws, size_t ws_bytes, void *stream);
+
 /* ---- SKCH1 file records (io.py:84-136) ---------------------------------------------
  * A record is the sample's m u32 indices followed by its m f64 values, 12 m bytes, no
  * padding; the file is a 61-byte header then n records. pack: (idx, val) -> out_words

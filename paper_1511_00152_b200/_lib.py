@@ -62,6 +62,9 @@ SIGNATURES = {
     "skc_kmeans_reseed_at": (_c.c_int, [_P, _P, _I32, _I64, _I32, _P, _P, _I32, _I32, _P, _P]),
     "skc_indices_philox": (_c.c_int, [_U64, _I64, _I64, _I32, _I32, _P, _P]),
     "skc_sketch_given": (_c.c_int, [_P, _I32, _I64, _I64, _I32, _I32, _I32, _U64, _I32, _I32, _P, _P, _I32, _P]),
+    "skc_stream_workspace": (_c.c_size_t, [_I64, _I32, _I32, _I32, _I32, _I32, _I32]),
+    "skc_stream_moments": (_c.c_int, [_P, _I32, _I64, _I64, _I32, _I32, _I32, _U64, _U64, _I64, _I32, _I32, _I32, _I64,
+                                      _P, _P, _P, _P, _SZ, _P]),
     "skc_sketch_pack_records": (_c.c_int, [_P, _P, _I32, _I64, _I32, _P, _P]),
     "skc_sketch_unpack_records": (_c.c_int, [_P, _I64, _I32, _P, _P, _P]),
     "skc_dense_assign_workspace": (_c.c_size_t, [_I32, _I32]),

@@ -410,4 +410,104 @@ int skc_dense_sums(const void* X, int32_t x_dtype, int64_t ld, int64_t n, int32_
                            S(stream));
 }
 
+// ---- native streaming runtime (stream_moments' loop in C++) ------------------------
+struct StreamLayout {
+  size_t off_buf[2], off_idx, off_val, off_mws, off_cws, total;
+};
+
+static StreamLayout stream_layout(int64_t chunk, int32_t p, int32_t p_pad, int32_t m, int x_f64, int v_f64, int cov) {
+  StreamLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t r = o;
+    o += (bytes + 255) & ~(size_t)255;
+    return r;
+  };
+  const size_t rows_bytes = (size_t)chunk * p * (x_f64 ? 8 : 4);
+  L.off_buf[0] = take(rows_bytes);
+  L.off_buf[1] = take(rows_bytes);
+  L.off_idx = take((size_t)chunk * m * 4);
+  L.off_val = take((size_t)chunk * m * (v_f64 ? 8 : 4));
+  L.off_mws = take(moments_ws(chunk, p_pad));
+  L.off_cws = take(cov ? cov_ws(chunk, m, p_pad) : 1);
+  L.total = o;
+  return L;
+}
+
+size_t skc_stream_workspace(int64_t chunk_rows, int32_t p, int32_t p_pad, int32_t m, int32_t x_dtype,
+                            int32_t compute_dtype, int32_t covariance) {
+  if (chunk_rows < 1 || p < 1 || p_pad < p || m < 1) return 0;
+  return stream_layout(chunk_rows, p, p_pad, m, x_dtype == SKC_F64, compute_dtype == SKC_F64, covariance).total;
+}
+
+int skc_stream_moments(const void* host_X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, int32_t p_pad,
+                       int32_t kind, uint64_t sign_seed, uint64_t master_seed, int64_t col0, int32_t m,
+                       int32_t compute_dtype, int32_t sampler, int64_t chunk_rows, double* acc, double* stats,
+                       double* tri, void* ws, size_t ws_bytes, void* stream) {
+  int rc;
+  if ((rc = check_spec(kind, p, p_pad)) || (rc = check_m(m, p_pad)) || (rc = check_dtype(x_dtype)) ||
+      (rc = check_dtype(compute_dtype)))
+    return rc;
+  if (n < 0 || ld < p) return fail(SKC_EDIM, "expected a (n, p) row block with ld >= p");
+  if (chunk_rows < 1) return fail(SKC_EPARAM, "chunk_rows must be >= 1");
+  if (sampler != 0 && sampler != 1) return fail(SKC_EPARAM, "sampler must be 0 (oracle) or 1 (philox)");
+  if (tri != nullptr && (m < 2 || (rc = cov_check(p_pad, m)))) return m < 2 ? fail(SKC_EPARAM, "covariance needs m >= 2") : rc;
+  const int x_f64 = x_dtype == SKC_F64, v_f64 = compute_dtype == SKC_F64;
+  const StreamLayout L = stream_layout(chunk_rows, p, p_pad, m, x_f64, v_f64, tri != nullptr);
+  if (ws_bytes < L.total) return fail(SKC_EPARAM, "workspace too small");
+  if (n == 0) return SKC_OK;
+  char* w = static_cast<char*>(ws);
+  const size_t es = x_f64 ? 8 : 4;
+  cudaStream_t cs = S(stream), cp;
+  if (cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking) != cudaSuccess) return check_launch("copy stream");
+  cudaEvent_t copied[2], freed[2];
+  for (int b = 0; b < 2; ++b) {
+    cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&freed[b], cudaEventDisableTiming);
+  }
+  int32_t* idx = reinterpret_cast<int32_t*>(w + L.off_idx);
+  void* val = w + L.off_val;
+  rc = SKC_OK;
+  int64_t k = 0;
+  for (int64_t c0 = 0; c0 < n && rc == SKC_OK; c0 += chunk_rows, ++k) {
+    const int64_t rows = n - c0 < chunk_rows ? n - c0 : chunk_rows;
+    const int b = (int)(k & 1);
+    void* buf = w + L.off_buf[b];
+    if (k >= 2) cudaStreamWaitEvent(cp, freed[b], 0);  // K1 of chunk k-2 has read this buffer
+    if (cudaMemcpy2DAsync(buf, (size_t)p * es, static_cast<const char*>(host_X) + (size_t)c0 * ld * es, (size_t)ld * es,
+                          (size_t)p * es, (size_t)rows, cudaMemcpyHostToDevice, cp) != cudaSuccess) {
+      rc = check_launch("chunk copy");
+      break;
+    }
+    cudaEventRecord(copied[b], cp);
+    cudaStreamWaitEvent(cs, copied[b], 0);
+    if (kind == SKC_KIND_NONE) {
+      if (sampler == 1) {
+        rc = philox_indices_launch(master_seed, col0 + c0, rows, p_pad, m, idx, cs);
+        if (!rc) rc = sketch_given_launch(buf, x_dtype, p, rows, p, p_pad, kind, sign_seed, m, compute_dtype, idx, val,
+                                          compute_dtype, cs);
+      } else {
+        rc = sketch_identity(buf, x_dtype, p, rows, p, p_pad, master_seed, col0 + c0, m, idx, val, compute_dtype,
+                             nullptr, cs);
+      }
+    } else if (sampler == 1) {
+      rc = philox_indices_launch(master_seed, col0 + c0, rows, p_pad, m, idx, cs);
+      if (!rc) rc = sketch_given_launch(buf, x_dtype, p, rows, p, p_pad, kind, sign_seed, m, compute_dtype, idx, val,
+                                        compute_dtype, cs);
+    } else {
+      rc = sketch_launch(buf, x_dtype, p, rows, p, p_pad, kind, sign_seed, master_seed, col0 + c0, m, compute_dtype, idx,
+                         val, compute_dtype, nullptr, cs);
+    }
+    cudaEventRecord(freed[b], cs);
+    if (!rc) rc = moments_launch(idx, val, v_f64, rows, m, p_pad, acc, stats, w + L.off_mws, cs);
+    if (!rc && tri != nullptr) rc = cov_launch(idx, val, v_f64, rows, m, p_pad, stats, tri, w + L.off_cws, cs);
+  }
+  for (int b = 0; b < 2; ++b) {
+    cudaEventDestroy(copied[b]);
+    cudaEventDestroy(freed[b]);
+  }
+  cudaStreamDestroy(cp);  // released once its queued copies finish
+  return rc;
+}
+
 }  // extern "C"

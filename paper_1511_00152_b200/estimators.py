@@ -86,7 +86,7 @@ def stream_moments(source, spec, plan, *, covariance: bool = True, compute: str 
     PCIe rate. K3's fixed-point scale follows the statistics accumulated so far; every
     chunk's sum is exact in its own quantum and the chunks add in fp64.
     """
-    from .sketch import COMPUTE, _launch_rows, as_source, device_row_chunks
+    from .sketch import COMPUTE, RowSource, _launch_rows, as_source, device_row_chunks
 
     source = as_source(source)
     if source.p != spec.p:
@@ -95,6 +95,10 @@ def stream_moments(source, spec, plan, *, covariance: bool = True, compute: str 
         raise ParameterError(f"compute must be 'f64' or 'f32', got {compute!r}")
     device = torch.device(device) if device is not None else default_device()
     vdt = torch.float64 if compute == "f64" else torch.float32
+    rows = getattr(source, "rows", None)
+    if (isinstance(source, RowSource) and isinstance(rows, torch.Tensor) and not rows.is_cuda and rows.is_pinned()
+            and rows.dtype in (torch.float32, torch.float64) and rows.ndim == 2 and rows.stride(1) == 1):
+        return _stream_moments_native(rows, source.chunk_cols, spec, plan, covariance, compute, device, col0, into)
     row_iter = source.row_chunks() if hasattr(source, "row_chunks") else (ch.T for ch in source.chunks())
     j0 = 0
     for rows in device_row_chunks(row_iter, device):
@@ -111,6 +115,32 @@ def stream_moments(source, spec, plan, *, covariance: bool = True, compute: str 
         raise DimensionError(f"source yielded {j0} columns, expected {source.n}")
     if into is None:
         raise ParameterError("empty source")
+    return into
+
+
+def _stream_moments_native(rows: torch.Tensor, chunk_rows: int, spec, plan, covariance: bool, compute: str, device,
+                           col0: int, into: Optional[Moments]) -> Moments:
+    """Pinned host rows: the chunk loop runs in C++ (``skc_stream_moments``): copies on a
+    private stream into two device buffers, each chunk's kernels on the current stream."""
+    from .sketch import COMPUTE
+
+    n, p = rows.shape
+    p_pad, m = spec.p_pad, plan.m
+    if into is None:
+        into = Moments(acc=torch.zeros(p_pad, dtype=torch.float64, device=device),
+                       stats=torch.zeros(3, dtype=torch.float64, device=device),
+                       tri=torch.zeros(p_pad * (p_pad + 1) // 2, dtype=torch.float64, device=device)
+                       if covariance else None, n=0)
+    chunk = max(1, min(int(chunk_rows), max(int(n), 1)))
+    L = _lib.lib()
+    xc = _lib.dtype_code(rows)
+    ws = _lib.workspace(L.skc_stream_workspace(chunk, p, p_pad, m, xc, COMPUTE[compute], int(covariance)), device)
+    with torch.cuda.device(device):
+        _lib.call("skc_stream_moments", rows.data_ptr(), xc, rows.stride(0), n, p, p_pad, spec.gpu_kind(),
+                  u64(spec.sign_seed), u64(plan.master_seed), int(col0), m, COMPUTE[compute],
+                  1 if plan.sampler == "philox" else 0, chunk, into.acc.data_ptr(), into.stats.data_ptr(),
+                  _lib.ptr(into.tri), ws.data_ptr(), ws.numel(), _lib.stream_ptr(device))
+    into.n += int(n)
     return into
 
 

@@ -402,3 +402,19 @@ def test_stream_moments_matches_one_shot(skc):
         assert rel_fro(C2, C1) < 1e-7
         mean = skc.mean_from_moments(mom, spec, plan.m, n).cpu().numpy()
         assert np.abs(mean - skc.estimate_mean(sk)).max() < 1e-12 * max(1.0, np.abs(mean).max())
+
+
+@pytest.mark.parametrize("sampler,kind", [("oracle", "hadamard"), ("philox", "hadamard"), ("oracle", "none")])
+def test_stream_moments_native_equals_python_loop(skc, sampler, kind):
+    # pinned host rows take the C++ chunk loop (skc_stream_moments); a pageable source the
+    # Python loop: same kernels, same chunking, bit-identical partial sums
+    rng = np.random.default_rng(31)
+    p, n = 300, 20000
+    X = rng.standard_normal((n, p)).astype(np.float32)
+    spec = skc.PreconditionSpec.create(kind, p, 4)
+    plan = skc.SamplingPlan(6, spec.p_pad, 20, sampler=sampler)
+    pinned = torch.from_numpy(X).pin_memory()
+    a = skc.stream_moments(skc.RowSource(pinned, chunk_cols=3000), spec, plan, compute="f32")
+    b = skc.stream_moments(skc.RowSource(torch.from_numpy(X), chunk_cols=3000), spec, plan, compute="f32")
+    assert a.n == b.n == n
+    assert torch.equal(a.acc, b.acc) and torch.equal(a.stats, b.stats) and torch.equal(a.tri, b.tri)
