@@ -1,0 +1,79 @@
+"""C3-scale properties (p=1024, m=51, n=2^23 rows, 32 GB resident), size-independent checks.
+
+At this size the oracle cannot run the whole job, so the checks are:
+* every row's indices are strictly increasing and in range;
+* 2000 random rows match the oracle bit for bit (indices and fp64 values);
+* covariance additivity: the sums of the two halves equal the sum of the whole, exactly,
+  because the fixed-point accumulator is integer for one shared scale;
+* the Philox sampler keeps every coordinate with frequency m/p.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def big():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1511_00152_b200 as skc
+
+    n, p, m = 1 << 23, 1024, 51
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(2026)
+    X = torch.randn((n, p), device=dev, generator=g, dtype=torch.float32)
+    X[:, 7] *= 40.0  # a heavy coordinate
+    spec = skc.PreconditionSpec.create("hadamard", p, 11)
+    plan = skc.SamplingPlan(13, p, m)
+    sk = skc.sketch_stream(skc.RowSource(X), spec, plan, compute="f64")
+    yield skc, X, spec, plan, sk
+    del X, sk
+    torch.cuda.empty_cache()
+
+
+def test_indices_sorted_and_random_rows_match_oracle(big):
+    skc, X, spec, plan, sk = big
+    idx = sk.indices
+    assert bool((idx[:, 1:] > idx[:, :-1]).all()) and int(idx.min()) >= 0 and int(idx.max()) < spec.p_pad
+    rows = np.sort(np.random.default_rng(1).choice(sk.n, 2000, replace=False))
+    Xr = X[torch.as_tensor(rows, device=X.device)].cpu().numpy()
+    for r in rows[:200]:  # the oracle's plan, per row, with the global column index
+        assert np.array_equal(idx[int(r)].cpu().numpy().astype(np.uint32),
+                              O.indices_block(plan.master_seed, int(r), int(r) + 1, spec.p_pad, plan.m)[0])
+    Y = O.precondition_rows(Xr.astype(np.float64), spec.p_pad, O.HADAMARD, spec.sign_seed)
+    got_idx = idx[torch.as_tensor(rows, device=X.device)].cpu().numpy().astype(np.int64)
+    got_val = sk.values[torch.as_tensor(rows, device=X.device)].cpu().numpy()
+    assert np.array_equal(got_val, np.take_along_axis(Y, got_idx, axis=1))
+
+
+def test_covariance_additive_over_halves(big):
+    skc, X, spec, plan, sk = big
+    n, m, p = sk.n, sk.m, sk.p
+    whole = skc.accumulate_moments(sk)
+    halves = [skc.SparseSketch(spec=spec, n=n // 2, indices=sk.indices[a:b], values=sk.values[a:b], plan=plan)
+              for a, b in ((0, n // 2), (n // 2, n))]
+    # one shared scale: both halves use the whole job's statistics
+    from paper_1511_00152_b200 import _lib
+
+    tri = torch.zeros_like(whole.tri)
+    L = _lib.lib()
+    for h in halves:
+        ws = _lib.workspace(L.skc_cov_workspace(h.n, m, p), X.device)
+        _lib.call("skc_cov_accumulate", h.indices.data_ptr(), h.values.data_ptr(), _lib.F64, h.n, m, p,
+                  whole.stats.data_ptr(), tri.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(X.device))
+    assert torch.equal(tri, whole.tri)
+
+
+def test_philox_inclusion_uniform_at_scale(big):
+    skc, X, spec, plan, sk = big
+    ph = skc.SamplingPlan(plan.master_seed, spec.p_pad, plan.m, sampler="philox")
+    idx = ph.device_indices(0, sk.n).long()
+    f = torch.bincount(idx.flatten(), minlength=spec.p_pad).double() / sk.n
+    q = plan.m / spec.p_pad
+    sd = (q * (1 - q) / sk.n) ** 0.5
+    assert float((f - q).abs().max()) < 6 * sd
