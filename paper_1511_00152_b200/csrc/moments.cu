@@ -189,9 +189,14 @@ constexpr int kMaxBands = 511;
 
 __host__ __device__ inline int64_t tri_off(int64_t a, int64_t p) { return a * p - a * (a - 1) / 2; }
 
+// visit pair table (m <= 64): bytes t[f], u[f] of the f-th pair (t <= u) in t-major order,
+// so the pairs of rows t in [nlo, nhi) are the contiguous range [tri_off(nlo), tri_off(nhi))
+static size_t pair_table_bytes(int32_t m) {
+  return m <= 64 ? ((size_t)m * (m + 1) + 7) & ~(size_t)7 : 0;
+}
 static int band_capacity(int32_t m, int32_t p_pad) {
-  // int32 entries left after the per-warp row staging and the row table
-  return (int)(((size_t)kSmemBudget - (size_t)kCovWarps * m * 16 - 4 * (size_t)p_pad) / 4);
+  // int32 entries left after the per-warp row staging, the row table and the pair table
+  return (int)(((size_t)kSmemBudget - (size_t)kCovWarps * m * 16 - 4 * (size_t)p_pad - pair_table_bytes(m)) / 4);
 }
 // greedy row bands of <= cap entries; returns the count, fills out[0..count] if given
 static int make_bands(int32_t p_pad, int cap, int* out) {
@@ -255,6 +260,7 @@ __device__ __forceinline__ int cov_scale(const double* stats, int m, double* tau
 // needs a drift of 2^31 quanta and is rare even for entries whose sum hovers around zero.
 constexpr uint32_t kBias = 0x80000000u;
 
+
 template <typename V, bool WIDE>  // WIDE: m > 64 (columns beyond the two register chunks)
 __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __grid_constant__ CovParams P) {
   extern __shared__ int smem_i[];
@@ -268,7 +274,10 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
   int* rowbase = smem_i + ((ne + 1) & ~1);  // [r1 - r0]: entry (a, b) sits at rowbase[a - r0] + b
   // per-warp staging, 4*m words: the general path uses [sidx: m][sval: m], the flat path
   // reuses it as int2 T[m], U[m]
-  int* stage = rowbase + ((r1 - r0 + 1) & ~1) + (size_t)warp * 4 * m;
+  const int npair = !WIDE ? m * (m + 1) / 2 : 0;
+  uint8_t* ptt = reinterpret_cast<uint8_t*>(rowbase + ((r1 - r0 + 1) & ~1));
+  uint8_t* ptu = ptt + npair;
+  int* stage = reinterpret_cast<int*>(ptt + ((2 * npair + 7) & ~7)) + (size_t)warp * 4 * m;
   int* sidx = stage;
   float* sval = reinterpret_cast<float*>(stage + m);
   unsigned long long* part = P.part + (size_t)group * tri_off(P.p_pad, P.p_pad) + e0;
@@ -281,6 +290,10 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
 
   for (int e = threadIdx.x; e < ne; e += blockDim.x) lo[e] = kBias;
   for (int a = r0 + threadIdx.x; a < r1; a += blockDim.x) rowbase[a - r0] = (int)(tri_off(a, P.p_pad) - e0) - a;
+  if (npair && threadIdx.x < m) {
+    const int t = threadIdx.x, f0 = t * m - ((t * (t - 1)) >> 1);
+    for (int u = t; u < m; ++u) ptt[f0 + u - t] = (uint8_t)t, ptu[f0 + u - t] = (uint8_t)(m + u);  // U = T + m
+  }
   __syncthreads();
 
   const int64_t g0 = P.n * group / P.groups, g1 = P.n * (group + 1) / P.groups;
@@ -320,13 +333,8 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
     if (nlo == nhi) return;  // none of this row's indices fall in the band
     const bool any_big = __any_sync(kFullMask, big);
     if (!WIDE && !any_big) {
-      // flat enumeration of the visit's pairs {(t, u): nlo <= t < nhi, t <= u < m}. Row x of
-      // the trapezoid (t = nlo + x) has length mn - x; folding row x with row h-1-x gives a
-      // rectangle of floor(h/2) rows of Lp = 2 mn - h + 1 (plus a half row when h is odd).
-      // Lane f -> rr = floor((f + 0.5) / Lp) by an approximate reciprocal (the fraction
-      // stays >= 1/(2 Lp) > 2^-9, far above the rounding error), c = f - rr * Lp, and
-      //   c <  mn - rr: t = nlo + rr,        u = t + c
-      //   otherwise:    t = nhi - 1 - rr,    u = c + nhi - 1 - mn
+      // the visit's pairs {(t, u): nlo <= t < nhi, t <= u < m} are the contiguous range
+      // [tri_off(nlo), tri_off(nhi)) of the t-major pair table; lane f takes pair f
       if (has0) U[lane] = make_int2(j0 << 2, __float_as_int(v0));
       if (has1) U[lane + 32] = make_int2(j1 << 2, __float_as_int(v1));
       if (lane >= nlo && lane < nhi)
@@ -334,22 +342,9 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
       if (lane + 32 >= nlo && lane + 32 < nhi)
         T[lane + 32] = make_int2((int)lo_sh + 4 * rowbase[j1 - r0], __float_as_int(v1 * scale_a));
       __syncwarp();
-      const int h = nhi - nlo, mn = m - nlo;
-      const int Lp = 2 * mn - h + 1;
-      const int F = h * mn - (h * (h - 1) >> 1);
-      // rr = floor((f + 0.5) / Lp) in fp32 (an IMAD.HI magic-number division measured slower)
-      float inv;
-      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"((float)Lp));
-      const int kB = nhi - 1 - mn, tB = nhi - 1;
-      float ff = (float)lane + 0.5f;
-      for (int f = lane; f < F; f += 32, ff += 32.0f) {
-        const int rr = (int)(ff * inv);
-        const int c = f - rr * Lp;
-        const bool first = c + rr < mn;
-        const int x = nlo + rr;
-        const int t = first ? x : tB - rr;
-        const int u = c + (first ? x : kB);
-        const int2 tt = T[t], uu = U[u];
+      const int F1 = nhi * m - ((nhi * (nhi - 1)) >> 1);
+      for (int f = nlo * m - ((nlo * (nlo - 1)) >> 1) + lane; f < F1; f += 32) {
+        const int2 tt = T[ptt[f]], uu = T[ptu[f]];
         const uint32_t addr = (uint32_t)(tt.x + uu.x);
         const int q = __float2int_rn(__int_as_float(tt.y) * __int_as_float(uu.y));
         uint32_t old;
@@ -578,7 +573,8 @@ static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int
     if (e > maxe) maxe = e;
     if (H.band_rows[b + 1] - H.band_rows[b] > maxr) maxr = H.band_rows[b + 1] - H.band_rows[b];
   }
-  const size_t smem = (size_t)((maxe + 1) & ~1) * 4 + (size_t)((maxr + 1) & ~1) * 4 + (size_t)kCovWarps * m * 16;
+  const size_t smem = (size_t)((maxe + 1) & ~1) * 4 + (size_t)((maxr + 1) & ~1) * 4 + pair_table_bytes(m) +
+                      (size_t)kCovWarps * m * 16;
   auto k = val_f64 ? (m > 64 ? cov_band_kernel<double, true> : cov_band_kernel<double, false>)
                    : (m > 64 ? cov_band_kernel<float, true> : cov_band_kernel<float, false>);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
