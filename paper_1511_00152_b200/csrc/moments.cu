@@ -538,14 +538,52 @@ static int cov_groups(int nbands, int64_t n) {
   return g;
 }
 
+// K3t (cov_tc.cu): the tensor-core path for large m/p
+bool covtc_supported(int32_t p_pad);
+size_t covtc_ws(int64_t n, int32_t m, int32_t p_pad);
+int covtc_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, int32_t p_pad,
+                 const double* stats, double* tri, void* ws, cudaStream_t st);
+// Smallest m at which the tensor-core path beats the scatter paths, per log2(p_pad) = 8..13
+// (dense MMA work is independent of m, the scatter's grows as m^2). Measured on one B200,
+// tools/covtc_probe.py (profiles/round1_covtc.log): p = 256: m 36, 512: 50, 1024: 70,
+// 2048: 75 (against K3g), 4096: 140 (K3g; 272 units run as two waves); 8192 extrapolated.
+static int tc_min_m(int32_t p_pad) {
+  static const int t[6] = {36, 50, 70, 75, 140, 280};
+  int l = 0;
+  while ((1 << l) < p_pad) ++l;
+  return l < 8 ? 1 << 30 : t[l > 13 ? 5 : l - 8];
+}
+
+// 'b' banded scatter (K3), 'g' global L2 scatter (K3g), 't' tensor cores (K3t).
+// SKC_COV_PATH=b|g|t forces a path where it applies.
+static char cov_path(int32_t m, int32_t p_pad) {
+  const int cap = band_capacity(m, p_pad);
+  const bool tc = covtc_supported(p_pad);
+  if (const char* f = getenv("SKC_COV_PATH")) {
+    if (f[0] == 't' && tc) return 't';
+    if (f[0] == 'g') return 'g';
+    if (f[0] == 'b' && cap >= p_pad) return 'b';
+  }
+  if (tc && (m >= tc_min_m(p_pad) || cap < p_pad)) return 't';
+  if (cap < p_pad) return 'g';
+  return make_bands(p_pad, cap, nullptr) > kCovGlobalBands ? 'g' : 'b';
+}
+
 int cov_check(int32_t p_pad, int32_t m) {
-  if (band_capacity(m, p_pad) < p_pad) return fail(SKC_EPARAM, "m too large for the shared-memory covariance bands");
+  const char path = cov_path(m, p_pad);
+  if (path == 't') return SKC_OK;
+  if (path == 'g') return (size_t)kCovGWarps * 2 * m * sizeof(int2) <= 200 * 1024
+                              ? SKC_OK
+                              : fail(SKC_EPARAM, "m too large for the covariance kernels");
   if (make_bands(p_pad, band_capacity(m, p_pad), nullptr) > kMaxBands)
     return fail(SKC_EPARAM, "too many covariance bands for p_pad");
   return SKC_OK;
 }
 
 size_t cov_ws(int64_t n, int32_t m, int32_t p_pad) {
+  const char path = cov_path(m, p_pad);
+  if (path == 't') return covtc_ws(n, m, p_pad);
+  if (path == 'g') return (size_t)tri_off(p_pad, p_pad) * sizeof(unsigned long long);
   const int nb = make_bands(p_pad, band_capacity(m, p_pad), nullptr);
   const int g = cov_groups(nb, n);
   return (size_t)g * tri_off(p_pad, p_pad) * sizeof(unsigned long long);
@@ -589,10 +627,9 @@ int cov_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int3
                const double* stats, double* tri, void* ws, cudaStream_t st) {
   if (n == 0) return SKC_OK;
   // path: banded shared-memory accumulation, or (many bands) the L2-resident global path
-  const int nbands = make_bands(p_pad, band_capacity(m, p_pad), nullptr);
-  const char* force = getenv("SKC_COV_PATH");
-  const bool global = force ? force[0] == 'g' : nbands > kCovGlobalBands;
-  if (global) return cov_launch_global(idx, val, val_f64, n, m, p_pad, stats, tri, ws, st);
+  const char path = cov_path(m, p_pad);
+  if (path == 't') return covtc_launch(idx, val, val_f64, n, m, p_pad, stats, tri, ws, st);
+  if (path == 'g') return cov_launch_global(idx, val, val_f64, n, m, p_pad, stats, tri, ws, st);
   // the kernel addresses a group's rows with 32-bit element offsets: split huge inputs
   const int groups = cov_groups(make_bands(p_pad, band_capacity(m, p_pad), nullptr), n);
   int64_t max_rows = (int64_t)groups * ((((int64_t)1 << 31) / m) - kCovWarps);
