@@ -226,7 +226,8 @@ def profiled_traffic(workload, n, stage):
     """dram read+write bytes per launch of the stage's kernel, from the committed ncu capture
     (profiles/<wl>_ncu_full.json, written by tools/ncu_summary.py) when it was taken at this
     exact size, else None."""
-    names = {"sketch": "sketch_kernel", "covariance": "cov_band_kernel", "moments": "moments_kernel"}
+    names = {"indices": "indices_kernel", "gather": "gather_kernel", "covariance": "cov_band_kernel",
+             "moments": "moments_kernel"}
     path = os.path.join(ROOT, "profiles", f"{workload}_ncu_full.json")
     try:
         with open(path) as f:
@@ -318,18 +319,11 @@ def main():
         ws1 = _lib.workspace(L.skc_moments_workspace(n, m, p), dev)
         ws2 = _lib.workspace(L.skc_cov_workspace(n, m, p), dev)
         st = _lib.stream_ptr(dev)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-        stage_names = ["sketch", "moments", "covariance", "finalize"]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        # the sketch as its two kernels (what skc_sketch runs internally), timed apart so the
+        # roofline can name the dominant kernel: K1a indices (oracle keys or Philox), K1b gather
+        stage_names = ["indices", "gather", "moments", "covariance", "finalize"]
         sampler = args.sampler
-
-        def sketch_call(which):
-            if which == "philox":  # Philox indices, then values at them
-                _lib.call("skc_indices_philox", plan.master_seed, col0, n, p, m, idx.data_ptr(), st)
-                _lib.call("skc_sketch_given", X.data_ptr(), _lib.F32, p, n, p, p, 0, spec.sign_seed, m, vcode,
-                          idx.data_ptr(), val.data_ptr(), vcode, st)
-            else:
-                _lib.call("skc_sketch", X.data_ptr(), _lib.F32, p, n, p, p, 0, spec.sign_seed, plan.master_seed, col0,
-                          m, vcode, idx.data_ptr(), val.data_ptr(), vcode, st)
 
         def step(record):
             acc.zero_()
@@ -337,27 +331,34 @@ def main():
             tri.zero_()
             if record:
                 ev[0].record()
-            sketch_call(sampler)
+            if sampler == "philox":
+                _lib.call("skc_indices_philox", plan.master_seed, col0, n, p, m, idx.data_ptr(), st)
+            else:
+                _lib.call("skc_indices", plan.master_seed, col0, n, p, m, idx.data_ptr(), st)
             if record:
                 ev[1].record()
+            _lib.call("skc_sketch_given", X.data_ptr(), _lib.F32, p, n, p, p, 0, spec.sign_seed, m, vcode,
+                      idx.data_ptr(), val.data_ptr(), vcode, st)
+            if record:
+                ev[2].record()
             _lib.call("skc_moments", idx.data_ptr(), val.data_ptr(), vcode, n, m, p, acc.data_ptr(), stats.data_ptr(),
                       ws1.data_ptr(), ws1.numel(), st)
             if record:
-                ev[2].record()
+                ev[3].record()
             _lib.call("skc_cov_accumulate", idx.data_ptr(), val.data_ptr(), vcode, n, m, p, stats.data_ptr(),
                       tri.data_ptr(), ws2.data_ptr(), ws2.numel(), st)
             if record:
-                ev[3].record()
+                ev[4].record()
             n_tot = sdist.combine_moments(acc, stats, tri, n)
             _lib.call("skc_cov_finalize", tri.data_ptr(), p, m, n_tot, C.data_ptr(), st)
             if record:
-                ev[4].record()
+                ev[5].record()
 
         for _ in range(args.warmup):
             step(False)
         barrier()
         launches0 = L.skc_launch_count()
-        sums = [0.0] * 4
+        sums = [0.0] * len(stage_names)
         with ClockSampler(local) as clk:
             t0 = torch.cuda.Event(enable_timing=True)
             t1 = torch.cuda.Event(enable_timing=True)
@@ -366,7 +367,7 @@ def main():
             for _ in range(args.steps):
                 step(True)
                 torch.cuda.synchronize()
-                for i in range(4):
+                for i in range(len(stage_names)):
                     sums[i] += ev[i].elapsed_time(ev[i + 1])
             t1.record()
             barrier()
@@ -374,7 +375,10 @@ def main():
         ms_total = t0.elapsed_time(t1)
         stage_ms = {k: sums[i] / args.steps for i, k in enumerate(stage_names)}
         ms_step = ms_total / args.steps
-        unit_bytes = {"sketch": 4 * p + 8 * m, "moments": 8 * m, "covariance": 8 * m, "finalize": 0}
+        vsz = 4 if args.compute == "f32" else 8
+        # algorithmic bytes per sample: indices write idx; gather reads the row and idx, writes values
+        unit_bytes = {"indices": 4 * m, "gather": 4 * p + 4 * m + vsz * m, "moments": (4 + vsz) * m,
+                      "covariance": (4 + vsz) * m, "finalize": 0}
         total_samples = n * world
         unit = "samples/s"
         metric = metric_name(cfg)
@@ -459,7 +463,7 @@ def main():
         for _ in range(args.warmup):
             step(False)
         barrier()
-        psums = [0.0] * 4
+        psums = [0.0] * len(stage_names)
         ksteps = max(1, min(args.steps, 5))
         p0 = torch.cuda.Event(enable_timing=True)
         p1 = torch.cuda.Event(enable_timing=True)
@@ -467,7 +471,7 @@ def main():
         for _ in range(ksteps):
             step(True)
             torch.cuda.synchronize()
-            for i in range(4):
+            for i in range(len(stage_names)):
                 psums[i] += ev[i].elapsed_time(ev[i + 1])
         p1.record()
         barrier()
@@ -477,7 +481,7 @@ def main():
         out["philox_mode"] = {
             "value": n * world / (float(pms.item()) * 1e-3), "unit": unit, "ms_per_step": float(pms.item()),
             "stages_ms": {k: psums[i] / ksteps for i, k in enumerate(stage_names)},
-            "sketch_frac_hbm": (4 * p + 8 * m) * n / (psums[0] / ksteps * 1e-3) / 1e9 / hbm_peak,
+            "gather_frac_hbm": unit_bytes["gather"] * n / (psums[1] / ksteps * 1e-3) / 1e9 / hbm_peak,
             "note": "skc_indices_philox + skc_sketch_given; uniform m-subsets, not the reference's subsets"}
         sampler = args.sampler
 
