@@ -339,6 +339,210 @@ __global__ void km_assign_reduce_kernel(const int64_t* __restrict__ blk_changed,
   }
 }
 
+// ======================================================================================
+// K5f: exact assignment by filter and verify, for tables that do not fit shared memory
+// (C5: p=2048, K=100). The exact kernel above is L2-bound there: every (point, centre)
+// gathers 2m table doubles. Here a warp takes one point at a time:
+//  filter  lanes = centres: d~ = colsq + sum_t fl32(v_t)*(-2 mu32) + mu32^2 with FMAs, and
+//          S = colsq + sum_t |v_t*(-2 mu32)| + mu32^2. A rigorous bound on |d~ - d| for the
+//          exact fp64 value d (reference order) is E = S ((2m+8) 2^-24 + (2m+1) 2^-53) 1.01:
+//          input conversion (3 u per product), recursive summation (2m u), fp64's own error.
+//          Every centre with d~ - E <= min(d~ + E) is a candidate; the exact argmin is one.
+//  verify  queued (point, candidate) pairs, 32 at a time, get the exact fp64 value in the
+//          reference order (the same arithmetic as km_assign_kernel), and each point takes
+//          the first minimum over its candidates (np.argmin), d2min = max(d, 0).
+// Labels, d2min, the changed count and the farthest point are bit-identical to K5.
+// ======================================================================================
+constexpr int kFiltWarps = 8;
+constexpr int kFiltQ = 32 + 256;  // queue: flushed once it holds >= 32 pairs (+ one point's K)
+__host__ __device__ inline size_t filt_warp_bytes(int m, int K) { return (size_t)m * 16 + (size_t)(32 + K) * 24 + 33 * 16; }
+
+__global__ void km_tables32_kernel(const double* __restrict__ mu, int64_t total, float* __restrict__ t32) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < total) t32[e] = (float)mu[e];
+}
+
+template <typename V, int NB>  // NB = ceil(K / 32) centre blocks per lane
+__global__ void __launch_bounds__(kFiltWarps * 32, 3)
+    km_assign_filter_kernel(const int32_t* __restrict__ idx, const void* __restrict__ val, int64_t n, int m,
+                            const float* __restrict__ t32, const double2* __restrict__ tab, int K,
+                            const int32_t* __restrict__ prev, int32_t* __restrict__ labels,
+                            double* __restrict__ d2min, int64_t* __restrict__ blk_changed,
+                            double* __restrict__ blk_max, int64_t* __restrict__ blk_arg) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // per warp: sidx[m] (j*K), sval[m] (double), sv32[m], queue (i, k, colsq, d), point table
+  const int qcap = 32 + K;
+  unsigned char* wb = sm + filt_warp_bytes(m, K) * warp;
+  double* sval = reinterpret_cast<double*>(wb);
+  int* sidx = reinterpret_cast<int*>(wb + (size_t)m * 8);
+  float* sv32 = reinterpret_cast<float*>(wb + (size_t)m * 12);
+  double* qc = reinterpret_cast<double*>(wb + (size_t)m * 16);  // colsq per queued pair
+  double* qd = qc + qcap;                                        // exact value per queued pair
+  int* qk = reinterpret_cast<int*>(qd + qcap);                   // centre per queued pair
+  int* qp = qk + qcap;                                           // point slot per queued pair
+  int64_t* pi = reinterpret_cast<int64_t*>(qp + qcap);           // point index per slot (32)
+  int* pstart = reinterpret_cast<int*>(pi + 33);                 // first queue entry per slot (33)
+  const double eu = ((2.0 * m + 16.0) * 0x1p-24 + (2.0 * m + 1.0) * 0x1p-53) * 1.1;
+  int64_t changed = 0;
+  double bmax = -1.0;
+  int64_t barg = -1;
+  int qn = 0, np = 0;  // queued pairs, queued points
+  auto flush = [&]() {
+    // exact values: lanes = pairs (the reference order of km_assign_kernel)
+    for (int q0 = 0; q0 < qn; q0 += 32) {
+      const int q = q0 + lane;
+      if (q < qn) {
+        const int64_t i = pi[qp[q]];
+        const int k = qk[q];
+        const int32_t* ir = idx + i * m;
+        const double* tk = reinterpret_cast<const double*>(tab + k);
+        double acc = 0.0;
+        for (int t = 0; t < m; ++t) acc = dadd(acc, dmul(ldd<V>(val, i * m + t), tk[2 * (size_t)__ldg(ir + t) * K]));
+        for (int t = 0; t < m; ++t) acc = dadd(acc, tk[2 * (size_t)__ldg(ir + t) * K + 1]);
+        qd[q] = dadd(acc, qc[q]);
+      }
+    }
+    __syncwarp();
+    // each point: first minimum over its candidates (queued in ascending k)
+    if (lane < np) {
+      const int64_t i = pi[lane];
+      double best = 0.0;
+      int bk = -1;
+      for (int q = pstart[lane]; q < pstart[lane + 1]; ++q)
+        if (bk < 0 || qd[q] < best) best = qd[q], bk = qk[q];
+      const double dm = best > 0.0 ? best : 0.0;  // np.clip(.., 0, None)
+      labels[i] = bk;
+      d2min[i] = dm;
+      if (prev != nullptr) changed += prev[i] != bk;
+      if (dm > bmax || (dm == bmax && (barg < 0 || i < barg))) bmax = dm, barg = i;
+    }
+    __syncwarp();
+    qn = 0;
+    np = 0;
+  };
+  const int64_t gw = (int64_t)blockIdx.x * kFiltWarps + warp, nw = (int64_t)gridDim.x * kFiltWarps;
+  for (int64_t i = gw; i < n; i += nw) {
+    __syncwarp();
+    for (int t = lane; t < m; t += 32) {
+      const double v = ldd<V>(val, i * m + t);
+      sidx[t] = __ldg(idx + i * m + t) * K;
+      sval[t] = v;
+      sv32[t] = (float)v;
+    }
+    __syncwarp();
+    // colsq = (v*v).sum() in numpy's pairwise order (as km_assign_kernel)
+    double colsq = 0.0;
+    if (m < 8) {
+      if (lane == 0)
+        for (int t = 0; t < m; ++t) colsq = dadd(colsq, dmul(sval[t], sval[t]));
+    } else if (m <= 128) {
+      double r = 0.0;
+      if (lane < 8) {
+        r = dmul(sval[lane], sval[lane]);
+        for (int t = 8 + lane; t < m - (m % 8); t += 8) r = dadd(r, dmul(sval[t], sval[t]));
+      }
+      const double r1 = __shfl_down_sync(kFM, r, 1);
+      const double s01 = dadd(r, r1);
+      const double s23 = __shfl_down_sync(kFM, s01, 2);
+      const double q = dadd(s01, s23);
+      const double q2 = __shfl_down_sync(kFM, q, 4);
+      if (lane == 0) {
+        colsq = dadd(q, q2);
+        for (int t = m - (m % 8); t < m; ++t) colsq = dadd(colsq, dmul(sval[t], sval[t]));
+      }
+    } else if (lane == 0) {
+      double* tmp = sval;  // square in place, restore after
+      for (int t = 0; t < m; ++t) tmp[t] = dmul(sval[t], sval[t]);
+      colsq = pw_rec(tmp, m);
+      for (int t = 0; t < m; ++t) tmp[t] = ldd<V>(val, i * m + t);
+    }
+    __syncwarp();
+    colsq = __shfl_sync(kFM, colsq, 0);
+    // filter: lane owns centres k = lane + 32 b (b < NB), one walk over the support:
+    // P = sum u^2 and Q = sum u v in fp32 (u = fl32(mu[j_t, k]), v = fl32(v_t)), d~ = P - 2Q + colsq.
+    // Cauchy-Schwarz: sum |u v| <= sqrt(P colsq), so every term's magnitude sums to at most
+    // S = P + 2 sqrt(P colsq) + colsq, and |d~ - d| <= E = S ((2m+16) 2^-24 + (2m+1) 2^-53) 1.1
+    // (input conversion, fp32 accumulation and combination, fp64's own rounding).
+    float P[NB], Q[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) P[b] = 0.f, Q[b] = 0.f;
+    const float* tl = t32 + lane;
+    bool okb[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) okb[b] = 32 * b + lane < K;
+    // unrolled by 4: 4 NB independent gathers in flight per lane
+#pragma unroll 4
+    for (int t = 0; t < m; ++t) {
+      const float* row = tl + sidx[t];
+      const float v = sv32[t];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const float u = okb[b] ? __ldg(row + 32 * b) : 0.f;
+        P[b] = fmaf(u, u, P[b]);
+        Q[b] = fmaf(u, v, Q[b]);
+      }
+    }
+    float dl[NB], el[NB];
+    float ub = __int_as_float(0x7F800000);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      dl[b] = __int_as_float(0x7F800000);
+      el[b] = 0.f;
+      if (okb[b]) {
+        const double Pd = P[b];
+        dl[b] = (float)(Pd - 2.0 * (double)Q[b] + colsq);
+        el[b] = (float)((Pd + 2.0 * sqrt(Pd * colsq) + colsq) * eu) * 1.001f;
+        ub = fminf(ub, dl[b] + el[b]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ub = fminf(ub, __shfl_xor_sync(kFM, ub, o));  // over all centres
+    // queue the candidates in ascending k
+    if (lane == 0) pi[np] = i, pstart[np] = qn;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const bool cand = okb[b] && dl[b] - el[b] <= ub;
+      const unsigned mk = __ballot_sync(kFM, cand);
+      if (cand) {
+        const int q = qn + __popc(mk & ((1u << lane) - 1u));
+        qk[q] = 32 * b + lane;
+        qp[q] = np;
+        qc[q] = colsq;
+      }
+      qn += __popc(mk);
+    }
+    ++np;
+    if (lane == 0) pstart[np] = qn;
+    __syncwarp();
+    if (qn >= 32 || np == 32) flush();
+  }
+  if (np > 0) flush();
+  // block reduction over all lanes: changed sum, (max, first index)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t oc = __shfl_xor_sync(kFM, changed, o), oa = __shfl_xor_sync(kFM, barg, o);
+    const double om = __shfl_xor_sync(kFM, bmax, o);
+    changed += oc;
+    if (oa >= 0 && (om > bmax || (om == bmax && (barg < 0 || oa < barg)))) bmax = om, barg = oa;
+  }
+  __shared__ int64_t s_ch[kFiltWarps], s_arg[kFiltWarps];
+  __shared__ double s_mx[kFiltWarps];
+  if (lane == 0) s_ch[warp] = changed, s_mx[warp] = bmax, s_arg[warp] = barg;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t c = 0, a = -1;
+    double mx = -1.0;
+    for (int w = 0; w < kFiltWarps; ++w) {
+      c += s_ch[w];
+      if (s_arg[w] >= 0 && (s_mx[w] > mx || (s_mx[w] == mx && (a < 0 || s_arg[w] < a)))) mx = s_mx[w], a = s_arg[w];
+    }
+    blk_changed[blockIdx.x] = c;
+    blk_max[blockIdx.x] = mx;
+    blk_arg[blockIdx.x] = a;
+  }
+}
+
 static int assign_grid(int64_t n) {
   int64_t g = (n + kAsgWarps - 1) / kAsgWarps;
   const int64_t cap = 4 * (int64_t)sm_count();
@@ -347,7 +551,15 @@ static int assign_grid(int64_t n) {
 }
 
 size_t assign_ws(int64_t n, int32_t p_pad, int32_t K) {
-  return (size_t)2 * p_pad * K * sizeof(double) + (size_t)assign_grid(n) * 24 + 64;
+  // [double2 table][per-block changed/max/arg][fp32 table for K5f]
+  return (size_t)2 * p_pad * K * sizeof(double) + (size_t)assign_grid(n) * 24 + (size_t)p_pad * K * 4 + 128;
+}
+// K5f instead of K5 when the packed table does not fit the shared-memory budget (SKC_ASSIGN_EXACT=1
+// keeps K5, for A/B runs and the bit-equality test)
+static bool use_filter(int32_t p_pad, int32_t K) {
+  if (K > 256) return false;
+  if (const char* e = getenv("SKC_ASSIGN_EXACT")) return e[0] != '1';
+  return (size_t)p_pad * K * 16 > 40 * 1024;
 }
 
 template <typename V, int KP>
@@ -384,6 +596,41 @@ int assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, i
   km_tables2_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(mu, total, tab);
   int rc = check_launch("km_tables2_kernel");
   if (rc) return rc;
+  if (n > 0 && use_filter(p_pad, K)) {
+    float* t32 = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(barg + G) + 127) & ~(uintptr_t)127);
+    km_tables32_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(mu, total, t32);
+    if ((rc = check_launch("km_tables32_kernel"))) return rc;
+    const size_t smem = filt_warp_bytes(m, K) * kFiltWarps;
+    int Gf = (int)((n + kFiltWarps - 1) / kFiltWarps);
+    if (Gf > G) Gf = G;  // the per-block arrays hold G entries
+    const int nb = (K + 31) / 32;
+    auto go = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kern<<<Gf, kFiltWarps * 32, smem, st>>>(idx, val, n, m, t32, tab, K, prev, labels, d2min, bch, bmx, barg);
+    };
+    if (val_f64) {
+      switch (nb) {
+        case 1: go(km_assign_filter_kernel<double, 1>); break;
+        case 2: go(km_assign_filter_kernel<double, 2>); break;
+        case 3: go(km_assign_filter_kernel<double, 3>); break;
+        case 4: go(km_assign_filter_kernel<double, 4>); break;
+        case 5: case 6: go(km_assign_filter_kernel<double, 6>); break;
+        default: go(km_assign_filter_kernel<double, 8>); break;
+      }
+    } else {
+      switch (nb) {
+        case 1: go(km_assign_filter_kernel<float, 1>); break;
+        case 2: go(km_assign_filter_kernel<float, 2>); break;
+        case 3: go(km_assign_filter_kernel<float, 3>); break;
+        case 4: go(km_assign_filter_kernel<float, 4>); break;
+        case 5: case 6: go(km_assign_filter_kernel<float, 6>); break;
+        default: go(km_assign_filter_kernel<float, 8>); break;
+      }
+    }
+    if ((rc = check_launch("km_assign_filter_kernel"))) return rc;
+    km_assign_reduce_kernel<<<1, 1024, 0, st>>>(bch, bmx, barg, Gf, out, d2max);
+    return check_launch("km_assign_reduce_kernel");
+  }
   if (n > 0) {
     if (val_f64) {
       if (K <= 8) launch_assign_kp<double, 8>(G, idx, val, n, m, tab, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);

@@ -748,6 +748,7 @@ static int launch_indices_t(SketchParams P, cudaStream_t st) {
     return check_launch("indices smem attribute");
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kIdxWarps * 32, smem);
+  if (const char* e = getenv("SKC_IDX_OCC")) occ = atoi(e) > 0 && atoi(e) < occ ? atoi(e) : occ;  // experiments
   if (occ < 1) occ = 1;
   int64_t grid = (int64_t)sm_count() * occ;
   const int64_t need = (P.n + kIdxWarps - 1) / kIdxWarps;

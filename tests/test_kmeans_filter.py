@@ -1,0 +1,67 @@
+"""K5f, exact assignment by an fp32 filter and fp64 verification (kmeans.cu), against K5.
+
+K5f runs when the packed (p, K) table does not fit shared memory (C5: p=2048, K=100). Its
+labels, d2min, changed count and farthest point must equal K5's bit for bit (K5 is pinned
+to the reference by the trajectory tests), including near-ties: clusters whose centres sit
+close together make many points' distances to two centres agree to within the fp32 error
+bound, so the verify step decides them.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def skc():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1511_00152_b200 as skc
+
+    return skc
+
+
+def _assign(skc, sk, mu, prev, exact, monkeypatch):
+    from paper_1511_00152_b200 import _lib
+
+    L = _lib.lib()
+    dev = mu.device
+    n, m = sk.indices.shape
+    K = mu.shape[1]
+    vcode = _lib.F64 if sk.values.dtype == torch.float64 else _lib.F32
+    ws = _lib.workspace(L.skc_kmeans_assign_workspace(n, sk.spec.p_pad, K), dev)
+    labels = torch.empty(n, dtype=torch.int32, device=dev)
+    d2min = torch.empty(n, dtype=torch.float64, device=dev)
+    out = torch.zeros(2, dtype=torch.int64, device=dev)
+    d2max = torch.zeros(1, dtype=torch.float64, device=dev)
+    monkeypatch.setenv("SKC_ASSIGN_EXACT", "1" if exact else "0")
+    _lib.call("skc_kmeans_assign", sk.indices.data_ptr(), sk.values.data_ptr(), vcode, n, m, mu.data_ptr(),
+              sk.spec.p_pad, K, _lib.ptr(prev), labels.data_ptr(), d2min.data_ptr(), out.data_ptr(),
+              d2max.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(dev))
+    torch.cuda.synchronize()
+    return labels.cpu().numpy(), d2min.cpu().numpy(), out.cpu().numpy(), d2max.cpu().numpy()
+
+
+@pytest.mark.parametrize("p,m,K,n,spread,compute", [
+    (2048, 102, 100, 20000, 3.0, "f64"),   # C5 shape
+    (2048, 102, 100, 20000, 0.05, "f64"),  # centres nearly on top of each other: near-ties
+    (1024, 51, 33, 9000, 1.0, "f32"),      # fp32 sketch values, ragged K
+    (512, 200, 256, 4000, 2.0, "f64"),     # largest K, m > 128 (pairwise colsq on one lane)
+])
+def test_filter_equals_exact(skc, monkeypatch, p, m, K, n, spread, compute):
+    rng = np.random.default_rng(p + K)
+    C = rng.standard_normal((p, K)) * spread
+    lab = rng.integers(0, K, n)
+    X = (C[:, lab] + rng.standard_normal((p, n))).astype(np.float32)
+    spec = skc.PreconditionSpec.create("hadamard", p, 3)
+    sk = skc.sketch_stream(X, spec, skc.SamplingPlan(4, spec.p_pad, m), compute=compute)
+    dev = sk.indices.device
+    mu = torch.as_tensor(rng.standard_normal((spec.p_pad, K)) * spread * 0.9, device=dev)
+    prev = torch.as_tensor(rng.integers(0, K, n).astype(np.int32), device=dev)
+    a = _assign(skc, sk, mu, prev, True, monkeypatch)
+    b = _assign(skc, sk, mu, prev, False, monkeypatch)
+    assert np.array_equal(a[0], b[0]), "labels"
+    assert np.array_equal(a[1], b[1]), "d2min"
+    assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3]), "changed / farthest point"
