@@ -354,7 +354,7 @@ __global__ void km_assign_reduce_kernel(const int64_t* __restrict__ blk_changed,
 // Labels, d2min, the changed count and the farthest point are bit-identical to K5.
 // ======================================================================================
 constexpr int kFiltWarps = 8;
-constexpr int kFiltQ = 32 + 256;  // queue: flushed once it holds >= 32 pairs (+ one point's K)
+// per warp queue of (point, candidate) pairs: flushed once it holds >= 32 (+ one point's K)
 __host__ __device__ inline size_t filt_warp_bytes(int m, int K) { return (size_t)m * 16 + (size_t)(32 + K) * 24 + 33 * 16; }
 
 __global__ void km_tables32_kernel(const double* __restrict__ mu, int64_t total, float* __restrict__ t32) {
@@ -362,8 +362,15 @@ __global__ void km_tables32_kernel(const double* __restrict__ mu, int64_t total,
   if (e < total) t32[e] = (float)mu[e];
 }
 
+#ifndef SKC_FILT_MINB
+#define SKC_FILT_MINB 2  // 2 CTAs per SM, 16-deep unroll: measured best for C5 (tools/ab_c5.sh)
+#endif
+#ifndef SKC_FILT_UNROLL
+#define SKC_FILT_UNROLL 16
+#endif
+constexpr int kFiltUnroll = SKC_FILT_UNROLL;
 template <typename V, int NB>  // NB = ceil(K / 32) centre blocks per lane
-__global__ void __launch_bounds__(kFiltWarps * 32, 3)
+__global__ void __launch_bounds__(kFiltWarps * 32, SKC_FILT_MINB)
     km_assign_filter_kernel(const int32_t* __restrict__ idx, const void* __restrict__ val, int64_t n, int m,
                             const float* __restrict__ t32, const double2* __restrict__ tab, int K,
                             const int32_t* __restrict__ prev, int32_t* __restrict__ labels,
@@ -471,8 +478,8 @@ __global__ void __launch_bounds__(kFiltWarps * 32, 3)
     bool okb[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) okb[b] = 32 * b + lane < K;
-    // unrolled by 4: 4 NB independent gathers in flight per lane
-#pragma unroll 4
+    // unrolled: SKC_FILT_UNROLL * NB independent gathers in flight per lane
+#pragma unroll kFiltUnroll
     for (int t = 0; t < m; ++t) {
       const float* row = tl + sidx[t];
       const float v = sv32[t];
