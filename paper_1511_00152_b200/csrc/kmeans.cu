@@ -363,10 +363,10 @@ __global__ void km_tables32_kernel(const double* __restrict__ mu, int64_t total,
 }
 
 #ifndef SKC_FILT_MINB
-#define SKC_FILT_MINB 2  // 2 CTAs per SM, 16-deep unroll: measured best for C5 (tools/ab_c5.sh)
+#define SKC_FILT_MINB 4  // 4 CTAs per SM (64 registers), 8-deep unroll: measured best for C5 (tools/ab_c5.sh)
 #endif
 #ifndef SKC_FILT_UNROLL
-#define SKC_FILT_UNROLL 16
+#define SKC_FILT_UNROLL 8
 #endif
 constexpr int kFiltUnroll = SKC_FILT_UNROLL;
 template <typename V, int NB>  // NB = ceil(K / 32) centre blocks per lane
@@ -847,17 +847,30 @@ __global__ void km_seg_scatter_kernel(const int64_t* __restrict__ off, int64_t R
   __syncwarp();
   int64_t a, b;
   seg_bounds(off, R, j, S, sg, &a, &b);
-  for (int64_t base = a; base < b; base += 32) {
-    const int64_t e = base + lane;
-    const int k = e < b ? (int)kbuf[e] : -1;
-    const uint32_t peers = __match_any_sync(kFM, k);
-    if (k >= 0) {
-      const int64_t at = q[k] + __popc(peers & lanemask_lt());
-      sorted[at] = vals[e];
+  // 4 steps of 32 elements per round: their label and value loads are all in flight before the
+  // (stable, in-order) placements
+  constexpr int kR = 4;
+  for (int64_t base = a; base < b; base += 32 * kR) {
+    int kk[kR];
+    V vv[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      const int64_t e = base + 32 * r + lane;
+      kk[r] = e < b ? (int)kbuf[e] : -1;
+      vv[r] = e < b ? vals[e] : V(0);
     }
-    __syncwarp();
-    if (k >= 0 && (peers & lanemask_lt()) == 0) q[k] += __popc(peers);
-    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      const int k = kk[r];
+      const uint32_t peers = __match_any_sync(kFM, k);
+      if (k >= 0) {
+        const int64_t at = q[k] + __popc(peers & lanemask_lt());
+        sorted[at] = vv[r];
+      }
+      __syncwarp();
+      if (k >= 0 && (peers & lanemask_lt()) == 0) q[k] += __popc(peers);
+      __syncwarp();
+    }
   }
 }
 
