@@ -127,6 +127,22 @@ int skc_kmeans_assign(const int32_t *idx, const void *val, int32_t val_dtype, in
                       double *d2min, int64_t *out, double *d2max, void *workspace, size_t ws_bytes,
                       void *stream);
 
+/* skc_kmeans_assign with the tensor-core filter (K5t, kmeans_tc.cu): identical results
+ * (labels, d2min, out, d2max bit-identical to skc_kmeans_assign). The sketch is prepared
+ * once (compact bf16 entries + numpy-order row norms) into prep with skc_kmeans_tc_prepare;
+ * each call builds the bf16 table of [-2 mu ; mu*mu], filters on tcgen05 and verifies the
+ * candidates in fp64. Applies when skc_kmeans_tc_supported(p_pad, K, m): p_pad % 32 == 0,
+ * K <= 128. Replaces _SparseOps.assign, cluster.py:181-187 (the same contract as above). */
+int skc_kmeans_tc_supported(int32_t p_pad, int32_t K, int32_t m);
+size_t skc_kmeans_tc_prepare_workspace(int64_t n, int32_t m, int32_t p_pad);
+int skc_kmeans_tc_prepare(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m, int32_t p_pad,
+                          void *prep, size_t prep_bytes, void *stream);
+size_t skc_kmeans_assign_tc_workspace(int64_t n, int32_t p_pad, int32_t K);
+int skc_kmeans_assign_tc(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m,
+                         const double *mu, int32_t p_pad, int32_t K, const int32_t *prev_labels, int32_t *labels,
+                         double *d2min, int64_t *out, double *d2max, const void *prep, void *workspace,
+                         size_t ws_bytes, void *stream);
+
 /* numpy pairwise summation of x[0..n) (objective = d2min.sum(), cluster.py:233). Bit-exact
  * to ndarray.sum. out: device[1] (=). */
 size_t skc_pairwise_sum_workspace(int64_t n);

@@ -49,6 +49,12 @@ SIGNATURES = {
     "skc_kmeans_init": (_c.c_int, [_P, _P, _I32, _I64, _I32, _P, _I32, _I32, _P, _P]),
     "skc_kmeans_assign_workspace": (_SZ, [_I64, _I32, _I32]),
     "skc_kmeans_assign": (_c.c_int, [_P, _P, _I32, _I64, _I32, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "skc_kmeans_tc_supported": (_c.c_int, [_I32, _I32, _I32]),
+    "skc_kmeans_tc_prepare_workspace": (_SZ, [_I64, _I32, _I32]),
+    "skc_kmeans_tc_prepare": (_c.c_int, [_P, _P, _I32, _I64, _I32, _I32, _P, _SZ, _P]),
+    "skc_kmeans_assign_tc_workspace": (_SZ, [_I64, _I32, _I32]),
+    "skc_kmeans_assign_tc": (_c.c_int, [_P, _P, _I32, _I64, _I32, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _SZ,
+                                        _P]),
     "skc_pairwise_sum_workspace": (_SZ, [_I64]),
     "skc_pairwise_sum": (_c.c_int, [_P, _I64, _P, _P, _SZ, _P]),
     "skc_kmeans_partials_workspace": (_SZ, [_I64, _I32, _I32, _I32]),

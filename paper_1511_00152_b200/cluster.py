@@ -13,6 +13,7 @@ row) drives the stopping rule of cluster.py:235-236.
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Optional
@@ -110,11 +111,34 @@ class SketchKMeans:
                       ch.data_ptr(), K, self.p, mu.data_ptr(), self._st())
         return mu
 
+    def _use_tc(self, K: int) -> bool:
+        # K5t (tensor-core filter) for tables beyond shared memory; SKC_ASSIGN_TC=0 disables it
+        if os.environ.get("SKC_ASSIGN_TC", "1") == "0":
+            return False
+        L = _lib.lib()
+        return self.p * K * 16 > 40 * 1024 and K > 16 and L.skc_kmeans_tc_supported(self.p, K, self.m) == 1
+
     def assign(self, mu: torch.Tensor, prev: Optional[torch.Tensor], labels: torch.Tensor, d2min: torch.Tensor,
                out: torch.Tensor, d2max: torch.Tensor) -> None:
         """cluster.py:181-187 (+ changed count vs prev, first argmax of d2min)"""
         K = mu.shape[1]
         L = _lib.lib()
+        # the first assignment (prev is None) is from seeded or K-means++ centres, which are
+        # sparse: nearly every point has near-ties there, and the fp32 filter (K5f) is the faster
+        if prev is not None and self._use_tc(K):
+            if "tcprep" not in self._ws:
+                prep = _lib.workspace(L.skc_kmeans_tc_prepare_workspace(self.n, self.m, self.p), self.dev)
+                with torch.cuda.device(self.dev):
+                    _lib.call("skc_kmeans_tc_prepare", self.idx.data_ptr(), self.val.data_ptr(), self.vcode, self.n,
+                              self.m, self.p, prep.data_ptr(), prep.numel(), self._st())
+                self._ws["tcprep"] = prep
+            prep = self._ws["tcprep"]
+            ws = self._workspace(("assign_tc", K), L.skc_kmeans_assign_tc_workspace(self.n, self.p, K))
+            with torch.cuda.device(self.dev):
+                _lib.call("skc_kmeans_assign_tc", self.idx.data_ptr(), self.val.data_ptr(), self.vcode, self.n,
+                          self.m, mu.data_ptr(), self.p, K, _lib.ptr(prev), labels.data_ptr(), d2min.data_ptr(),
+                          out.data_ptr(), d2max.data_ptr(), prep.data_ptr(), ws.data_ptr(), ws.numel(), self._st())
+            return
         ws = self._workspace("assign", L.skc_kmeans_assign_workspace(self.n, self.p, K))
         with torch.cuda.device(self.dev):
             _lib.call("skc_kmeans_assign", self.idx.data_ptr(), self.val.data_ptr(), self.vcode, self.n, self.m,

@@ -88,6 +88,12 @@ int reseed_launch(const int32_t*, const void*, int, int32_t, const int32_t*, int
                   cudaStream_t);
 int init_launch(const int32_t*, const void*, int, int32_t, const int64_t*, int32_t, int32_t, double*, cudaStream_t);
 int row_sqnorms_launch(const void*, int, int64_t, int32_t, double*, cudaStream_t);
+bool kmtc_supported(int32_t, int32_t, int32_t);
+size_t kmtc_prep_ws(int64_t, int32_t, int32_t);
+int kmtc_prepare_launch(const int32_t*, const void*, int, int64_t, int32_t, int32_t, void*, cudaStream_t);
+size_t kmtc_assign_ws(int64_t, int32_t, int32_t);
+int kmtc_assign_launch(const int32_t*, const void*, int, int64_t, int32_t, const double*, int32_t, int32_t,
+                       const int32_t*, int32_t*, double*, int64_t*, double*, const void*, void*, cudaStream_t);
 int d2_point_launch(const int32_t*, const void*, int, int64_t, int32_t, int32_t, int64_t, const double*, double*,
                     double*, cudaStream_t);
 
@@ -275,6 +281,37 @@ int skc_kmeans_assign(const int32_t* idx, const void* val, int32_t val_dtype, in
   if (ws_bytes < assign_ws(n, p_pad, K)) return fail(SKC_EPARAM, "workspace too small");
   return assign_launch(idx, val, val_dtype == SKC_F64, n, m, mu, p_pad, K, prev_labels, labels, d2min, out, d2max,
                        workspace, S(stream));
+}
+
+int skc_kmeans_tc_supported(int32_t p_pad, int32_t K, int32_t m) { return kmtc_supported(p_pad, K, m) ? 1 : 0; }
+
+size_t skc_kmeans_tc_prepare_workspace(int64_t n, int32_t m, int32_t p_pad) { return kmtc_prep_ws(n, m, p_pad); }
+
+int skc_kmeans_tc_prepare(const int32_t* idx, const void* val, int32_t val_dtype, int64_t n, int32_t m, int32_t p_pad,
+                          void* prep, size_t prep_bytes, void* stream) {
+  int rc;
+  if ((rc = check_dtype(val_dtype))) return rc;
+  if (m < 1 || m > p_pad) return fail(SKC_EDIM, "bad (m, p_pad)");
+  if (!kmtc_supported(p_pad, 1, m)) return fail(SKC_EPARAM, "tensor-core assignment needs p_pad % 32 == 0");
+  if ((size_t)8 * m * 8 > 200 * 1024) return fail(SKC_EPARAM, "m too large for the row-norm kernel");
+  if (prep_bytes < kmtc_prep_ws(n, m, p_pad)) return fail(SKC_EPARAM, "workspace too small");
+  return kmtc_prepare_launch(idx, val, val_dtype == SKC_F64, n, m, p_pad, prep, S(stream));
+}
+
+size_t skc_kmeans_assign_tc_workspace(int64_t n, int32_t p_pad, int32_t K) { return kmtc_assign_ws(n, p_pad, K); }
+
+int skc_kmeans_assign_tc(const int32_t* idx, const void* val, int32_t val_dtype, int64_t n, int32_t m,
+                         const double* mu, int32_t p_pad, int32_t K, const int32_t* prev_labels, int32_t* labels,
+                         double* d2min, int64_t* out, double* d2max, const void* prep, void* workspace,
+                         size_t ws_bytes, void* stream) {
+  int rc;
+  if ((rc = check_dtype(val_dtype))) return rc;
+  if (m < 1 || m > p_pad) return fail(SKC_EDIM, "bad (m, p_pad)");
+  if (!kmtc_supported(p_pad, K, m)) return fail(SKC_EPARAM, "tensor-core assignment needs p_pad % 32 == 0, K <= 128");
+  if ((size_t)8 * m * 20 > 227 * 1024) return fail(SKC_EPARAM, "m too large for the assignment kernel");
+  if (ws_bytes < kmtc_assign_ws(n, p_pad, K)) return fail(SKC_EPARAM, "workspace too small");
+  return kmtc_assign_launch(idx, val, val_dtype == SKC_F64, n, m, mu, p_pad, K, prev_labels, labels, d2min, out, d2max,
+                            prep, workspace, S(stream));
 }
 
 size_t skc_pairwise_sum_workspace(int64_t n) {

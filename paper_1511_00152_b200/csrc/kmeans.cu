@@ -357,9 +357,28 @@ constexpr int kFiltWarps = 8;
 // per warp queue of (point, candidate) pairs: flushed once it holds >= 32 (+ one point's K)
 __host__ __device__ inline size_t filt_warp_bytes(int m, int K) { return (size_t)m * 16 + (size_t)(32 + K) * 24 + 33 * 16; }
 
-__global__ void km_tables32_kernel(const double* __restrict__ mu, int64_t total, float* __restrict__ t32) {
+// fp32 copy of mu as [p][K4] rows (K4 = K rounded up to 4, zero padded): a lane reads 4 centres
+// with one 16-byte load
+__global__ void km_tables32_kernel(const double* __restrict__ mu, int32_t p_pad, int K, int K4,
+                                   float* __restrict__ t32) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e < total) t32[e] = (float)mu[e];
+  if (e >= (int64_t)p_pad * K4) return;
+  const int64_t j = e / K4;
+  const int k = (int)(e - j * K4);
+  t32[e] = k < K ? (float)mu[j * K + k] : 0.f;
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t x, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(x));
 }
 
 #ifndef SKC_FILT_MINB
@@ -369,13 +388,15 @@ __global__ void km_tables32_kernel(const double* __restrict__ mu, int64_t total,
 #define SKC_FILT_UNROLL 8
 #endif
 constexpr int kFiltUnroll = SKC_FILT_UNROLL;
-template <typename V, int NB>  // NB = ceil(K / 32) centre blocks per lane
+template <typename V, int NB>  // NB = ceil(K4 / 128) blocks of 4 centres per lane
 __global__ void __launch_bounds__(kFiltWarps * 32, SKC_FILT_MINB)
     km_assign_filter_kernel(const int32_t* __restrict__ idx, const void* __restrict__ val, int64_t n, int m,
-                            const float* __restrict__ t32, const double2* __restrict__ tab, int K,
+                            const float* __restrict__ t32, int K4, const double2* __restrict__ tab, int K,
                             const int32_t* __restrict__ prev, int32_t* __restrict__ labels,
                             double* __restrict__ d2min, int64_t* __restrict__ blk_changed,
-                            double* __restrict__ blk_max, int64_t* __restrict__ blk_arg) {
+                            double* __restrict__ blk_max, int64_t* __restrict__ blk_arg,
+                            const int64_t* __restrict__ list, const int32_t* __restrict__ list_n) {
+  // list != nullptr: only the points list[0 .. *list_n) (K5t's unresolved points)
   extern __shared__ __align__(16) unsigned char sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // per warp: sidx[m] (j*K), sval[m] (double), sv32[m], queue (i, k, colsq, d), point table
@@ -416,8 +437,8 @@ __global__ void __launch_bounds__(kFiltWarps * 32, SKC_FILT_MINB)
       const int64_t i = pi[lane];
       double best = 0.0;
       int bk = -1;
-      for (int q = pstart[lane]; q < pstart[lane + 1]; ++q)
-        if (bk < 0 || qd[q] < best) best = qd[q], bk = qk[q];
+      for (int q = pstart[lane]; q < pstart[lane + 1]; ++q)  // queued in any order: lowest k on ties
+        if (bk < 0 || qd[q] < best || (qd[q] == best && qk[q] < bk)) best = qd[q], bk = qk[q];
       const double dm = best > 0.0 ? best : 0.0;  // np.clip(.., 0, None)
       labels[i] = bk;
       d2min[i] = dm;
@@ -429,11 +450,13 @@ __global__ void __launch_bounds__(kFiltWarps * 32, SKC_FILT_MINB)
     np = 0;
   };
   const int64_t gw = (int64_t)blockIdx.x * kFiltWarps + warp, nw = (int64_t)gridDim.x * kFiltWarps;
-  for (int64_t i = gw; i < n; i += nw) {
+  const int64_t cnt = list ? (int64_t)*list_n : n;
+  for (int64_t li = gw; li < cnt; li += nw) {
+    const int64_t i = list ? list[li] : li;
     __syncwarp();
     for (int t = lane; t < m; t += 32) {
       const double v = ldd<V>(val, i * m + t);
-      sidx[t] = __ldg(idx + i * m + t) * K;
+      sidx[t] = __ldg(idx + i * m + t) * K4;
       sval[t] = v;
       sv32[t] = (float)v;
     }
@@ -471,53 +494,70 @@ __global__ void __launch_bounds__(kFiltWarps * 32, SKC_FILT_MINB)
     // Cauchy-Schwarz: sum |u v| <= sqrt(P colsq), so every term's magnitude sums to at most
     // S = P + 2 sqrt(P colsq) + colsq, and |d~ - d| <= E = S ((2m+16) 2^-24 + (2m+1) 2^-53) 1.1
     // (input conversion, fp32 accumulation and combination, fp64's own rounding).
-    float P[NB], Q[NB];
+    // P, Q as packed fp32 pairs: lane owns centres k = 128 b + 4 lane + c (c < 4)
+    uint64_t P[NB][2], Q[NB][2];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) P[b] = 0.f, Q[b] = 0.f;
-    const float* tl = t32 + lane;
+    for (int b = 0; b < NB; ++b) P[b][0] = P[b][1] = Q[b][0] = Q[b][1] = 0;
+    const float* tl = t32 + 4 * lane;
     bool okb[NB];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) okb[b] = 32 * b + lane < K;
-    // unrolled: SKC_FILT_UNROLL * NB independent gathers in flight per lane
+    for (int b = 0; b < NB; ++b) okb[b] = 128 * b + 4 * lane < K4;
+    // unrolled: SKC_FILT_UNROLL * NB independent 16-byte gathers in flight per lane
 #pragma unroll kFiltUnroll
     for (int t = 0; t < m; ++t) {
       const float* row = tl + sidx[t];
       const float v = sv32[t];
+      const uint64_t vv = pk2(v, v);
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
-        const float u = okb[b] ? __ldg(row + 32 * b) : 0.f;
-        P[b] = fmaf(u, u, P[b]);
-        Q[b] = fmaf(u, v, Q[b]);
+        const float4 u = okb[b] ? __ldg(reinterpret_cast<const float4*>(row + 128 * b)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const uint64_t u01 = pk2(u.x, u.y), u23 = pk2(u.z, u.w);
+        P[b][0] = fma2(u01, u01, P[b][0]);
+        P[b][1] = fma2(u23, u23, P[b][1]);
+        Q[b][0] = fma2(u01, vv, Q[b][0]);
+        Q[b][1] = fma2(u23, vv, Q[b][1]);
       }
     }
-    float dl[NB], el[NB];
+    float dl[NB][4], el[NB][4];
     float ub = __int_as_float(0x7F800000);
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-      dl[b] = __int_as_float(0x7F800000);
-      el[b] = 0.f;
-      if (okb[b]) {
-        const double Pd = P[b];
-        dl[b] = (float)(Pd - 2.0 * (double)Q[b] + colsq);
-        el[b] = (float)((Pd + 2.0 * sqrt(Pd * colsq) + colsq) * eu) * 1.001f;
-        ub = fminf(ub, dl[b] + el[b]);
+      float pf[4], qf[4];
+      upk2(P[b][0], pf[0], pf[1]);
+      upk2(P[b][1], pf[2], pf[3]);
+      upk2(Q[b][0], qf[0], qf[1]);
+      upk2(Q[b][1], qf[2], qf[3]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        dl[b][c] = __int_as_float(0x7F800000);
+        el[b][c] = 0.f;
+        if (128 * b + 4 * lane + c < K) {
+          const double Pd = pf[c];
+          dl[b][c] = (float)(Pd - 2.0 * (double)qf[c] + colsq);
+          el[b][c] = (float)((Pd + 2.0 * sqrt(Pd * colsq) + colsq) * eu) * 1.001f;
+          ub = fminf(ub, dl[b][c] + el[b][c]);
+        }
       }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ub = fminf(ub, __shfl_xor_sync(kFM, ub, o));  // over all centres
-    // queue the candidates in ascending k
+    // queue the candidates (the flush breaks ties by the lowest k, so any queue order works)
     if (lane == 0) pi[np] = i, pstart[np] = qn;
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-      const bool cand = okb[b] && dl[b] - el[b] <= ub;
-      const unsigned mk = __ballot_sync(kFM, cand);
-      if (cand) {
-        const int q = qn + __popc(mk & ((1u << lane) - 1u));
-        qk[q] = 32 * b + lane;
-        qp[q] = np;
-        qc[q] = colsq;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int k = 128 * b + 4 * lane + c;
+        const bool cand = k < K && dl[b][c] - el[b][c] <= ub;
+        const unsigned mk = __ballot_sync(kFM, cand);
+        if (cand) {
+          const int q = qn + __popc(mk & ((1u << lane) - 1u));
+          qk[q] = k;
+          qp[q] = np;
+          qc[q] = colsq;
+        }
+        qn += __popc(mk);
       }
-      qn += __popc(mk);
     }
     ++np;
     if (lane == 0) pstart[np] = qn;
@@ -559,7 +599,8 @@ static int assign_grid(int64_t n) {
 
 size_t assign_ws(int64_t n, int32_t p_pad, int32_t K) {
   // [double2 table][per-block changed/max/arg][fp32 table for K5f]
-  return (size_t)2 * p_pad * K * sizeof(double) + (size_t)assign_grid(n) * 24 + (size_t)p_pad * K * 4 + 128;
+  return (size_t)2 * p_pad * K * sizeof(double) + (size_t)assign_grid(n) * 24 + (size_t)p_pad * ((K + 3) & ~3) * 4 +
+         128;
 }
 // K5f instead of K5 when the packed table does not fit the shared-memory budget (SKC_ASSIGN_EXACT=1
 // keeps K5, for A/B runs and the bit-equality test)
@@ -606,33 +647,27 @@ int assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, i
   if (rc) return rc;
   if (n > 0 && use_filter(p_pad, K)) {
     float* t32 = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(barg + G) + 127) & ~(uintptr_t)127);
-    km_tables32_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(mu, total, t32);
+    const int K4 = (K + 3) & ~3;
+    km_tables32_kernel<<<(unsigned)(((int64_t)p_pad * K4 + 255) / 256), 256, 0, st>>>(mu, p_pad, K, K4, t32);
     if ((rc = check_launch("km_tables32_kernel"))) return rc;
     const size_t smem = filt_warp_bytes(m, K) * kFiltWarps;
     int Gf = (int)((n + kFiltWarps - 1) / kFiltWarps);
     if (Gf > G) Gf = G;  // the per-block arrays hold G entries
-    const int nb = (K + 31) / 32;
+    const int nb = (K4 + 127) / 128;
     auto go = [&](auto kern) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kern<<<Gf, kFiltWarps * 32, smem, st>>>(idx, val, n, m, t32, tab, K, prev, labels, d2min, bch, bmx, barg);
+      kern<<<Gf, kFiltWarps * 32, smem, st>>>(idx, val, n, m, t32, K4, tab, K, prev, labels, d2min, bch, bmx, barg,
+                                               nullptr, nullptr);
     };
     if (val_f64) {
       switch (nb) {
         case 1: go(km_assign_filter_kernel<double, 1>); break;
-        case 2: go(km_assign_filter_kernel<double, 2>); break;
-        case 3: go(km_assign_filter_kernel<double, 3>); break;
-        case 4: go(km_assign_filter_kernel<double, 4>); break;
-        case 5: case 6: go(km_assign_filter_kernel<double, 6>); break;
-        default: go(km_assign_filter_kernel<double, 8>); break;
+        default: go(km_assign_filter_kernel<double, 2>); break;  // use_filter: K <= 256
       }
     } else {
       switch (nb) {
         case 1: go(km_assign_filter_kernel<float, 1>); break;
-        case 2: go(km_assign_filter_kernel<float, 2>); break;
-        case 3: go(km_assign_filter_kernel<float, 3>); break;
-        case 4: go(km_assign_filter_kernel<float, 4>); break;
-        case 5: case 6: go(km_assign_filter_kernel<float, 6>); break;
-        default: go(km_assign_filter_kernel<float, 8>); break;
+        default: go(km_assign_filter_kernel<float, 2>); break;  // use_filter: K <= 256
       }
     }
     if ((rc = check_launch("km_assign_filter_kernel"))) return rc;
@@ -654,6 +689,45 @@ int assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, i
   }
   km_assign_reduce_kernel<<<1, 1024, 0, st>>>(bch, bmx, barg, n > 0 ? G : 0, out, d2max);
   return check_launch("km_assign_reduce_kernel");
+}
+
+// K5f over a device-side list of points (K5t's unresolved points), G blocks of partials
+int assign_filter_list_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m,
+                              const double* mu, int32_t p_pad, int32_t K, const int32_t* prev, int32_t* labels,
+                              double* d2min, const int64_t* list, const int32_t* list_n, const double2* tab,
+                              float* t32, int64_t* bch, double* bmx, int64_t* barg, int G, cudaStream_t st) {
+  if (K > 256) return fail(SKC_EPARAM, "K5f list pass needs K <= 256");
+  const int K4 = (K + 3) & ~3;
+  km_tables32_kernel<<<(unsigned)(((int64_t)p_pad * K4 + 255) / 256), 256, 0, st>>>(mu, p_pad, K, K4, t32);
+  int rc = check_launch("km_tables32_kernel");
+  if (rc) return rc;
+  const size_t smem = filt_warp_bytes(m, K) * kFiltWarps;
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<G, kFiltWarps * 32, smem, st>>>(idx, val, n, m, t32, K4, tab, K, prev, labels, d2min, bch, bmx, barg, list,
+                                            list_n);
+  };
+  const int nb = (K4 + 127) / 128;
+  if (val_f64) {
+    if (nb == 1) go(km_assign_filter_kernel<double, 1>);
+    else go(km_assign_filter_kernel<double, 2>);
+  } else {
+    if (nb == 1) go(km_assign_filter_kernel<float, 1>);
+    else go(km_assign_filter_kernel<float, 2>);
+  }
+  return check_launch("km_assign_filter_kernel (list)");
+}
+
+int assign_reduce_launch(const int64_t* bch, const double* bmx, const int64_t* barg, int G, int64_t* out,
+                         double* d2max, cudaStream_t st) {
+  km_assign_reduce_kernel<<<1, 1024, 0, st>>>(bch, bmx, barg, G, out, d2max);
+  return check_launch("km_assign_reduce_kernel");
+}
+
+int tables2_launch(const double* mu, int32_t p_pad, int32_t K, double2* tab, cudaStream_t st) {
+  const int64_t total = (int64_t)p_pad * K;
+  km_tables2_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(mu, total, tab);
+  return check_launch("km_tables2_kernel");
 }
 
 // ---------------------------------------------------------------------------------
@@ -901,6 +975,104 @@ __global__ void km_chain_sum_kernel(const int64_t* __restrict__ pos0, const V* _
   counts[c] = b - a;
 }
 
+// Walk path (default where K fits shared memory): one warp walks one coordinate's whole
+// list in order, 32 entries per step, with kWalkAhead steps of loads in flight (rows and
+// values stream, labels are gathered). Lanes holding equal labels (match_any) add into the
+// warp's acc[k] in rank order, one round per rank, so every (j, k) chain is still the
+// sequential fp64 sum in ascending point index: no scatter, no scan, no sorted copy.
+constexpr int kWalkWarps = 4;
+#ifndef SKC_WALK_AHEAD
+#define SKC_WALK_AHEAD 8
+#endif
+constexpr int kWalkAhead = SKC_WALK_AHEAD;  // steps of 32 entries per group; groups are software-pipelined
+template <typename V>
+__global__ void __launch_bounds__(kWalkWarps * 32) km_walk_kernel(const int64_t* __restrict__ off, int64_t R,
+                                                                  const int32_t* __restrict__ rows,
+                                                                  const V* __restrict__ vals,
+                                                                  const int32_t* __restrict__ labels, int32_t p_pad,
+                                                                  int K, double* __restrict__ sums,
+                                                                  int64_t* __restrict__ counts) {
+  extern __shared__ double wacc[];  // [warps][K] fp64 sums, then [warps][K] int32 counts
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t j = blockIdx.x * (int64_t)kWalkWarps + warp;
+  if (j >= p_pad) return;
+  double* acc = wacc + (size_t)warp * K;
+  int* cnt = reinterpret_cast<int*>(wacc + (size_t)kWalkWarps * K) + (size_t)warp * K;
+  for (int k = lane; k < K; k += 32) acc[k] = 0.0, cnt[k] = 0;
+  __syncwarp();
+  const int64_t a = off[j * R], b = off[(j + 1) * R];
+  const uint32_t lt = lanemask_lt();
+  constexpr int G = 32 * kWalkAhead;
+  // three groups in flight: rows/values of group g+2 load, labels of group g+1 gather, group g adds
+  int r1[kWalkAhead], r2[kWalkAhead], k1[kWalkAhead];
+  V v0[kWalkAhead], v1[kWalkAhead], v2[kWalkAhead];
+  int k0[kWalkAhead];
+  auto load_rv = [&](int64_t base, int (&rr)[kWalkAhead], V (&vv)[kWalkAhead]) {
+#pragma unroll
+    for (int s = 0; s < kWalkAhead; ++s) {
+      const int64_t e = base + 32 * s + lane;
+      rr[s] = e < b ? __ldg(rows + e) : -1;
+      vv[s] = e < b ? __ldg(vals + e) : V(0);
+    }
+  };
+  auto gather = [&](const int (&rr)[kWalkAhead], int (&kk)[kWalkAhead]) {
+#pragma unroll
+    for (int s = 0; s < kWalkAhead; ++s) kk[s] = rr[s] >= 0 ? __ldg(labels + rr[s]) : -1;
+  };
+  int r0[kWalkAhead];
+  load_rv(a, r0, v0);
+  load_rv(a + G, r1, v1);
+  gather(r0, k0);
+  for (int64_t base = a; base < b; base += G) {
+    gather(r1, k1);                 // labels of group g+1
+    load_rv(base + 2 * G, r2, v2);  // rows and values of group g+2
+    // the group's label matches are independent of the sums: all in flight before the adds
+    uint32_t peers[kWalkAhead];
+    int last[kWalkAhead];
+#pragma unroll
+    for (int s = 0; s < kWalkAhead; ++s) peers[s] = __match_any_sync(kFM, k0[s]);
+#pragma unroll
+    for (int s = 0; s < kWalkAhead; ++s) last[s] = __reduce_max_sync(kFM, k0[s] >= 0 ? __popc(peers[s]) : 0);
+#pragma unroll
+    for (int s = 0; s < kWalkAhead; ++s) {
+      // the leader (lowest lane) of each label adds its peers' values in lane (= point) order
+      const int k = k0[s];
+      const bool lead = k >= 0 && (peers[s] & lt) == 0;
+      double t = lead ? acc[k] : 0.0;
+      uint32_t rem = peers[s];
+      for (int q = 0; q < last[s]; ++q) {
+        const int src = rem ? __ffs(rem) - 1 : lane;
+        const double vq = __shfl_sync(kFM, (double)v0[s], src);
+        if (lead && rem) t = dadd(t, vq);
+        rem &= rem - 1;
+      }
+      if (lead) {
+        acc[k] = t;
+        cnt[k] += __popc(peers[s]);
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int s = 0; s < kWalkAhead; ++s) {
+      k0[s] = k1[s];
+      v0[s] = v1[s];
+      r1[s] = r2[s];
+      v1[s] = v2[s];
+    }
+  }
+  __syncwarp();
+  for (int k = lane; k < K; k += 32) {
+    sums[j * K + k] = acc[k];
+    counts[j * K + k] = cnt[k];
+  }
+}
+
+static size_t walk_smem(int K) { return (size_t)kWalkWarps * K * 12; }
+static bool use_walk(int K) {
+  if (const char* e = getenv("SKC_PARTIALS")) return e[0] != 's';  // A/B: SKC_PARTIALS=seg
+  return walk_smem(K) <= 96 * 1024;
+}
+
 // cluster sizes: bincount(labels), exact
 __global__ void km_sizes_kernel(const int32_t* __restrict__ labels, int64_t n, int K, int64_t* __restrict__ sizes) {
   extern __shared__ int hs[];
@@ -959,7 +1131,20 @@ int csc_build_launch(const int32_t* idx, const void* val, int val_f64, int64_t n
   return SKC_OK;
 }
 
+static int sizes_launch(const int32_t* labels, int64_t n, int32_t K, int64_t* sizes, cudaStream_t st) {
+  cudaMemsetAsync(sizes, 0, (size_t)K * 8, st);
+  if (n > 0) {
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 4LL * sm_count()) blocks = 4LL * sm_count();
+    cudaFuncSetAttribute(km_sizes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(K * 4));
+    km_sizes_kernel<<<(unsigned)blocks, 256, (size_t)K * 4, st>>>(labels, n, K, sizes);
+    return check_launch("km_sizes_kernel");
+  }
+  return SKC_OK;
+}
+
 size_t seg_ws(int64_t n, int32_t m, int32_t p_pad, int32_t K, int val_f64) {
+  if (use_walk(K)) return 256;  // the walk path needs no per-iteration scratch
   return seg_layout(n, m, p_pad, K, val_f64).total;
 }
 
@@ -971,6 +1156,22 @@ int csc_partials_launch(const void* ws, int val_f64, int64_t n, int32_t m, int32
   char* g = reinterpret_cast<char*>(seg_ws_ptr);
   const int64_t* off = reinterpret_cast<const int64_t*>(w + L.off_off);
   const int32_t* rows = reinterpret_cast<const int32_t*>(w + L.off_rows);
+  int rc;
+  if (use_walk(K)) {
+    const unsigned wgrid = (unsigned)((p_pad + kWalkWarps - 1) / kWalkWarps);
+    const size_t wsm = walk_smem(K);
+    if (val_f64) {
+      cudaFuncSetAttribute(km_walk_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
+      km_walk_kernel<double><<<wgrid, kWalkWarps * 32, wsm, st>>>(
+          off, L.R, rows, reinterpret_cast<const double*>(w + L.off_vals), labels, p_pad, K, sums, counts);
+    } else {
+      cudaFuncSetAttribute(km_walk_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
+      km_walk_kernel<float><<<wgrid, kWalkWarps * 32, wsm, st>>>(
+          off, L.R, rows, reinterpret_cast<const float*>(w + L.off_vals), labels, p_pad, K, sums, counts);
+    }
+    if ((rc = check_launch("km_walk_kernel"))) return rc;
+    return sizes_launch(labels, n, K, sizes, st);
+  }
   uint8_t* kbuf = reinterpret_cast<uint8_t*>(g + G.off_kbuf);
   int64_t* seg = reinterpret_cast<int64_t*>(g + G.off_seg);
   const int S = G.S;
@@ -978,7 +1179,6 @@ int csc_partials_launch(const void* ws, int val_f64, int64_t n, int32_t m, int32
   const int64_t cells = (int64_t)p_pad * K * S + 1;
   constexpr int kW = 4;  // warps per CTA (one segment each)
   const unsigned grid = (unsigned)((items + kW - 1) / kW);
-  int rc;
   cudaMemsetAsync(seg + cells - 1, 0, 8, st);
   cudaFuncSetAttribute(km_seg_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kW * K * 4));
   km_seg_hist_kernel<<<grid, kW * 32, (size_t)kW * K * 4, st>>>(off, L.R, rows, labels, p_pad, K, S, kbuf, seg);
@@ -1004,15 +1204,7 @@ int csc_partials_launch(const void* ws, int val_f64, int64_t n, int32_t m, int32
     km_chain_sum_kernel<float><<<cgrid, 32, 0, st>>>(seg, sorted, p_pad, K, S, sums, counts);
   }
   if ((rc = check_launch("km_chain_sum_kernel"))) return rc;
-  cudaMemsetAsync(sizes, 0, (size_t)K * 8, st);
-  if (n > 0) {
-    int64_t blocks = (n + 255) / 256;
-    if (blocks > 4LL * sm_count()) blocks = 4LL * sm_count();
-    cudaFuncSetAttribute(km_sizes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(K * 4));
-    km_sizes_kernel<<<(unsigned)blocks, 256, (size_t)K * 4, st>>>(labels, n, K, sizes);
-    if ((rc = check_launch("km_sizes_kernel"))) return rc;
-  }
-  return SKC_OK;
+  return sizes_launch(labels, n, K, sizes, st);
 }
 
 // ---------------------------------------------------------------------------------

@@ -686,6 +686,7 @@ static int launch_gather_t(SketchParams P, cudaStream_t st) {
     return check_launch("gather smem attribute");
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
+  if (const char* e = getenv("SKC_GATHER_OCC")) occ = atoi(e) > 0 && atoi(e) < occ ? atoi(e) : occ;  // experiments
   if (occ < 1) occ = 1;
   P.num_tiles = (P.n + G::S - 1) / G::S;
   int64_t grid = (int64_t)sm_count() * occ;

@@ -1,4 +1,5 @@
-"""K5f, exact assignment by an fp32 filter and fp64 verification (kmeans.cu), against K5.
+"""K5f (fp32 filter) and K5t (tensor-core bf16 filter, kmeans_tc.cu), each followed by fp64
+verification, against the exact assignment K5.
 
 K5f runs when the packed (p, K) table does not fit shared memory (C5: p=2048, K=100). Its
 labels, d2min, changed count and farthest point must equal K5's bit for bit (K5 is pinned
@@ -62,6 +63,59 @@ def test_filter_equals_exact(skc, monkeypatch, p, m, K, n, spread, compute):
     prev = torch.as_tensor(rng.integers(0, K, n).astype(np.int32), device=dev)
     a = _assign(skc, sk, mu, prev, True, monkeypatch)
     b = _assign(skc, sk, mu, prev, False, monkeypatch)
+    assert np.array_equal(a[0], b[0]), "labels"
+    assert np.array_equal(a[1], b[1]), "d2min"
+    assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3]), "changed / farthest point"
+
+
+def _assign_tc(skc, sk, mu, prev):
+    from paper_1511_00152_b200 import _lib
+
+    L = _lib.lib()
+    dev = mu.device
+    n, m = sk.indices.shape
+    K, p_pad = mu.shape[1], sk.spec.p_pad
+    assert L.skc_kmeans_tc_supported(p_pad, K, m) == 1
+    vcode = _lib.F64 if sk.values.dtype == torch.float64 else _lib.F32
+    prep = _lib.workspace(L.skc_kmeans_tc_prepare_workspace(n, m, p_pad), dev)
+    st = _lib.stream_ptr(dev)
+    _lib.call("skc_kmeans_tc_prepare", sk.indices.data_ptr(), sk.values.data_ptr(), vcode, n, m, p_pad,
+              prep.data_ptr(), prep.numel(), st)
+    ws = _lib.workspace(L.skc_kmeans_assign_tc_workspace(n, p_pad, K), dev)
+    labels = torch.empty(n, dtype=torch.int32, device=dev)
+    d2min = torch.empty(n, dtype=torch.float64, device=dev)
+    out = torch.zeros(2, dtype=torch.int64, device=dev)
+    d2max = torch.zeros(1, dtype=torch.float64, device=dev)
+    _lib.call("skc_kmeans_assign_tc", sk.indices.data_ptr(), sk.values.data_ptr(), vcode, n, m, mu.data_ptr(), p_pad,
+              K, _lib.ptr(prev), labels.data_ptr(), d2min.data_ptr(), out.data_ptr(), d2max.data_ptr(),
+              prep.data_ptr(), ws.data_ptr(), ws.numel(), st)
+    torch.cuda.synchronize()
+    return labels.cpu().numpy(), d2min.cpu().numpy(), out.cpu().numpy(), d2max.cpu().numpy()
+
+
+@pytest.mark.parametrize("p,m,K,n,spread,compute,init", [
+    (2048, 102, 100, 20000, 3.0, "f64", "dense"),   # C5 shape
+    (2048, 102, 100, 20000, 3.0, "f64", "points"),  # sparse initial centres: most points unresolved
+    (2048, 102, 100, 9001, 0.05, "f64", "dense"),   # near-ties, ragged tile pairs
+    (1024, 51, 33, 9000, 1.0, "f32", "dense"),      # fp32 sketch values, ragged K
+    (512, 200, 128, 4000, 2.0, "f64", "dense"),     # largest K, m > 128
+    (256, 25, 1, 700, 1.0, "f64", "dense"),         # one centre
+])
+def test_tc_filter_equals_exact(skc, monkeypatch, p, m, K, n, spread, compute, init):
+    rng = np.random.default_rng(p + K + n)
+    C = rng.standard_normal((p, K)) * spread
+    lab = rng.integers(0, K, n)
+    X = (C[:, lab] + rng.standard_normal((p, n))).astype(np.float32)
+    spec = skc.PreconditionSpec.create("hadamard", p, 3)
+    sk = skc.sketch_stream(X, spec, skc.SamplingPlan(4, spec.p_pad, m), compute=compute)
+    dev = sk.indices.device
+    if init == "points":
+        mu = skc.SketchKMeans(sk).init_centers(rng.choice(n, K, replace=False))
+    else:
+        mu = torch.as_tensor(rng.standard_normal((spec.p_pad, K)) * spread * 0.9, device=dev)
+    prev = torch.as_tensor(rng.integers(0, K, n).astype(np.int32), device=dev)
+    a = _assign(skc, sk, mu, prev, True, monkeypatch)
+    b = _assign_tc(skc, sk, mu, prev)
     assert np.array_equal(a[0], b[0]), "labels"
     assert np.array_equal(a[1], b[1]), "d2min"
     assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3]), "changed / farthest point"

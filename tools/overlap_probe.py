@@ -58,9 +58,11 @@ def both():
     gat(s2)
 
 
-for occ in ("8", "6", "4", "3"):
-    os.environ["SKC_IDX_OCC"] = occ
+for gocc, iocc in (("3", "8"), ("2", "3"), ("2", "4"), ("1", "5"), ("1", "6"), ("2", "2")):
+    os.environ["SKC_IDX_OCC"] = iocc
+    os.environ["SKC_GATHER_OCC"] = gocc
     a = timed(lambda: ind(torch.cuda.current_stream()))
     b = timed(lambda: gat(torch.cuda.current_stream()))
     c = timed(both)
-    print(f"idx occ {occ}: indices {a:6.2f} ms, gather {b:6.2f} ms, sum {a + b:6.2f}, concurrent {c:6.2f} ms", flush=True)
+    print(f"gather occ {gocc} idx occ {iocc}: indices {a:6.2f} ms, gather {b:6.2f} ms, sum {a + b:6.2f}, "
+          f"concurrent {c:6.2f} ms", flush=True)
