@@ -1068,9 +1068,12 @@ __global__ void __launch_bounds__(kWalkWarps * 32) km_walk_kernel(const int64_t*
 }
 
 static size_t walk_smem(int K) { return (size_t)kWalkWarps * K * 12; }
-static bool use_walk(int K) {
-  if (const char* e = getenv("SKC_PARTIALS")) return e[0] != 's';  // A/B: SKC_PARTIALS=seg
-  return walk_smem(K) <= 96 * 1024;
+// The walk has one warp per coordinate list: it needs enough lists to fill the GPU (C5, p = 2048:
+// 8.7 vs 24 ms per iteration); with few lists the segment path's thousands of segments win
+// (C2, p = 512: 2.17 vs 2.44 ms per 6-iteration run).
+static bool use_walk(int32_t p_pad, int K) {
+  if (const char* e = getenv("SKC_PARTIALS")) return e[0] != 's';  // A/B: SKC_PARTIALS=seg|walk
+  return walk_smem(K) <= 96 * 1024 && p_pad >= 1024;
 }
 
 // cluster sizes: bincount(labels), exact
@@ -1144,7 +1147,7 @@ static int sizes_launch(const int32_t* labels, int64_t n, int32_t K, int64_t* si
 }
 
 size_t seg_ws(int64_t n, int32_t m, int32_t p_pad, int32_t K, int val_f64) {
-  if (use_walk(K)) return 256;  // the walk path needs no per-iteration scratch
+  if (use_walk(p_pad, K)) return 256;  // the walk path needs no per-iteration scratch
   return seg_layout(n, m, p_pad, K, val_f64).total;
 }
 
@@ -1157,7 +1160,7 @@ int csc_partials_launch(const void* ws, int val_f64, int64_t n, int32_t m, int32
   const int64_t* off = reinterpret_cast<const int64_t*>(w + L.off_off);
   const int32_t* rows = reinterpret_cast<const int32_t*>(w + L.off_rows);
   int rc;
-  if (use_walk(K)) {
+  if (use_walk(p_pad, K)) {
     const unsigned wgrid = (unsigned)((p_pad + kWalkWarps - 1) / kWalkWarps);
     const size_t wsm = walk_smem(K);
     if (val_f64) {

@@ -54,6 +54,8 @@ constexpr int kPts = kRows * kTiles;
 #endif
 constexpr int kChunk = SKC_KT_CHUNK;  // coordinates per stage
 constexpr int kKC = 2 * kChunk;       // K elements per stage: values part, then ones part
+constexpr int kRowShift = 16 + (kChunk == 32 ? 5 : kChunk == 64 ? 6 : 4);  // list entry: value | x | row
+static_assert(kChunk == 16 || kChunk == 32 || kChunk == 64, "chunk of 16, 32 or 64 coordinates");
 constexpr int kSBO = kKC * 16;        // bytes between 8-row core-matrix groups
 constexpr int kTileA = kRows * kKC * 2;
 #ifndef SKC_KT_STAGES
@@ -156,7 +158,7 @@ __global__ void km_tc_entries_kernel(const int32_t* __restrict__ idx, const V* _
 }
 
 // per tile pair and 32-coordinate chunk, the list of its entries as u32 (bf16 value | x << 16 |
-// row << 21, x = coordinate - chunk start), so each stage's A operand is a zero fill plus one
+// row << kRowShift, x = coordinate - chunk start), so each stage's A operand is a zero fill plus one
 // coalesced pass over a short list. offs[tp][c] (nch + 1 per tile pair) index into the tile
 // pair's 256 m entries; the order inside a list is irrelevant (positions are distinct).
 template <typename V>
@@ -197,7 +199,7 @@ __global__ void __launch_bounds__(kPts) km_tc_bucket_kernel(const int32_t* __res
       for (int t = 0; t < m; ++t) {
         const uint32_t j = (uint32_t)__ldg(idx + i * m + t);
         const uint32_t b = __bfloat16_as_ushort(__double2bfloat16((double)__ldg(val + i * m + t)));
-        L[atomicAdd(&pos[j / kChunk], 1u)] = b | ((j % kChunk) << 16) | ((uint32_t)r << 21);
+        L[atomicAdd(&pos[j / kChunk], 1u)] = b | ((j % kChunk) << 16) | ((uint32_t)r << kRowShift);
       }
     __syncthreads();
   }
@@ -285,23 +287,29 @@ __global__ void __launch_bounds__(kWarps * 32, 1) km_tc_filter_kernel(const __gr
       const uint32_t* of = P.offs + (size_t)tp * (nch + 1);
       // chunk c's first kPF entries of this thread, loaded two chunks ahead into one of three
       // register sets (fixed roles: a register move would wait for its load)
-      uint32_t e0[kPF], e1[kPF], e2[kPF];
-      auto fetch = [&](int c, uint32_t (&e)[kPF]) {
-        const uint32_t o0 = c < nch ? __ldg(of + c) : 0u, o1 = c < nch ? __ldg(of + c + 1) : 0u;
+      struct Set {
+        uint32_t e[kPF];
+        uint32_t o0, o1;  // the chunk's list range
+      };
+      Set e0, e1, e2;
+      auto fetch = [&](int c, Set& f) {
+        f.o0 = c < nch ? __ldg(of + c) : 0u;
+        f.o1 = c < nch ? __ldg(of + c + 1) : 0u;
 #pragma unroll
         for (int u = 0; u < kPF; ++u) {
-          const uint32_t q = o0 + (uint32_t)(ft + u * kPts);
-          e[u] = q < o1 ? __ldg(L + q) : 0xFFFFFFFFu;
+          const uint32_t q = f.o0 + (uint32_t)(ft + u * kPts);
+          f.e[u] = q < f.o1 ? __ldg(L + q) : 0xFFFFFFFFu;
         }
       };
       auto put = [&](uint32_t sa, uint32_t w) {  // returns the entry's offset inside the stage
-        const uint32_t r = w >> 21, x = (w >> 16) & 31u;
+        const uint32_t r = w >> kRowShift, x = (w >> 16) & (kChunk - 1u);
         const uint32_t a0 = (r >> 7) * kTileA + ((r & 127u) >> 3) * kSBO + (r & 7u) * 16u + (x >> 3) * 128u + (x & 7u) * 2u;
         asm volatile("st.shared.u16 [%0], %1;" ::"r"(sa + a0), "h"((uint16_t)(w & 0xFFFFu)) : "memory");
         asm volatile("st.shared.u16 [%0], %1;" ::"r"(sa + a0 + 128u * (kChunk / 8)), "h"((uint16_t)0x3F80u) : "memory");
         return a0;
       };
-      auto body = [&](int c, const uint32_t (&e)[kPF], uint32_t (&f)[kPF]) {
+      auto body = [&](int c, const Set& cur, Set& f) {
+        const uint32_t(&e)[kPF] = cur.e;
         fetch(c + 2, f);
         const int s = (int)(gc % kNst);
         mbar_wait(empty_bar(s), (uint32_t)(((gc / kNst) & 1) ^ 1));
@@ -325,8 +333,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) km_tc_filter_kernel(const __gr
         asm volatile("bar.sync 1, %0;" ::"n"(kPts) : "memory");
 #pragma unroll
         for (int u = 0; u < kPF; ++u) prev_off[s][u][ft] = e[u] != 0xFFFFFFFFu ? put(sa, e[u]) : 0xFFFFFFFFu;
-        const uint32_t o1 = __ldg(of + c + 1);
-        for (uint32_t q = __ldg(of + c) + (uint32_t)(ft + kPF * kPts); q < o1; q += kPts) {
+        for (uint32_t q = cur.o0 + (uint32_t)(ft + kPF * kPts); q < cur.o1; q += kPts) {
           put(sa, __ldg(L + q));
           dirty[s] = (int)gc;
         }
