@@ -242,6 +242,31 @@ def profiled_traffic(workload, n, stage):
     return None
 
 
+def kmeans_secondary(wl, dev, torch, skc, hbm_peak, runs=2):
+    """The Lloyd loop of a K-means config (sketch HBM-resident, seeded initial points), device-timed."""
+    c = WORKLOADS[wl]
+    X = gen_rows(wl, c["n"], 0, dev, torch)
+    spec = skc.PreconditionSpec.create("hadamard", c["p"], sign_seed=derive_seed(SEED, 0xD5))
+    plan = skc.SamplingPlan(derive_seed(SEED, 0x5A), spec.p_pad, c["m"])
+    sk = skc.sketch_stream(skc.RowSource(X), spec, plan, compute="f64")
+    del X
+    torch.cuda.empty_cache()
+    ops = skc.SketchKMeans(sk)
+    mu0 = ops.init_centers(np.random.default_rng(SEED).choice(c["n"], c["K"], replace=False))
+    ops.lloyd(mu0, c["iters"])  # warm-up: builds the transposed sketch and the tensor-core entries
+    its, el = 0, 0.0
+    for _ in range(runs):
+        _, _, _, it_done, secs = ops.lloyd(mu0, c["iters"])
+        its += it_done
+        el += secs
+    rate = c["n"] * its / el
+    gbs = (8 * c["m"] + 4) * rate / 1e9  # algorithmic bytes per point-iteration: the sketch row + a label
+    return {"metric": "K-means point-iters/s", "value": rate, "iterations_per_run": its / runs,
+            "ms_per_run": el * 1e3 / runs, "desc": c["desc"],
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak},
+            "note": "Lloyd loop on the HBM-resident f64 sketch, exact reference arithmetic (bit-identical labels)"}
+
+
 def metric_name(cfg):
     if cfg["kind"] == "cov":
         return "samples/s precondition+sparsify+covariance"
@@ -264,6 +289,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-kmeans", action="store_true")
     ap.add_argument("--no-philox", action="store_true", help="skip the Philox-sampler secondary measurement")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 K-means secondary measurement")
     args = ap.parse_args()
     cfg = dict(WORKLOADS[args.workload])
     if args.n:
@@ -530,14 +556,12 @@ def main():
         mu0 = ops.init_centers(np.random.default_rng(SEED).choice(c2["n"], c2["K"], replace=False))
         ops.lloyd(mu0, c2["iters"])
         torch.cuda.synchronize()
-        ts = time.perf_counter()
         reps = 5
-        its = 0
-        for _ in range(reps):
-            _, _, _, it_done, _ = ops.lloyd(mu0, c2["iters"])
+        its, el = 0, 0.0
+        for _ in range(reps):  # device time of each run (CUDA events inside the Lloyd loop)
+            _, _, _, it_done, secs = ops.lloyd(mu0, c2["iters"])
             its += it_done
-        torch.cuda.synchronize()
-        el = time.perf_counter() - ts
+            el += secs
         out["kmeans_c2"] = {"metric": "K-means point-iters/s", "value": c2["n"] * its / el,
                             "iterations_per_run": its / reps, "ms_per_run": el * 1e3 / reps,
                             "note": "Lloyd loop on the HBM-resident f64 sketch, exact reference arithmetic"}
@@ -546,7 +570,10 @@ def main():
             r, el2 = cpu_kmeans_rate(rows2, c2, os.cpu_count() or 1, min_seconds=5.0)
             out["kmeans_c2"]["cpu_baseline"] = {"value": r, "unit": "point-iters/s", "cores": os.cpu_count(),
                                                 "kind": "port", "sample": "65536 C2 rows"}
-        del X2
+        del X2, sk2, ops
+        torch.cuda.empty_cache()
+        if not args.no_c5:
+            out["kmeans_c5"] = kmeans_secondary("c5", dev, torch, skc, hbm_peak)
 
     if rank == 0 and world == 1 and not args.no_cpu:
         sample_rows = 1 << 16

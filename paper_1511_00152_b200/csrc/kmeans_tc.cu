@@ -734,6 +734,9 @@ int kmtc_assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t
     const double eps = 1.001 * 0x1p-8 + (2.0 * m + 2.0 * p_pad / 16.0 + 64.0) * 0x1p-22 + (2.0 * m + 1.0) * 0x1p-53 +
                        0x1p-20;
     H.eps = (float)(1.1 * eps / (1.0 - 2.0 * eps));
+#ifdef SKC_KT_EPS_SCALE  // experiment only (unsafe): how the candidate count depends on the bound
+    H.eps *= (float)SKC_KT_EPS_SCALE;
+#endif
     H.cand = cand;
     H.ncand = ncand;
     H.list = list;

@@ -31,7 +31,9 @@ orig = cluster.SketchKMeans.assign
 
 def assign(self, mu, prev, labels, d2min, out, d2max):
     orig(self, mu, prev, labels, d2min, out, d2max)
-    ws = self._ws[("assign_tc", mu.shape[1])]
+    ws = self._ws.get(("assign_tc", mu.shape[1]))
+    if ws is None or prev is None:
+        return
     nc = ws[off_ncand:off_ncand + self.n].cpu().numpy()
     h = np.bincount(np.where(nc == 255, 9, nc), minlength=10)
     print("ncand histogram (0..8, overflow):", h.tolist(), flush=True)
