@@ -1067,13 +1067,142 @@ __global__ void __launch_bounds__(kWalkWarps * 32) km_walk_kernel(const int64_t*
   }
 }
 
+// Tile path (default for K <= 256): a CTA per coordinate list, kTileE entries at a time. The tile's
+// values and labels are staged in shared memory; a stable counting sort by label (per-warp
+// counts over contiguous sub-ranges, a scan over (label, warp), match_any ranks inside each
+// 32-entry step) makes every label's entries contiguous in point order; then thread k adds
+// label k's run to its running fp64 sum, so each (j, k) chain is still the sequential sum in
+// ascending point index. Loads are coalesced and the sort runs in shared memory, so the pass
+// streams the transposed sketch instead of chasing one warp's latency chain per list.
+constexpr int kTileE = 4096;
+constexpr int kTileWarps = 8;
+constexpr int kTileThreads = kTileWarps * 32;
+constexpr int kTileMaxK = 256;
+static size_t tile_smem(int K) {
+  return (size_t)kTileE * 8 * 2 + (size_t)kTileE + (size_t)kTileWarps * K * 4 + (size_t)(K + 1) * 4 * 2 + 64;
+}
+template <typename V>
+__global__ void __launch_bounds__(kTileThreads, 2) km_tile_walk_kernel(
+    const int64_t* __restrict__ off, int64_t R, const int32_t* __restrict__ rows, const V* __restrict__ vals,
+    const int32_t* __restrict__ labels, int32_t p_pad, int K, double* __restrict__ sums, int64_t* __restrict__ counts) {
+  extern __shared__ __align__(16) unsigned char tsm[];
+  double* tv = reinterpret_cast<double*>(tsm);  // tile values, list order
+  double* ts = tv + kTileE;                     // tile values, sorted by label (stable)
+  uint8_t* tl = reinterpret_cast<uint8_t*>(ts + kTileE);
+  int* wc = reinterpret_cast<int*>(tl + kTileE);  // [warp][K]: counts, then placement cursors
+  int* lb = wc + kTileWarps * K;                  // [K + 1]: label run starts
+  int* lt = lb + K + 1;                           // [K]: label run lengths
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t j = blockIdx.x;
+  const int64_t a = off[j * R], b = off[(j + 1) * R];
+  const uint32_t ltm = lanemask_lt();
+  double acc[(kTileMaxK + kTileThreads - 1) / kTileThreads] = {0.0};
+  int64_t cntk[(kTileMaxK + kTileThreads - 1) / kTileThreads] = {0};
+  for (int64_t t0 = a; t0 < b; t0 += kTileE) {
+    const int L = (int)min((int64_t)kTileE, b - t0);
+    for (int q = tid; q < kTileWarps * K; q += kTileThreads) wc[q] = 0;
+    // stage: values and gathered labels (all loads of a thread in flight together)
+#pragma unroll 4
+    for (int e = tid; e < L; e += kTileThreads) {
+      tv[e] = (double)__ldg(vals + t0 + e);
+      tl[e] = (uint8_t)__ldg(labels + __ldg(rows + t0 + e));
+    }
+    __syncthreads();
+    // per-warp label counts over the warp's contiguous sub-range
+    const int s0 = (int)((int64_t)L * warp / kTileWarps), s1 = (int)((int64_t)L * (warp + 1) / kTileWarps);
+    for (int e = s0 + lane; e < s1; e += 32) atomicAdd(&wc[warp * K + tl[e]], 1);
+    __syncthreads();
+    // run lengths per label and the exclusive scan over labels (warp 0)
+    for (int k = tid; k < K; k += kTileThreads) {
+      int t = 0;
+      for (int w = 0; w < kTileWarps; ++w) t += wc[w * K + k];
+      lt[k] = t;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int run = 0;
+      for (int k0 = 0; k0 < K; k0 += 32) {
+        const int k = k0 + lane;
+        const int c = k < K ? lt[k] : 0;
+        int x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(kFM, x, o);
+          if (lane >= o) x += y;
+        }
+        if (k < K) lb[k] = run + x - c;
+        run += __shfl_sync(kFM, x, 31);
+      }
+      if (lane == 0) lb[K] = run;
+    }
+    __syncthreads();
+    // cursors: label k's entries of warp w start after those of warps < w
+    for (int k = tid; k < K; k += kTileThreads) {
+      int pos = lb[k];
+      for (int w = 0; w < kTileWarps; ++w) {
+        const int c = wc[w * K + k];
+        wc[w * K + k] = pos;
+        pos += c;
+      }
+    }
+    __syncthreads();
+    // stable placement: warp sub-ranges in order, lanes in order inside each 32-entry step
+    for (int e0 = s0; e0 < s1; e0 += 32) {
+      const int e = e0 + lane;
+      const int k = e < s1 ? (int)tl[e] : -1;
+      const uint32_t peers = __match_any_sync(kFM, k);
+      if (k >= 0) ts[wc[warp * K + k] + __popc(peers & ltm)] = tv[e];
+      __syncwarp();
+      if (k >= 0 && (peers & ltm) == 0) wc[warp * K + k] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    // chains: thread k adds label k's run in order (loads ahead of the dependent adds)
+#pragma unroll
+    for (int u = 0; u < (kTileMaxK + kTileThreads - 1) / kTileThreads; ++u) {
+      const int k = tid + u * kTileThreads;
+      if (k < K) {
+        const int r0 = lb[k], r1 = r0 + lt[k];
+        double x = acc[u];
+        int e = r0;
+        for (; e + 8 <= r1; e += 8) {
+          double w[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) w[q] = ts[e + q];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) x = dadd(x, w[q]);
+        }
+        for (; e < r1; ++e) x = dadd(x, ts[e]);
+        acc[u] = x;
+        cntk[u] += r1 - r0;
+      }
+    }
+    __syncthreads();  // the next tile overwrites the staging
+  }
+#pragma unroll
+  for (int u = 0; u < (kTileMaxK + kTileThreads - 1) / kTileThreads; ++u) {
+    const int k = tid + u * kTileThreads;
+    if (k < K) {
+      sums[j * K + k] = acc[u];
+      counts[j * K + k] = cntk[u];
+    }
+  }
+}
+
 static size_t walk_smem(int K) { return (size_t)kWalkWarps * K * 12; }
 // The walk has one warp per coordinate list: it needs enough lists to fill the GPU (C5, p = 2048:
 // 8.7 vs 24 ms per iteration); with few lists the segment path's thousands of segments win
 // (C2, p = 512: 2.17 vs 2.44 ms per 6-iteration run).
+// Path choice (measured): long lists (p_pad >= 1024: C5's 2048 lists of ~500K entries) take the walk
+// (8.7 ms per C5 iteration; tile 12.5, segments 24); short ones (C2: 512 lists of ~10K) the
+// tile path (1.94 ms per C2 run; segments 2.14, walk 2.40); K > 256 the segment path.
 static bool use_walk(int32_t p_pad, int K) {
-  if (const char* e = getenv("SKC_PARTIALS")) return e[0] != 's';  // A/B: SKC_PARTIALS=seg|walk
-  return walk_smem(K) <= 96 * 1024 && p_pad >= 1024;
+  if (const char* e = getenv("SKC_PARTIALS")) return e[0] == 'w';  // A/B: SKC_PARTIALS=seg|walk|tile
+  return p_pad >= 1024 && walk_smem(K) <= 96 * 1024;
+}
+static bool use_tile(int32_t p_pad, int K) {
+  if (const char* e = getenv("SKC_PARTIALS")) return e[0] == 't' && K <= kTileMaxK;
+  return !use_walk(p_pad, K) && K <= kTileMaxK;
 }
 
 // cluster sizes: bincount(labels), exact
@@ -1147,7 +1276,7 @@ static int sizes_launch(const int32_t* labels, int64_t n, int32_t K, int64_t* si
 }
 
 size_t seg_ws(int64_t n, int32_t m, int32_t p_pad, int32_t K, int val_f64) {
-  if (use_walk(p_pad, K)) return 256;  // the walk path needs no per-iteration scratch
+  if (use_walk(p_pad, K) || use_tile(p_pad, K)) return 256;  // the walk and tile paths need no per-iteration scratch
   return seg_layout(n, m, p_pad, K, val_f64).total;
 }
 
@@ -1160,6 +1289,20 @@ int csc_partials_launch(const void* ws, int val_f64, int64_t n, int32_t m, int32
   const int64_t* off = reinterpret_cast<const int64_t*>(w + L.off_off);
   const int32_t* rows = reinterpret_cast<const int32_t*>(w + L.off_rows);
   int rc;
+  if (use_tile(p_pad, K)) {
+    const size_t tsm = tile_smem(K);
+    if (val_f64) {
+      cudaFuncSetAttribute(km_tile_walk_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+      km_tile_walk_kernel<double><<<(unsigned)p_pad, kTileThreads, tsm, st>>>(
+          off, L.R, rows, reinterpret_cast<const double*>(w + L.off_vals), labels, p_pad, K, sums, counts);
+    } else {
+      cudaFuncSetAttribute(km_tile_walk_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+      km_tile_walk_kernel<float><<<(unsigned)p_pad, kTileThreads, tsm, st>>>(
+          off, L.R, rows, reinterpret_cast<const float*>(w + L.off_vals), labels, p_pad, K, sums, counts);
+    }
+    if ((rc = check_launch("km_tile_walk_kernel"))) return rc;
+    return sizes_launch(labels, n, K, sizes, st);
+  }
   if (use_walk(p_pad, K)) {
     const unsigned wgrid = (unsigned)((p_pad + kWalkWarps - 1) / kWalkWarps);
     const size_t wsm = walk_smem(K);

@@ -121,9 +121,10 @@ def test_tc_filter_equals_exact(skc, monkeypatch, p, m, K, n, spread, compute, i
     assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3]), "changed / farthest point"
 
 
-@pytest.mark.parametrize("p,m,K,n", [(2048, 102, 100, 30000), (1024, 51, 7, 20001), (512, 26, 10, 9000)])
-def test_partials_walk_equals_segments(skc, monkeypatch, p, m, K, n):
-    """K6's two exact paths (warp-per-coordinate walk, segmented label sort) give identical sums."""
+@pytest.mark.parametrize("p,m,K,n", [(2048, 102, 100, 30000), (1024, 51, 7, 20001), (512, 26, 10, 90000),
+                                     (256, 25, 256, 50000)])
+def test_partials_paths_agree(skc, monkeypatch, p, m, K, n):
+    """K6's exact paths (tiled counting sort, warp-per-coordinate walk, segmented label sort) agree bit for bit."""
     rng = np.random.default_rng(p * 7 + K)
     X = (rng.standard_normal((p, K))[:, rng.integers(0, K, n)] * 2 + rng.standard_normal((p, n))).astype(np.float32)
     spec = skc.PreconditionSpec.create("hadamard", p, 5)
@@ -131,9 +132,10 @@ def test_partials_walk_equals_segments(skc, monkeypatch, p, m, K, n):
     ops = skc.SketchKMeans(sk)
     labels = torch.as_tensor(rng.integers(0, K, n).astype(np.int32), device=sk.indices.device)
     res = {}
-    for path in ("seg", "walk"):
+    for path in ("seg", "walk", "tile"):
         monkeypatch.setenv("SKC_PARTIALS", path)
         ops._ws.pop(("seg", K), None)
         res[path] = [t.cpu().numpy() for t in ops.partials(labels, K)]
-    for a, b in zip(res["seg"], res["walk"]):
-        assert np.array_equal(a, b)
+    for other in ("walk", "tile"):
+        for a, b in zip(res["seg"], res[other]):
+            assert np.array_equal(a, b), other
