@@ -183,8 +183,14 @@ int moments_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, 
 // into the same int64 partial. A reduce kernel sums the groups in int64 and scales to fp64.
 // tau = 8 * rms(values), from K2's statistics. Quantum 2^-S ~ 6e-8 * tau^2.
 // ======================================================================================
-constexpr int kSmemBudget = 220 * 1024;  // dynamic smem per CTA
-constexpr int kCovWarps = 32;
+#ifndef SKC_COV_SMEM_KB
+#define SKC_COV_SMEM_KB 220
+#endif
+#ifndef SKC_COV_WARPS
+#define SKC_COV_WARPS 32
+#endif
+constexpr int kSmemBudget = SKC_COV_SMEM_KB * 1024;  // dynamic smem per CTA
+constexpr int kCovWarps = SKC_COV_WARPS;
 constexpr int kMaxBands = 511;
 
 __host__ __device__ inline int64_t tri_off(int64_t a, int64_t p) { return a * p - a * (a - 1) / 2; }
