@@ -414,7 +414,9 @@ def main():
         sk = skc.sketch_stream(skc.RowSource(X), spec, plan, compute="f64", col0=col0)
         ops = skc.SketchKMeans(sk)
         chosen = np.random.default_rng(SEED).choice(n, K, replace=False)
-        mu0 = ops.init_centers(chosen)
+        mu0 = ops.init_centers(chosen)  # seeded points of rank 0's shard, the same centres on every rank
+        if world > 1:
+            tdist.broadcast(mu0, src=0)
         for _ in range(args.warmup):
             ops.lloyd(mu0, iters_max)
         barrier()
