@@ -520,6 +520,7 @@ __global__ void __launch_bounds__(kFiltWarps * 32, SKC_FILT_MINB)
     }
     float dl[NB][4], el[NB][4];
     float ub = __int_as_float(0x7F800000);
+    const bool wide = !(colsq >= 0x1p-90 && colsq <= 0x1p100);
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       float pf[4], qf[4];
@@ -548,7 +549,9 @@ __global__ void __launch_bounds__(kFiltWarps * 32, SKC_FILT_MINB)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int k = 128 * b + 4 * lane + c;
-        const bool cand = k < K && dl[b][c] - el[b][c] <= ub;
+        // outside the range the fp32 bound covers (colsq beyond [2^-90, 2^100], or a non-finite
+        // estimate), every centre stays a candidate and the exact pass decides
+        const bool cand = k < K && (wide || !isfinite(dl[b][c]) || !isfinite(el[b][c]) || dl[b][c] - el[b][c] <= ub);
         const unsigned mk = __ballot_sync(kFM, cand);
         if (cand) {
           const int q = qn + __popc(mk & ((1u << lane) - 1u));

@@ -419,7 +419,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) km_tc_filter_kernel(const __gr
         const float e8 = 8.f * cf;
         const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(b * 256 + t * 128);
         float ub = __int_as_float(0x7F800000);
-        bool bad = false;
+        // the bound needs colsq in [2^-90, 2^100] (no fp32 under/overflow of the terms that matter)
+        bool bad = !(cf >= 0x1p-90f && cf <= 0x1p100f);
 #pragma unroll 1
         for (int cb = 0; cb < nb16; ++cb) {
           float f[16];

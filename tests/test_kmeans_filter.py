@@ -139,3 +139,25 @@ def test_partials_paths_agree(skc, monkeypatch, p, m, K, n):
     for other in ("walk", "tile"):
         for a, b in zip(res["seg"], res[other]):
             assert np.array_equal(a, b), other
+
+
+@pytest.mark.parametrize("scale", [1e-30, 1e-12, 1.0, 1e25])
+def test_filters_at_extreme_scales(skc, monkeypatch, scale):
+    """Both filters stay exact when the data sit far from unit scale (the fp32 / bf16 bounds hold
+    only for colsq in [2^-90, 2^100]; outside it every centre is verified) and for all-zero points."""
+    p, m, K, n = 1024, 51, 40, 6000
+    rng = np.random.default_rng(11)
+    C = rng.standard_normal((p, K)) * 3.0
+    X = (C[:, rng.integers(0, K, n)] + rng.standard_normal((p, n))) * scale
+    X[:, ::97] = 0.0  # some all-zero points (colsq = 0)
+    X = X.astype(np.float32)
+    spec = skc.PreconditionSpec.create("hadamard", p, 3)
+    sk = skc.sketch_stream(X, spec, skc.SamplingPlan(4, spec.p_pad, m), compute="f64")
+    dev = sk.indices.device
+    mu = torch.as_tensor(rng.standard_normal((spec.p_pad, K)) * 2.7 * scale, device=dev)
+    prev = torch.as_tensor(rng.integers(0, K, n).astype(np.int32), device=dev)
+    a = _assign(skc, sk, mu, prev, True, monkeypatch)
+    for b in (_assign(skc, sk, mu, prev, False, monkeypatch), _assign_tc(skc, sk, mu, prev)):
+        assert np.array_equal(a[0], b[0]), "labels"
+        assert np.array_equal(a[1], b[1]), "d2min"
+        assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3]), "changed / farthest point"
