@@ -51,14 +51,19 @@ __device__ double pw_rec(const double* a, int64_t n) {
 
 constexpr int kPwDeep = 14;  // subtrees at depth 14: one thread each, 64 blocks
 
+// res[t]: the sum of path t's subtree; ld[t]: the depth at which path t reaches a leaf (<= 128
+// elements), kPwDeep if it does not. Node t of depth d (stored at t << (kPwDeep - d)) is an internal
+// node of numpy's tree exactly when ld[t << (kPwDeep - d)] > d.
 __global__ void __launch_bounds__(256) pairwise_leaves_kernel(const double* __restrict__ x, int64_t n,
-                                                              double* __restrict__ res) {
+                                                              double* __restrict__ res, uint8_t* __restrict__ ld) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;  // path of depth kPwDeep
   int64_t off = 0, len = n;
   bool active = true;
+  int leafd = kPwDeep;
   for (int d = 0; d < kPwDeep; ++d) {
     const int bit = (t >> (kPwDeep - 1 - d)) & 1;
     if (len <= 128) {  // leaf above the split depth: owned by the all-zero suffix path
+      if (leafd == kPwDeep) leafd = d;
       if (bit) active = false;
       continue;
     }
@@ -72,42 +77,39 @@ __global__ void __launch_bounds__(256) pairwise_leaves_kernel(const double* __re
     }
   }
   res[t] = active ? pw_rec(x + off, len) : 0.0;
+  ld[t] = (uint8_t)leafd;
 }
 
-__global__ void __launch_bounds__(1024) pairwise_combine_kernel(double* __restrict__ res, int64_t n,
+// The 2^kPwDeep subtree sums are combined in shared memory (128 KB), level by level; whether a
+// node is internal comes from ld (one lookup instead of re-walking its path).
+__global__ void __launch_bounds__(1024) pairwise_combine_kernel(const double* __restrict__ gres,
+                                                                const uint8_t* __restrict__ gld, int64_t n,
                                                                 double* __restrict__ out) {
+  extern __shared__ double res[];
+  uint8_t* ld = reinterpret_cast<uint8_t*>(res + (1 << kPwDeep));
+  for (int t = threadIdx.x; t < (1 << kPwDeep); t += blockDim.x) res[t] = gres[t], ld[t] = gld[t];
+  __syncthreads();
   for (int d = kPwDeep - 1; d >= 0; --d) {
-    for (int t = threadIdx.x; t < (1 << d); t += blockDim.x) {
-      bool leaf_above;
-      int64_t L = n;
-      leaf_above = false;
-      for (int k = 0; k < d; ++k) {
-        if (L <= 128) {
-          leaf_above = true;
-          break;
-        }
-        int64_t n2 = L / 2;
-        n2 -= n2 % 8;
-        L = ((t >> (d - 1 - k)) & 1) ? L - n2 : n2;
-      }
-      if (!leaf_above && L > 128) {
-        const int sh = kPwDeep - d;
-        res[(size_t)t << sh] = dadd(res[(size_t)(2 * t) << (sh - 1)], res[(size_t)(2 * t + 1) << (sh - 1)]);
-      }
-    }
+    const int sh = kPwDeep - d;
+    for (int t = threadIdx.x; t < (1 << d); t += blockDim.x)
+      if (ld[t << sh] > d) res[t << sh] = dadd(res[(2 * t) << (sh - 1)], res[(2 * t + 1) << (sh - 1)]);
     __syncthreads();
   }
   if (threadIdx.x == 0) out[0] = res[0];
+  (void)n;
 }
 
-size_t pairwise_ws() { return ((size_t)1 << kPwDeep) * sizeof(double); }
+size_t pairwise_ws() { return ((size_t)1 << kPwDeep) * (sizeof(double) + 1); }
 
 int pairwise_launch(const double* x, int64_t n, double* out, void* ws, cudaStream_t st) {
   double* res = reinterpret_cast<double*>(ws);
-  pairwise_leaves_kernel<<<(1 << kPwDeep) / 256, 256, 0, st>>>(x, n, res);
+  uint8_t* ld = reinterpret_cast<uint8_t*>(res + (1 << kPwDeep));
+  pairwise_leaves_kernel<<<(1 << kPwDeep) / 256, 256, 0, st>>>(x, n, res, ld);
   int rc = check_launch("pairwise_leaves_kernel");
   if (rc) return rc;
-  pairwise_combine_kernel<<<1, 1024, 0, st>>>(res, n, out);
+  const size_t smem = ((size_t)1 << kPwDeep) * (sizeof(double) + 1);
+  cudaFuncSetAttribute(pairwise_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  pairwise_combine_kernel<<<1, 1024, smem, st>>>(res, ld, n, out);
   return check_launch("pairwise_combine_kernel");
 }
 

@@ -418,3 +418,17 @@ def test_stream_moments_native_equals_python_loop(skc, sampler, kind):
     b = skc.stream_moments(skc.RowSource(torch.from_numpy(X), chunk_cols=3000), spec, plan, compute="f32")
     assert a.n == b.n == n
     assert torch.equal(a.acc, b.acc) and torch.equal(a.stats, b.stats) and torch.equal(a.tri, b.tri)
+
+
+@pytest.mark.parametrize("n", [1, 7, 8, 127, 128, 129, 1000, 4097, 200000, 3000001, 10000000])
+def test_pairwise_sum_bit_exact(skc, n):
+    """skc_pairwise_sum reproduces numpy's pairwise float64 sum (ndarray.sum) bit for bit."""
+    from paper_1511_00152_b200 import _lib
+
+    L = _lib.lib()
+    x = np.random.default_rng(n).standard_normal(n) * 10.0 ** np.random.default_rng(n + 1).integers(-3, 4, n)
+    xd = torch.as_tensor(x, device="cuda")
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ws = _lib.workspace(L.skc_pairwise_sum_workspace(n), xd.device)
+    _lib.call("skc_pairwise_sum", xd.data_ptr(), n, out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(xd.device))
+    assert float(out.item()) == float(x.sum())
