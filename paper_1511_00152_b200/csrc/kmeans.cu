@@ -1079,7 +1079,13 @@ __global__ void __launch_bounds__(kWalkWarps * 32) km_walk_kernel(const int64_t*
 // label k's run to its running fp64 sum, so each (j, k) chain is still the sequential sum in
 // ascending point index. Loads are coalesced and the sort runs in shared memory, so the pass
 // streams the transposed sketch instead of chasing one warp's latency chain per list.
-constexpr int kTileE = 4096;
+#ifndef SKC_TILE_E
+#define SKC_TILE_E 2048
+#endif
+#ifndef SKC_TILE_MINB
+#define SKC_TILE_MINB 4
+#endif
+constexpr int kTileE = SKC_TILE_E;
 constexpr int kTileWarps = 8;
 constexpr int kTileThreads = kTileWarps * 32;
 constexpr int kTileMaxK = 256;
@@ -1087,7 +1093,7 @@ static size_t tile_smem(int K) {
   return (size_t)kTileE * 8 * 2 + (size_t)kTileE + (size_t)kTileWarps * K * 4 + (size_t)(K + 1) * 4 * 2 + 64;
 }
 template <typename V>
-__global__ void __launch_bounds__(kTileThreads, 2) km_tile_walk_kernel(
+__global__ void __launch_bounds__(kTileThreads, SKC_TILE_MINB) km_tile_walk_kernel(
     const int64_t* __restrict__ off, int64_t R, const int32_t* __restrict__ rows, const V* __restrict__ vals,
     const int32_t* __restrict__ labels, int32_t p_pad, int K, double* __restrict__ sums, int64_t* __restrict__ counts) {
   extern __shared__ __align__(16) unsigned char tsm[];
