@@ -655,9 +655,16 @@ int kmtc_prepare_launch(const int32_t* idx, const void* val, int val_f64, int64_
   return check_launch("km_tc_bucket_kernel");
 }
 
+// one resident wave of the grid-stride verify blocks (each loops over tile pairs): a second,
+// partial wave would leave most SMs idle while it finishes
 static int verify_grid(int64_t n) {
+  static int occ = 0;
+  if (occ == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, km_tc_verify_kernel, kVerifyThreads, 0);
+    if (occ < 1) occ = 1;
+  }
   int64_t g = kt_ntp(n);
-  const int64_t cap = 8 * (int64_t)sm_count();
+  const int64_t cap = (int64_t)occ * sm_count();
   if (g > cap) g = cap;
   return (int)(g < 1 ? 1 : g);
 }
