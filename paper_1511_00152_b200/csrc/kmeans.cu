@@ -987,7 +987,7 @@ __global__ void km_chain_sum_kernel(const int64_t* __restrict__ pos0, const V* _
 // sequential fp64 sum in ascending point index: no scatter, no scan, no sorted copy.
 constexpr int kWalkWarps = 4;
 #ifndef SKC_WALK_AHEAD
-#define SKC_WALK_AHEAD 8
+#define SKC_WALK_AHEAD 4
 #endif
 constexpr int kWalkAhead = SKC_WALK_AHEAD;  // steps of 32 entries per group; groups are software-pipelined
 template <typename V>
@@ -1008,46 +1008,43 @@ __global__ void __launch_bounds__(kWalkWarps * 32) km_walk_kernel(const int64_t*
   const int64_t a = off[j * R], b = off[(j + 1) * R];
   const uint32_t lt = lanemask_lt();
   constexpr int G = 32 * kWalkAhead;
-  // three groups in flight: rows/values of group g+2 load, labels of group g+1 gather, group g adds
-  int r1[kWalkAhead], r2[kWalkAhead], k1[kWalkAhead];
-  V v0[kWalkAhead], v1[kWalkAhead], v2[kWalkAhead];
-  int k0[kWalkAhead];
-  auto load_rv = [&](int64_t base, int (&rr)[kWalkAhead], V (&vv)[kWalkAhead]) {
+  // three groups in flight: rows/values of group g+2 load, labels of group g+1 gather, group g adds.
+  // The three register sets keep fixed roles per unrolled step: rotating them with register moves
+  // would make each move wait for its load and collapse the pipeline.
+  struct Set {
+    int r[kWalkAhead], k[kWalkAhead];
+    V v[kWalkAhead];
+  };
+  auto load_rv = [&](int64_t base, Set& S) {
 #pragma unroll
     for (int s = 0; s < kWalkAhead; ++s) {
       const int64_t e = base + 32 * s + lane;
-      rr[s] = e < b ? __ldg(rows + e) : -1;
-      vv[s] = e < b ? __ldg(vals + e) : V(0);
+      S.r[s] = e < b ? __ldg(rows + e) : -1;
+      S.v[s] = e < b ? __ldg(vals + e) : V(0);
     }
   };
-  auto gather = [&](const int (&rr)[kWalkAhead], int (&kk)[kWalkAhead]) {
+  auto gather = [&](Set& S) {
 #pragma unroll
-    for (int s = 0; s < kWalkAhead; ++s) kk[s] = rr[s] >= 0 ? __ldg(labels + rr[s]) : -1;
+    for (int s = 0; s < kWalkAhead; ++s) S.k[s] = S.r[s] >= 0 ? __ldg(labels + S.r[s]) : -1;
   };
-  int r0[kWalkAhead];
-  load_rv(a, r0, v0);
-  load_rv(a + G, r1, v1);
-  gather(r0, k0);
-  for (int64_t base = a; base < b; base += G) {
-    gather(r1, k1);                 // labels of group g+1
-    load_rv(base + 2 * G, r2, v2);  // rows and values of group g+2
+  auto process = [&](const Set& S) {
     // the group's label matches are independent of the sums: all in flight before the adds
     uint32_t peers[kWalkAhead];
     int last[kWalkAhead];
 #pragma unroll
-    for (int s = 0; s < kWalkAhead; ++s) peers[s] = __match_any_sync(kFM, k0[s]);
+    for (int s = 0; s < kWalkAhead; ++s) peers[s] = __match_any_sync(kFM, S.k[s]);
 #pragma unroll
-    for (int s = 0; s < kWalkAhead; ++s) last[s] = __reduce_max_sync(kFM, k0[s] >= 0 ? __popc(peers[s]) : 0);
+    for (int s = 0; s < kWalkAhead; ++s) last[s] = __reduce_max_sync(kFM, S.k[s] >= 0 ? __popc(peers[s]) : 0);
 #pragma unroll
     for (int s = 0; s < kWalkAhead; ++s) {
       // the leader (lowest lane) of each label adds its peers' values in lane (= point) order
-      const int k = k0[s];
+      const int k = S.k[s];
       const bool lead = k >= 0 && (peers[s] & lt) == 0;
       double t = lead ? acc[k] : 0.0;
       uint32_t rem = peers[s];
       for (int q = 0; q < last[s]; ++q) {
         const int src = rem ? __ffs(rem) - 1 : lane;
-        const double vq = __shfl_sync(kFM, (double)v0[s], src);
+        const double vq = __shfl_sync(kFM, (double)S.v[s], src);
         if (lead && rem) t = dadd(t, vq);
         rem &= rem - 1;
       }
@@ -1057,13 +1054,20 @@ __global__ void __launch_bounds__(kWalkWarps * 32) km_walk_kernel(const int64_t*
       }
       __syncwarp();
     }
-#pragma unroll
-    for (int s = 0; s < kWalkAhead; ++s) {
-      k0[s] = k1[s];
-      v0[s] = v1[s];
-      r1[s] = r2[s];
-      v1[s] = v2[s];
-    }
+  };
+  auto step = [&](int64_t base, Set& X, Set& Y, Set& Z) {
+    gather(Y);                // labels of group g+1
+    load_rv(base + 2 * G, Z);  // rows and values of group g+2
+    process(X);               // group g
+  };
+  Set A, B, C;
+  load_rv(a, A);
+  load_rv(a + G, B);
+  gather(A);
+  for (int64_t base = a; base < b; base += 3 * G) {
+    step(base, A, B, C);
+    if (base + G < b) step(base + G, B, C, A);
+    if (base + 2 * G < b) step(base + 2 * G, C, A, B);
   }
   __syncwarp();
   for (int k = lane; k < K; k += 32) {
