@@ -118,11 +118,15 @@ int pairwise_launch(const double* x, int64_t n, double* out, void* ws, cudaStrea
 constexpr int kAsgWarps = 8;
 
 // packed per-(j,k) table: {-2 mu, mu*mu} (np.vstack([-2.0 * mu, mu * mu]), cluster.py:182)
-__global__ void km_tables2_kernel(const double* __restrict__ mu, int64_t total, double2* __restrict__ tab) {
+// as two planes, tx = -2 mu and ty = mu * mu, each [p][K]: a group's K lanes then read K
+// contiguous doubles per coordinate (half the L1 wavefronts of an interleaved {x, y} table)
+__global__ void km_tables2_kernel(const double* __restrict__ mu, int64_t total, double* __restrict__ tx,
+                                  double* __restrict__ ty) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= total) return;
   const double v = mu[e];
-  tab[e] = make_double2(dmul(-2.0, v), dmul(v, v));
+  tx[e] = dmul(-2.0, v);
+  ty[e] = dmul(v, v);
 }
 
 // A warp holds G = 32/KP points; lane = g*KP + k. For K > KP the lane loops over k += KP.
@@ -132,7 +136,8 @@ __global__ void km_tables2_kernel(const double* __restrict__ mu, int64_t total, 
 template <typename V, int KP, bool SMEM_TAB>
 __global__ void __launch_bounds__(kAsgWarps * 32, 4)
     km_assign_kernel(const int32_t* __restrict__ idx, const void* __restrict__ val, int64_t n, int m,
-                     const double2* __restrict__ gtab, int K, int p_pad, const int32_t* __restrict__ prev,
+                     const double* __restrict__ gtx, const double* __restrict__ gty, int K, int p_pad,
+                     const int32_t* __restrict__ prev,
                      int32_t* __restrict__ labels, double* __restrict__ d2min, int64_t* __restrict__ blk_changed,
                      double* __restrict__ blk_max, int64_t* __restrict__ blk_arg) {
   constexpr int G = 32 / KP;
@@ -141,11 +146,13 @@ __global__ void __launch_bounds__(kAsgWarps * 32, 4)
   const int g = lane / KP, k0 = lane % KP;
   // layout: [table (SMEM_TAB)] [per warp: sidx G*m int | sval G*m double | msq 32*m double]
   size_t off = 0;
-  const double2* tab = gtab;
+  const double* tabx = gtx;
+  const double* taby = gty;
   if constexpr (SMEM_TAB) {
-    double2* st = reinterpret_cast<double2*>(sm);
-    for (int e = threadIdx.x; e < p_pad * K; e += blockDim.x) st[e] = gtab[e];
-    tab = st;
+    double* st = reinterpret_cast<double*>(sm);
+    for (int e = threadIdx.x; e < p_pad * K; e += blockDim.x) st[e] = gtx[e], st[p_pad * K + e] = gty[e];
+    tabx = st;
+    taby = st + p_pad * K;
     off = (size_t)p_pad * K * 16;
     __syncthreads();
   }
@@ -209,27 +216,26 @@ __global__ void __launch_bounds__(kAsgWarps * 32, 4)
       double v = __longlong_as_double(0x7FF0000000000000LL);
       int kk = 0x7FFFFFFF;
       if (k < K && i < n) {
-        const double2* tk = tab + k;
         double acc = 0.0;
         int t = 0;
-        const double* tkx = reinterpret_cast<const double*>(tk);
+        const double* tkx = tabx + k;
+        const double* tky = taby + k;
         for (; t + 4 <= m; t += 4) {
-          const double a0 = tkx[2 * si[t]], a1 = tkx[2 * si[t + 1]], a2 = tkx[2 * si[t + 2]], a3 = tkx[2 * si[t + 3]];
+          const double a0 = tkx[si[t]], a1 = tkx[si[t + 1]], a2 = tkx[si[t + 2]], a3 = tkx[si[t + 3]];
           acc = dadd(acc, dmul(sv[t], a0));
           acc = dadd(acc, dmul(sv[t + 1], a1));
           acc = dadd(acc, dmul(sv[t + 2], a2));
           acc = dadd(acc, dmul(sv[t + 3], a3));
         }
-        for (; t < m; ++t) acc = dadd(acc, dmul(sv[t], tkx[2 * si[t]]));
+        for (; t < m; ++t) acc = dadd(acc, dmul(sv[t], tkx[si[t]]));
         for (t = 0; t + 4 <= m; t += 4) {
-          const double b0 = tkx[2 * si[t] + 1], b1 = tkx[2 * si[t + 1] + 1], b2 = tkx[2 * si[t + 2] + 1],
-                       b3 = tkx[2 * si[t + 3] + 1];
+          const double b0 = tky[si[t]], b1 = tky[si[t + 1]], b2 = tky[si[t + 2]], b3 = tky[si[t + 3]];
           acc = dadd(acc, b0);
           acc = dadd(acc, b1);
           acc = dadd(acc, b2);
           acc = dadd(acc, b3);
         }
-        for (; t < m; ++t) acc = dadd(acc, tkx[2 * si[t] + 1]);
+        for (; t < m; ++t) acc = dadd(acc, tky[si[t]]);
         v = dadd(acc, colsq);
         kk = k;
       }
@@ -393,7 +399,8 @@ constexpr int kFiltUnroll = SKC_FILT_UNROLL;
 template <typename V, int NB>  // NB = ceil(K4 / 128) blocks of 4 centres per lane
 __global__ void __launch_bounds__(kFiltWarps * 32, SKC_FILT_MINB)
     km_assign_filter_kernel(const int32_t* __restrict__ idx, const void* __restrict__ val, int64_t n, int m,
-                            const float* __restrict__ t32, int K4, const double2* __restrict__ tab, int K,
+                            const float* __restrict__ t32, int K4, const double* __restrict__ tabx,
+                            const double* __restrict__ taby, int K,
                             const int32_t* __restrict__ prev, int32_t* __restrict__ labels,
                             double* __restrict__ d2min, int64_t* __restrict__ blk_changed,
                             double* __restrict__ blk_max, int64_t* __restrict__ blk_arg,
@@ -426,10 +433,11 @@ __global__ void __launch_bounds__(kFiltWarps * 32, SKC_FILT_MINB)
         const int64_t i = pi[qp[q]];
         const int k = qk[q];
         const int32_t* ir = idx + i * m;
-        const double* tk = reinterpret_cast<const double*>(tab + k);
+        const double* tkx = tabx + k;
+        const double* tky = taby + k;
         double acc = 0.0;
-        for (int t = 0; t < m; ++t) acc = dadd(acc, dmul(ldd<V>(val, i * m + t), tk[2 * (size_t)__ldg(ir + t) * K]));
-        for (int t = 0; t < m; ++t) acc = dadd(acc, tk[2 * (size_t)__ldg(ir + t) * K + 1]);
+        for (int t = 0; t < m; ++t) acc = dadd(acc, dmul(ldd<V>(val, i * m + t), tkx[(size_t)__ldg(ir + t) * K]));
+        for (int t = 0; t < m; ++t) acc = dadd(acc, tky[(size_t)__ldg(ir + t) * K]);
         qd[q] = dadd(acc, qc[q]);
       }
     }
@@ -617,7 +625,8 @@ static bool use_filter(int32_t p_pad, int32_t K) {
 }
 
 template <typename V, int KP>
-static void launch_assign_kp(int G, const int32_t* idx, const void* val, int64_t n, int32_t m, const double2* tab,
+static void launch_assign_kp(int G, const int32_t* idx, const void* val, int64_t n, int32_t m, const double* tx,
+                             const double* ty,
                              int32_t K, int32_t p_pad, const int32_t* prev, int32_t* labels, double* d2min,
                              int64_t* bch, double* bmx, int64_t* barg, cudaStream_t st) {
   constexpr int GP = 32 / KP;
@@ -629,25 +638,26 @@ static void launch_assign_kp(int G, const int32_t* idx, const void* val, int64_t
     auto k = km_assign_kernel<V, KP, true>;
     const size_t smem = tab_bytes + per_warp * warps;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<G, warps * 32, smem, st>>>(idx, val, n, m, tab, K, p_pad, prev, labels, d2min, bch, bmx, barg);
+    k<<<G, warps * 32, smem, st>>>(idx, val, n, m, tx, ty, K, p_pad, prev, labels, d2min, bch, bmx, barg);
   } else {
     auto k = km_assign_kernel<V, KP, false>;
     const size_t smem = per_warp * warps;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<G, warps * 32, smem, st>>>(idx, val, n, m, tab, K, p_pad, prev, labels, d2min, bch, bmx, barg);
+    k<<<G, warps * 32, smem, st>>>(idx, val, n, m, tx, ty, K, p_pad, prev, labels, d2min, bch, bmx, barg);
   }
 }
 
 int assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, const double* mu,
                   int32_t p_pad, int32_t K, const int32_t* prev, int32_t* labels, double* d2min, int64_t* out,
                   double* d2max, void* ws, cudaStream_t st) {
-  double2* tab = reinterpret_cast<double2*>(ws);
+  double* tx = reinterpret_cast<double*>(ws);  // [-2 mu] plane, then the [mu * mu] plane
+  double* ty = tx + (size_t)p_pad * K;
   const int G = assign_grid(n);
-  int64_t* bch = reinterpret_cast<int64_t*>(tab + (size_t)p_pad * K);
+  int64_t* bch = reinterpret_cast<int64_t*>(ty + (size_t)p_pad * K);
   double* bmx = reinterpret_cast<double*>(bch + G);
   int64_t* barg = reinterpret_cast<int64_t*>(bmx + G);
   const int64_t total = (int64_t)p_pad * K;
-  km_tables2_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(mu, total, tab);
+  km_tables2_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(mu, total, tx, ty);
   int rc = check_launch("km_tables2_kernel");
   if (rc) return rc;
   if (n > 0 && use_filter(p_pad, K)) {
@@ -661,7 +671,7 @@ int assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, i
     const int nb = (K4 + 127) / 128;
     auto go = [&](auto kern) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kern<<<Gf, kFiltWarps * 32, smem, st>>>(idx, val, n, m, t32, K4, tab, K, prev, labels, d2min, bch, bmx, barg,
+      kern<<<Gf, kFiltWarps * 32, smem, st>>>(idx, val, n, m, t32, K4, tx, ty, K, prev, labels, d2min, bch, bmx, barg,
                                                nullptr, nullptr);
     };
     if (val_f64) {
@@ -681,13 +691,13 @@ int assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, i
   }
   if (n > 0) {
     if (val_f64) {
-      if (K <= 8) launch_assign_kp<double, 8>(G, idx, val, n, m, tab, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);
-      else if (K <= 16) launch_assign_kp<double, 16>(G, idx, val, n, m, tab, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);
-      else launch_assign_kp<double, 32>(G, idx, val, n, m, tab, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);
+      if (K <= 8) launch_assign_kp<double, 8>(G, idx, val, n, m, tx, ty, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);
+      else if (K <= 16) launch_assign_kp<double, 16>(G, idx, val, n, m, tx, ty, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);
+      else launch_assign_kp<double, 32>(G, idx, val, n, m, tx, ty, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);
     } else {
-      if (K <= 8) launch_assign_kp<float, 8>(G, idx, val, n, m, tab, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);
-      else if (K <= 16) launch_assign_kp<float, 16>(G, idx, val, n, m, tab, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);
-      else launch_assign_kp<float, 32>(G, idx, val, n, m, tab, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);
+      if (K <= 8) launch_assign_kp<float, 8>(G, idx, val, n, m, tx, ty, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);
+      else if (K <= 16) launch_assign_kp<float, 16>(G, idx, val, n, m, tx, ty, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);
+      else launch_assign_kp<float, 32>(G, idx, val, n, m, tx, ty, K, p_pad, prev, labels, d2min, bch, bmx, barg, st);
     }
     rc = check_launch("km_assign_kernel");
     if (rc) return rc;
@@ -699,7 +709,8 @@ int assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, i
 // K5f over a device-side list of points (K5t's unresolved points), G blocks of partials
 int assign_filter_list_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m,
                               const double* mu, int32_t p_pad, int32_t K, const int32_t* prev, int32_t* labels,
-                              double* d2min, const int64_t* list, const int32_t* list_n, const double2* tab,
+                              double* d2min, const int64_t* list, const int32_t* list_n, const double* tx,
+                              const double* ty,
                               float* t32, int64_t* bch, double* bmx, int64_t* barg, int G, cudaStream_t st) {
   if (K > 256) return fail(SKC_EPARAM, "K5f list pass needs K <= 256");
   const int K4 = (K + 3) & ~3;
@@ -709,7 +720,7 @@ int assign_filter_list_launch(const int32_t* idx, const void* val, int val_f64, 
   const size_t smem = filt_warp_bytes(m, K) * kFiltWarps;
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<G, kFiltWarps * 32, smem, st>>>(idx, val, n, m, t32, K4, tab, K, prev, labels, d2min, bch, bmx, barg, list,
+    kern<<<G, kFiltWarps * 32, smem, st>>>(idx, val, n, m, t32, K4, tx, ty, K, prev, labels, d2min, bch, bmx, barg, list,
                                             list_n);
   };
   const int nb = (K4 + 127) / 128;
@@ -729,9 +740,9 @@ int assign_reduce_launch(const int64_t* bch, const double* bmx, const int64_t* b
   return check_launch("km_assign_reduce_kernel");
 }
 
-int tables2_launch(const double* mu, int32_t p_pad, int32_t K, double2* tab, cudaStream_t st) {
+int tables2_launch(const double* mu, int32_t p_pad, int32_t K, double* tx, double* ty, cudaStream_t st) {
   const int64_t total = (int64_t)p_pad * K;
-  km_tables2_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(mu, total, tab);
+  km_tables2_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(mu, total, tx, ty);
   return check_launch("km_tables2_kernel");
 }
 

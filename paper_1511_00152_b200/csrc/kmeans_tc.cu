@@ -39,11 +39,12 @@ namespace skc {
 int row_sqnorms_launch(const void* val, int val_f64, int64_t n, int32_t m, double* out, cudaStream_t st);
 int assign_filter_list_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m,
                               const double* mu, int32_t p_pad, int32_t K, const int32_t* prev, int32_t* labels,
-                              double* d2min, const int64_t* list, const int32_t* list_n, const double2* tab,
-                              float* t32, int64_t* bch, double* bmx, int64_t* barg, int G, cudaStream_t st);
+                              double* d2min, const int64_t* list, const int32_t* list_n, const double* tx,
+                              const double* ty, float* t32, int64_t* bch, double* bmx, int64_t* barg, int G,
+                              cudaStream_t st);
 int assign_reduce_launch(const int64_t* bch, const double* bmx, const int64_t* barg, int G, int64_t* out,
                          double* d2max, cudaStream_t st);
-int tables2_launch(const double* mu, int32_t p_pad, int32_t K, double2* tab, cudaStream_t st);
+int tables2_launch(const double* mu, int32_t p_pad, int32_t K, double* tx, double* ty, cudaStream_t st);
 
 namespace {
 constexpr int kRows = 128;  // M of one MMA = rows of one tile
@@ -477,7 +478,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) km_tc_filter_kernel(const __gr
 // first index).
 __global__ void __launch_bounds__(kVerifyThreads) km_tc_verify_kernel(
     const uint4* __restrict__ ent, const double* __restrict__ vT, int G, int64_t ntp, int64_t n, int m,
-    const double2* __restrict__ tab, int K, const double* __restrict__ colsq, const uint8_t* __restrict__ cand,
+    const double* __restrict__ tabx, const double* __restrict__ taby, int K, const double* __restrict__ colsq,
+    const uint8_t* __restrict__ cand,
     const uint8_t* __restrict__ ncand, const int32_t* __restrict__ prev, int32_t* __restrict__ labels,
     double* __restrict__ d2min, int64_t* __restrict__ blk_changed, double* __restrict__ blk_max,
     int64_t* __restrict__ blk_arg) {
@@ -489,7 +491,6 @@ __global__ void __launch_bounds__(kVerifyThreads) km_tc_verify_kernel(
   double bmax = -1.0;
   int64_t barg = -1;
   const int r = threadIdx.x, lane = r & 31, wp = r >> 5;
-  const size_t tK = 2 * (size_t)K;
   for (int64_t tp = blockIdx.x; tp < ntp; tp += gridDim.x) {
     const int64_t i = tp * kPts + r;
     int nc = i < n ? ncand[i] : 0;
@@ -516,7 +517,8 @@ __global__ void __launch_bounds__(kVerifyThreads) km_tc_verify_kernel(
       const int rr = pr[q], k = pk[q];
       const uint4* ep = ent + (size_t)tp * G * kPts + rr;
       const double* vp = vT + (size_t)tp * m * kPts + rr;
-      const double* tk = reinterpret_cast<const double*>(tab + k);
+      const double* tkx = tabx + k;
+      const double* tky = taby + k;
       double acc = 0.0;
       for (int g = 0; g < G; ++g) {
         const uint4 w = __ldg(ep + (size_t)g * kPts);
@@ -524,7 +526,7 @@ __global__ void __launch_bounds__(kVerifyThreads) km_tc_verify_kernel(
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int t = 4 * g + u;
-          if (t < m) acc = dadd(acc, dmul(__ldg(vp + (size_t)t * kPts), __ldg(tk + (ww[u] & 0xFFFFu) * tK)));
+          if (t < m) acc = dadd(acc, dmul(__ldg(vp + (size_t)t * kPts), __ldg(tkx + (ww[u] & 0xFFFFu) * (size_t)K)));
         }
       }
       for (int g = 0; g < G; ++g) {
@@ -532,7 +534,7 @@ __global__ void __launch_bounds__(kVerifyThreads) km_tc_verify_kernel(
         const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          if (4 * g + u < m) acc = dadd(acc, __ldg(tk + (ww[u] & 0xFFFFu) * tK + 1));
+          if (4 * g + u < m) acc = dadd(acc, __ldg(tky + (ww[u] & 0xFFFFu) * (size_t)K));
       }
       sd[q] = dadd(acc, __ldg(colsq + tp * kPts + rr));
     }
@@ -671,7 +673,7 @@ static int verify_grid(int64_t n) {
 static int list_grid() { return 4 * sm_count(); }
 static int kt_npad(int32_t K) { return (K + 15) & ~15; }
 
-// per-iteration: [tab double2 p*K][t32 p*K4][img][cand n*8][ncand n][list n][list_n][block partials]
+// per-iteration: [tab: -2 mu and mu*mu planes, p*K each][t32 p*K4][img][cand n*8][ncand n][list n][list_n][block partials]
 struct KtWs {
   size_t tab, t32, img, cand, ncand, list, list_n, bch, bmx, barg, total;
 };
@@ -704,7 +706,8 @@ int kmtc_assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t
                        double* d2max, const void* prep, void* ws, cudaStream_t st) {
   const KtWs L = kt_ws(n, p_pad, K);
   char* w = static_cast<char*>(ws);
-  double2* tab = reinterpret_cast<double2*>(w + L.tab);
+  double* tx = reinterpret_cast<double*>(w + L.tab);
+  double* ty = tx + (size_t)p_pad * K;
   float* t32 = reinterpret_cast<float*>(w + L.t32);
   __nv_bfloat16* img = reinterpret_cast<__nv_bfloat16*>(w + L.img);
   uint8_t* cand = reinterpret_cast<uint8_t*>(w + L.cand);
@@ -719,7 +722,7 @@ int kmtc_assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t
   const uint4* ent = R.ent;
   const double* vT = R.vT;
   int rc;
-  if ((rc = tables2_launch(mu, p_pad, K, tab, st))) return rc;
+  if ((rc = tables2_launch(mu, p_pad, K, tx, ty, st))) return rc;
   const int Npad = kt_npad(K);
   const int64_t img_elems = (int64_t)(p_pad / kChunk) * Npad * kKC;
   km_tc_table_kernel<<<(unsigned)((img_elems + 255) / 256), 256, 0, st>>>(mu, p_pad, K, Npad, img);
@@ -755,10 +758,10 @@ int kmtc_assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t
     if (grid > H.ntp) grid = H.ntp;
     km_tc_filter_kernel<<<(unsigned)grid, kWarps * 32, smem, st>>>(H);
     if ((rc = check_launch("km_tc_filter_kernel"))) return rc;
-    km_tc_verify_kernel<<<Gv, kVerifyThreads, 0, st>>>(ent, vT, H.G, H.ntp, n, m, tab, K, colsq, cand, ncand, prev,
+    km_tc_verify_kernel<<<Gv, kVerifyThreads, 0, st>>>(ent, vT, H.G, H.ntp, n, m, tx, ty, K, colsq, cand, ncand, prev,
                                                         labels, d2min, bch, bmx, barg);
     if ((rc = check_launch("km_tc_verify_kernel"))) return rc;
-    if ((rc = assign_filter_list_launch(idx, val, val_f64, n, m, mu, p_pad, K, prev, labels, d2min, list, list_n, tab,
+    if ((rc = assign_filter_list_launch(idx, val, val_f64, n, m, mu, p_pad, K, prev, labels, d2min, list, list_n, tx, ty,
                                         t32, bch + Gv, bmx + Gv, barg + Gv, Gl, st)))
       return rc;
   }
