@@ -100,6 +100,8 @@ def _assign_tc(skc, sk, mu, prev):
     (1024, 51, 33, 9000, 1.0, "f32", "dense"),      # fp32 sketch values, ragged K
     (512, 200, 128, 4000, 2.0, "f64", "dense"),     # largest K, m > 128
     (256, 25, 1, 700, 1.0, "f64", "dense"),         # one centre
+    (4096, 82, 64, 3000, 2.0, "f32", "dense"),      # C4 shape (128 chunks per tile pair)
+    (512, 1, 17, 2000, 1.0, "f64", "dense"),        # one kept coordinate per point
 ])
 def test_tc_filter_equals_exact(skc, monkeypatch, p, m, K, n, spread, compute, init):
     rng = np.random.default_rng(p + K + n)
