@@ -64,7 +64,12 @@ constexpr int kTileA = kRows * kKC * 2;
 #endif
 constexpr int kNst = SKC_KT_STAGES;
 constexpr int kNmax = 128;  // two tiles x two TMEM buffers x 128 columns = 512
-constexpr int kFillWarps = kPts / 32;
+#ifndef SKC_KT_FILLW
+#define SKC_KT_FILLW 8
+#endif
+constexpr int kFillWarps = SKC_KT_FILLW;        // fill warps (8: two entries per thread per chunk)
+constexpr int kFillT = kFillWarps * 32;
+constexpr int kPF = kPts * 2 / kFillT;          // entries per fill thread per chunk kept in registers
 constexpr int kProdWarp = kFillWarps;
 constexpr int kMmaWarp = kFillWarps + 1;
 constexpr int kEpi0 = kFillWarps + 2;
@@ -245,7 +250,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) km_tc_filter_kernel(const __gr
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[2 * kNst + 4];
   __shared__ uint32_t tmem_base;
-  __shared__ uint32_t prev_off[kNst][2][kPts];  // fill: offsets this thread wrote in each stage
+  __shared__ uint32_t prev_off[kNst][kPF][kFillT];  // fill: offsets this thread wrote in each stage
   __shared__ int dirty[kNst];                   // chunk sequence number of a stage's last overflow
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bbytes = (uint32_t)P.Npad * kKC * 2;
@@ -267,9 +272,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) km_tc_filter_kernel(const __gr
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (warp < kFillWarps) {  // every A operand starts zero; the fill then only clears what it wrote
-    for (uint32_t q = threadIdx.x; q < (uint32_t)kNst * stage_bytes / 16; q += kPts)
+    for (uint32_t q = threadIdx.x; q < (uint32_t)kNst * stage_bytes / 16; q += kFillT)
       if ((16u * q) % stage_bytes < (uint32_t)(kTiles * kTileA)) sts128(base_sh + 16u * q, 0u, 0u, 0u, 0u);
-    for (int s = 0; s < kNst; ++s) prev_off[s][0][threadIdx.x] = prev_off[s][1][threadIdx.x] = 0xFFFFFFFFu;
+    for (int s = 0; s < kNst; ++s)
+      for (int u = 0; u < kPF; ++u) prev_off[s][u][threadIdx.x] = 0xFFFFFFFFu;
     if (threadIdx.x < kNst) dirty[threadIdx.x] = -1 - kNst;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -280,8 +286,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) km_tc_filter_kernel(const __gr
 
   if (warp < kFillWarps) {
     // ------------------------------------------------------------ fill: zero + scatter per stage
-    const int ft = threadIdx.x;  // 0 .. kPts-1
-    constexpr int kPF = 2;       // entries per thread per chunk held in registers (more: loop)
+    const int ft = threadIdx.x;  // 0 .. kFillT-1
     int64_t gc = 0;
     for (int64_t tp = blockIdx.x; tp < P.ntp; tp += gridDim.x) {
       const uint32_t* L = P.lists + (size_t)tp * kPts * P.m;
@@ -298,7 +303,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) km_tc_filter_kernel(const __gr
         f.o1 = c < nch ? __ldg(of + c + 1) : 0u;
 #pragma unroll
         for (int u = 0; u < kPF; ++u) {
-          const uint32_t q = f.o0 + (uint32_t)(ft + u * kPts);
+          const uint32_t q = f.o0 + (uint32_t)(ft + u * kFillT);
           f.e[u] = q < f.o1 ? __ldg(L + q) : 0xFFFFFFFFu;
         }
       };
@@ -320,7 +325,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) km_tc_filter_kernel(const __gr
         // (or everything, if that chunk had entries beyond the kPF per thread kept here)
         if (dirty[s] == (int)gc - kNst) {
 #pragma unroll
-          for (int q = 0; q < kTiles * kTileA / 16 / kPts; ++q) sts128(sa + 16u * (ft + q * kPts), 0u, 0u, 0u, 0u);
+          for (int q = 0; q < kTiles * kTileA / 16 / kFillT; ++q) sts128(sa + 16u * (ft + q * kFillT), 0u, 0u, 0u, 0u);
         } else {
 #pragma unroll
           for (int u = 0; u < kPF; ++u) {
@@ -331,10 +336,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) km_tc_filter_kernel(const __gr
             }
           }
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(kPts) : "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(kFillT) : "memory");
 #pragma unroll
         for (int u = 0; u < kPF; ++u) prev_off[s][u][ft] = e[u] != 0xFFFFFFFFu ? put(sa, e[u]) : 0xFFFFFFFFu;
-        for (uint32_t q = cur.o0 + (uint32_t)(ft + kPF * kPts); q < cur.o1; q += kPts) {
+        for (uint32_t q = cur.o0 + (uint32_t)(ft + kPF * kFillT); q < cur.o1; q += kFillT) {
           put(sa, __ldg(L + q));
           dirty[s] = (int)gc;
         }
