@@ -23,6 +23,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include")]
+# experiments only: extra nvcc flags, e.g. SKC_EXTRA_NVCC_FLAGS="-DSKC_GATHER_STAGES=3"
+FLAGS += os.environ.get("SKC_EXTRA_NVCC_FLAGS", "").split()
 
 
 def _newer(target: str, deps) -> bool:

@@ -594,14 +594,18 @@ __global__ void __launch_bounds__(kThreads, 3) sketch_kernel(const SketchParams 
 // kGiven with fp32 rows: K1 without the selection, double-buffered. Tile k+1's cp.async
 // copies are in flight while tile k is transformed and its values gathered, so the kernel
 // streams at HBM rate instead of exposing each tile's load latency.
+#ifndef SKC_GATHER_STAGES
+#define SKC_GATHER_STAGES 2  // tile buffers per CTA: STAGES - 1 tiles load while one transforms
+#endif
+constexpr int kGatherStages = SKC_GATHER_STAGES;
 template <int LOGP>
-__global__ void __launch_bounds__(kThreads, 3) gather_kernel(const SketchParams P) {
+__global__ void __launch_bounds__(kThreads, kGatherStages > 2 ? 2 : 3) gather_kernel(const SketchParams P) {
   using G = Geo<LOGP>;
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr size_t kTileBytes = sizeof(float) * ((G::WORDS + 3) & ~3);
   float* xs0 = reinterpret_cast<float*>(smem);
   constexpr int kSignWords = (G::P + 31) / 32;
-  uint32_t* sgn = reinterpret_cast<uint32_t*>(smem + 2 * kTileBytes);
+  uint32_t* sgn = reinterpret_cast<uint32_t*>(smem + kGatherStages * kTileBytes);
   const int warp = threadIdx.x >> 5;
   if (P.use_signs) {  // D diagonal, _hash.py:38-43, regenerated per CTA
     for (int w = threadIdx.x; w < kSignWords; w += kThreads) {
@@ -632,16 +636,20 @@ __global__ void __launch_bounds__(kThreads, 3) gather_kernel(const SketchParams 
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   int64_t tile = blockIdx.x;
-  if (tile < P.num_tiles) issue(tile, 0);
+  // prologue: tiles it = 0 .. STAGES-2 in flight; every iteration commits one group (empty
+  // past the end), so wait_group STAGES-1 always means "this iteration's tile has landed"
+#pragma unroll
+  for (int k = 0; k < kGatherStages - 1; ++k) {
+    const int64_t t = tile + (int64_t)k * gridDim.x;
+    if (t < P.num_tiles) issue(t, k);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   for (int it = 0; tile < P.num_tiles; tile += gridDim.x, ++it) {
-    const int buf = it & 1;
-    const int64_t next = tile + gridDim.x;
-    if (next < P.num_tiles) {
-      issue(next, buf ^ 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_all;" ::: "memory");
-    }
+    const int buf = it % kGatherStages;
+    const int64_t next = tile + (int64_t)(kGatherStages - 1) * gridDim.x;
+    if (next < P.num_tiles) issue(next, (it + kGatherStages - 1) % kGatherStages);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(kGatherStages - 1) : "memory");
     const int64_t row0 = tile * G::S;
     const int64_t rows_left = P.n - row0;
     // this warp's first sample's indices load during the transform (m <= 64 in registers)
@@ -680,7 +688,7 @@ __global__ void __launch_bounds__(kThreads, 3) gather_kernel(const SketchParams 
 template <int LOGP>
 static int launch_gather_t(SketchParams P, cudaStream_t st) {
   using G = Geo<LOGP>;
-  const size_t smem = 2 * sizeof(float) * ((G::WORDS + 3) & ~3) + 4 * (((G::P + 31) / 32 + 3) & ~3);
+  const size_t smem = kGatherStages * sizeof(float) * ((G::WORDS + 3) & ~3) + 4 * (((G::P + 31) / 32 + 3) & ~3);
   auto kern = gather_kernel<LOGP>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return check_launch("gather smem attribute");
