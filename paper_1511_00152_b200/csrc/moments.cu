@@ -183,12 +183,16 @@ int moments_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, 
 // into the same int64 partial. A reduce kernel sums the groups in int64 and scales to fp64.
 // tau = 8 * rms(values), from K2's statistics. Quantum 2^-S ~ 6e-8 * tau^2.
 // ======================================================================================
+#ifndef SKC_COV_UNROLL
+#define SKC_COV_UNROLL 1  // unroll of the flat pair loop (experiments)
+#endif
 #ifndef SKC_COV_SMEM_KB
 #define SKC_COV_SMEM_KB 220
 #endif
 #ifndef SKC_COV_WARPS
 #define SKC_COV_WARPS 32
 #endif
+constexpr int kCovUnroll = SKC_COV_UNROLL;
 constexpr int kSmemBudget = SKC_COV_SMEM_KB * 1024;  // dynamic smem per CTA
 constexpr int kCovWarps = SKC_COV_WARPS;
 constexpr int kMaxBands = 511;
@@ -349,6 +353,7 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
         T[lane + 32] = make_int2((int)lo_sh + 4 * rowbase[j1 - r0], __float_as_int(v1 * scale_a));
       __syncwarp();
       const int F1 = nhi * m - ((nhi * (nhi - 1)) >> 1);
+#pragma unroll kCovUnroll
       for (int f = nlo * m - ((nlo * (nlo - 1)) >> 1) + lane; f < F1; f += 32) {
         const int2 tt = T[ptt[f]], uu = T[ptu[f]];
         const uint32_t addr = (uint32_t)(tt.x + uu.x);
