@@ -282,7 +282,7 @@ def main():
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=None, help="override rows per GPU")
-    ap.add_argument("--compute", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--compute", default="f64", choices=["f32", "f64"])
     ap.add_argument("--sampler", default="oracle", choices=["oracle", "philox"],
                     help="oracle: the reference's index rule (bit-exact, headline); philox: north_star's Philox sampler")
     ap.add_argument("--no-e2e", action="store_true")

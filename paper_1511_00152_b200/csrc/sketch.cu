@@ -853,6 +853,11 @@ static void plan_select(int32_t pk, int32_t m, SketchParams& P) {
   }
 }
 
+// gather.cu: the TMA-staged gather (-1 when the shape is not eligible)
+int gather_tma_launch(const void* X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, int32_t p_pad,
+                      int32_t use_signs, uint64_t sign_seed, int32_t m, int32_t compute_dtype, const int32_t* idx_in,
+                      void* val_out, int32_t val_dtype, cudaStream_t st);
+
 int sketch_launch(const void* X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, int32_t p_pad, int32_t kind,
                   uint64_t sign_seed, uint64_t master_seed, int64_t col0, int32_t m, int32_t compute_dtype,
                   int32_t* idx_out, void* val_out, int32_t val_dtype, double* y_out, cudaStream_t st) {
@@ -899,6 +904,9 @@ int sketch_launch(const void* X, int32_t x_dtype, int64_t ld, int64_t n, int32_t
   G.idx_out = nullptr;
   G.cap = 0;  // no selection scratch
   if (val_out == nullptr) return SKC_OK;
+  rc = gather_tma_launch(X, x_dtype, ld, n, p, p_pad, P.use_signs, sign_seed, m, compute_dtype, idx_out, val_out,
+                         val_dtype, st);
+  if (rc != -1) return rc;
   if (compute_dtype == SKC_F64) return launch_sketch_logp<double>(logp, G, st);
   if (G.vec && !G.x_f64 && logp >= 2) return launch_gather_logp(logp, G, st);
   return launch_sketch_logp<float>(logp, G, st);
@@ -1046,6 +1054,9 @@ int sketch_given_launch(const void* X, int32_t x_dtype, int64_t ld, int64_t n, i
   while ((1 << logp) < p_pad) ++logp;
   const uintptr_t xa = reinterpret_cast<uintptr_t>(X);
   P.vec = p == p_pad && p_pad >= 4 && (ld % 4) == 0 && (xa % 16) == 0;
+  const int rc = gather_tma_launch(X, x_dtype, ld, n, p, p_pad, P.use_signs, sign_seed, m, compute_dtype, idx_in,
+                                   val_out, val_dtype, st);
+  if (rc != -1) return rc;
   if (compute_dtype == SKC_F64) return launch_sketch_logp<double>(logp, P, st);
   if (P.vec && !P.x_f64 && logp >= 2) return launch_gather_logp(logp, P, st);
   return launch_sketch_logp<float>(logp, P, st);
