@@ -100,10 +100,10 @@ __host__ __device__ __forceinline__ int units_total(int nb) {
   for (int i = 0; i < nb; ++i) t += nb / 2 - (i >> 1);
   return t;
 }
-__device__ __forceinline__ float value_scale(const double* stats) {
+__device__ __forceinline__ double value_scale(const double* stats) {
   int E = 0;
-  frexp(stats[1] > 0.0 ? stats[1] : 1.0, &E);  // x = w * 2^(15 - E): |x| <= 2^15
-  return ldexpf(1.0f, 15 - E);
+  frexp(stats[1] > 0.0 && stats[1] <= 1.0e300 ? stats[1] : 1.0, &E);  // x = w * 2^(15 - E): |x| <= 2^15
+  return ldexp(1.0, 15 - E);  // applied in fp64, so any exponent range scales exactly
 }
 }  // namespace
 
@@ -151,11 +151,11 @@ __global__ void __launch_bounds__(256) cov_bucket_kernel(const int32_t* __restri
   }
   if (lane == 0) boff[c * (nb + 1) + nb] = run;
   __syncwarp();
-  const float xs = value_scale(stats);
+  const double xs = value_scale(stats);
   for (int k = 0; k < rows; ++k)
     for (int t = lane; t < m; t += 32) {
       const int j = __ldg(ic + k * m + t);
-      const float x = (float)__ldg(vc + k * m + t) * xs;
+      const float x = (float)((double)__ldg(vc + k * m + t) * xs);
       const __half h = __float2half_rn(x);
       const uint32_t lo = __half_as_ushort(__float2half_rn(x - __half2float(h)));
       const int cc = j & 127;
@@ -331,7 +331,7 @@ __global__ void cov_tc_reduce_kernel(const double* __restrict__ part, int nunits
   const int b = blockIdx.x * blockDim.x + threadIdx.x, a = blockIdx.y;
   if (b >= p_pad || b < a) return;
   int E = 0;
-  frexp(stats[1] > 0.0 ? stats[1] : 1.0, &E);
+  frexp(stats[1] > 0.0 && stats[1] <= 1.0e300 ? stats[1] : 1.0, &E);
   const double inv = ldexp(1.0, 2 * (E - 15));
   const int nb2 = p_pad / kB, I = a / kA, J2 = b / kB;
   int u = 0;

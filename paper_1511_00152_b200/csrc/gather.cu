@@ -315,7 +315,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       windows_from<LOGP, T, 1>(work, tu, team);
       team_sync<L::TW>(team);
       auto val_at = [&](int f, int j) -> T {
-        const int s = f / m;
+        const int s = L::Q == 1 ? 0 : f / m;
         return Arith<T>::mul(work[s * L::SP + j + L::PAD * (j >> 5)], scale);
       };
       const int64_t o = row0 * m;
@@ -339,14 +339,27 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
 // host side
 template <typename T>
 struct Cfg;
-template <>
-struct Cfg<float> {
-  static constexpr int NCW = 8, NST = 4;
+// consumer warps and stages per type (A/B: tools/variant_build.sh NAME "-DSKC_GT64_NCW=12 ...")
+#ifndef SKC_GT32_NCW
+#define SKC_GT32_NCW 16
+#endif
+#ifndef SKC_GT32_NST
+#define SKC_GT32_NST 2
+#endif
+#ifndef SKC_GT64_NCW
+#define SKC_GT64_NCW 8
+#endif
+#ifndef SKC_GT64_NST
+#define SKC_GT64_NST 3
+#endif
+template <int A, int B>
+struct CfgV {
+  static constexpr int NCW = A, NST = B;
 };
 template <>
-struct Cfg<double> {
-  static constexpr int NCW = 8, NST = 3;
-};
+struct Cfg<float> : CfgV<SKC_GT32_NCW, SKC_GT32_NST> {};
+template <>
+struct Cfg<double> : CfgV<SKC_GT64_NCW, SKC_GT64_NST> {};
 
 template <int LOGP, typename T>
 static size_t smem_bytes() {

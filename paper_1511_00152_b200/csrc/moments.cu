@@ -233,6 +233,7 @@ struct CovParams {
   int64_t n;
   int32_t m, p_pad;
   const double* stats;
+  double* tri;               // output triangle (wide-range / huge products go here in fp64)
   unsigned long long* part;  // [groups][tri_total] int64 fixed-point partials
   int nbands, groups;
   int aligned;               // idx/val 16-byte aligned: tiles may use bulk copies
@@ -252,15 +253,30 @@ __device__ __forceinline__ void red_if(bool p, unsigned long long* addr, unsigne
       : "memory");
 }
 
-// S from the value statistics; identical in every CTA and in the reduce kernel
+// S from the value statistics; identical in every CTA and in the reduce kernel. Products are
+// w_a * w_b * 2^S, |q| <= 2^30 for |w| <= tau; S is even and each factor carries 2^(S/2) as a
+// float. Outside |S| <= kWideS (rms below ~2^-105 or above ~2^135, e.g. fp64 sketches of
+// extreme data) the factors are not representable as scaled floats, and every product takes
+// the exact fp64 path instead (cov_wide).
+constexpr int kWideS = 240;
 __device__ __forceinline__ int cov_scale(const double* stats, int m, double* tau_out) {
   const double cnt = stats[2] * (double)m;
   const double rms = cnt > 0 ? sqrt(stats[0] / cnt) : 0.0;
   double tau = 8.0 * rms;
-  if (!(tau > 0.0)) tau = 1.0;
+  if (!(tau > 0.0) || !(tau <= 1.0e300)) tau = 1.0;  // zero, NaN or overflowed statistics
   *tau_out = tau;
-  int S = (int)floor(log2(1073741824.0 / (tau * tau)));
-  return S & ~1;  // even, so each factor carries 2^(S/2)
+  const int S = (int)floor(30.0 - 2.0 * log2(tau));
+  return max(-1000, min(1000, S)) & ~1;
+}
+__device__ __forceinline__ bool cov_wide(int S) { return S > kWideS || S < -kWideS; }
+// exact fp64 fallback for one product: int64 fixed point when it fits, else (huge outliers,
+// NaN/inf, or a wide-range scale) an fp64 atomic straight into the output triangle
+__device__ __forceinline__ void cov_add_exact(double va, double vb, double full_s, bool wide,
+                                              unsigned long long* part_e, double* tri_e) {
+  const double pr = dmul(va, vb);
+  const double q = dmul(pr, full_s);
+  if (!wide && fabs(q) < 4.611686018427387904e18) atomicAdd(part_e, (unsigned long long)__double2ll_rn(q));
+  else atomicAdd(tri_e, pr);
 }
 
 // Each warp streams its own rows (no CTA-wide synchronisation), prefetching the next row
@@ -294,9 +310,11 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
 
   double tau;
   const int S = cov_scale(P.stats, m, &tau);
-  const float scale_a = (float)ldexp(1.0, S);
+  const bool wide = cov_wide(S);
+  const float sh = wide ? 1.0f : (float)ldexp(1.0, S / 2);  // 2^(S/2) on each factor
   const double full_s = ldexp(1.0, S);
-  const float ftau = (float)tau;
+  const float ftau = wide ? -1.0f : (float)tau;  // wide: every row takes the exact path
+  double* tri_b = P.tri + e0;
 
   for (int e = threadIdx.x; e < ne; e += blockDim.x) lo[e] = kBias;
   for (int a = r0 + threadIdx.x; a < r1; a += blockDim.x) rowbase[a - r0] = (int)(tri_off(a, P.p_pad) - e0) - a;
@@ -330,12 +348,12 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
   auto visit = [&](const int64_t r, const int j0, const int j1, const float v0, const float v1) {
     int nlo = __popc(__ballot_sync(kFullMask, j0 < r0)) + __popc(__ballot_sync(kFullMask, j1 < r0));
     int nhi = __popc(__ballot_sync(kFullMask, j0 < r1)) + __popc(__ballot_sync(kFullMask, j1 < r1));
-    bool big = fabsf(v0) > ftau || fabsf(v1) > ftau;  // lanes past m hold 0
+    bool big = !(fabsf(v0) <= ftau) || !(fabsf(v1) <= ftau);  // lanes past m hold 0; NaN is big
     if constexpr (WIDE) {
       for (int t0 = 64; t0 < m; t0 += 32) {  // columns beyond the two register chunks
         const int t = t0 + lane;
         const int j = t < m ? __ldg(P.idx + r * m + t) : 0x7FFFFFFF;
-        if (t < m) big |= fabsf((float)__ldg(val + r * m + t)) > ftau;
+        if (t < m) big |= !(fabsf((float)__ldg(val + r * m + t)) <= ftau);
         nlo += __popc(__ballot_sync(kFullMask, j < r0));
         nhi += __popc(__ballot_sync(kFullMask, j < r1));
       }
@@ -345,12 +363,12 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
     if (!WIDE && !any_big) {
       // the visit's pairs {(t, u): nlo <= t < nhi, t <= u < m} are the contiguous range
       // [tri_off(nlo), tri_off(nhi)) of the t-major pair table; lane f takes pair f
-      if (has0) U[lane] = make_int2(j0 << 2, __float_as_int(v0));
-      if (has1) U[lane + 32] = make_int2(j1 << 2, __float_as_int(v1));
-      if (lane >= nlo && lane < nhi)
-        T[lane] = make_int2((int)lo_sh + 4 * rowbase[j0 - r0], __float_as_int(v0 * scale_a));
+      const float s0 = v0 * sh, s1 = v1 * sh;  // exact power-of-two scalings
+      if (has0) U[lane] = make_int2(j0 << 2, __float_as_int(s0));
+      if (has1) U[lane + 32] = make_int2(j1 << 2, __float_as_int(s1));
+      if (lane >= nlo && lane < nhi) T[lane] = make_int2((int)lo_sh + 4 * rowbase[j0 - r0], __float_as_int(s0));
       if (lane + 32 >= nlo && lane + 32 < nhi)
-        T[lane + 32] = make_int2((int)lo_sh + 4 * rowbase[j1 - r0], __float_as_int(v1 * scale_a));
+        T[lane + 32] = make_int2((int)lo_sh + 4 * rowbase[j1 - r0], __float_as_int(s1));
       __syncwarp();
       const int F1 = nhi * m - ((nhi * (nhi - 1)) >> 1);
 #pragma unroll kCovUnroll
@@ -371,17 +389,17 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
     const V* vr = val + r * m;
     if (has0) {
       sidx[lane] = j0;
-      sval[lane] = v0 * scale_a;
+      sval[lane] = v0 * sh;
     }
     if (has1) {
       sidx[lane + 32] = j1;
-      sval[lane + 32] = v1 * scale_a;
+      sval[lane + 32] = v1 * sh;
     }
     for (int t0 = 64; t0 < m; t0 += 32) {
       const int t = t0 + lane;
       if (t < m) {
         sidx[t] = __ldg(ir + t);
-        sval[t] = (float)__ldg(vr + t) * scale_a;
+        sval[t] = (float)__ldg(vr + t) * sh;
       }
     }
     __syncwarp();
@@ -391,7 +409,7 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
         const int tmax = min(nhi, c0 + 32);  // rows t <= u within this chunk
         if (nlo >= tmax) continue;
         const int bu = u < m ? sidx[u] : 0;
-        const float vu = u < m ? (c0 == 0 ? v0 : (c0 == 32 ? v1 : (float)__ldg(vr + u))) : 0.f;
+        const float vu = u < m ? sval[u] : 0.f;
         for (int t = nlo; t < tmax; ++t) {
           const int base = rowbase[sidx[t] - r0];
           const float va = sval[t];
@@ -405,14 +423,12 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
         }
       }
     } else {
-      // a value above tau: exact fp64 product, scaled, straight to the int64 partial
+      // a value above tau (or a wide-range scale): exact fp64 products
       for (int t = nlo; t < nhi; ++t) {
         const double va = (double)__ldg(vr + t);
         const int base = rowbase[sidx[t] - r0];
-        for (int u = t + lane; u < m; u += 32) {
-          const long long q = __double2ll_rn(dmul(dmul(va, (double)__ldg(vr + u)), full_s));
-          atomicAdd(part + base + sidx[u], (unsigned long long)q);
-        }
+        for (int u = t + lane; u < m; u += 32)
+          cov_add_exact(va, (double)__ldg(vr + u), full_s, wide, part + base + sidx[u], tri_b + base + sidx[u]);
       }
     }
     __syncwarp();
@@ -461,16 +477,18 @@ template <typename V>
 __global__ void __launch_bounds__(kCovGWarps * 32) cov_global_kernel(const int32_t* __restrict__ idx,
                                                                     const V* __restrict__ val, int64_t n, int m,
                                                                     int32_t p_pad, const double* __restrict__ stats,
-                                                                    unsigned long long* __restrict__ acc) {
+                                                                    unsigned long long* __restrict__ acc,
+                                                                    double* __restrict__ tri) {
   extern __shared__ int2 gst[];  // per warp: T[m] = (tri_off(j) - j, w * 2^S), U[m] = (j, w)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int2* T = gst + (size_t)warp * 2 * m;
   int2* U = T + m;
   double tau;
   const int S = cov_scale(stats, m, &tau);
-  const float scale_a = (float)ldexp(1.0, S);
+  const bool wide = cov_wide(S);
+  const float sh = wide ? 1.0f : (float)ldexp(1.0, S / 2);  // 2^(S/2) on each factor
   const double full_s = ldexp(1.0, S);
-  const float ftau = (float)tau;
+  const float ftau = wide ? -1.0f : (float)tau;
   const int Lp = m + 1;
   const int F = m * (m + 1) / 2;
   float inv;
@@ -483,9 +501,9 @@ __global__ void __launch_bounds__(kCovGWarps * 32) cov_global_kernel(const int32
     for (int t = lane; t < m; t += 32) {
       const int j = __ldg(ir + t);
       const float w = (float)__ldg(vr + t);
-      big |= fabsf(w) > ftau;
-      U[t] = make_int2(j, __float_as_int(w));
-      T[t] = make_int2((int)(tri_off(j, p_pad) - j), __float_as_int(w * scale_a));
+      big |= !(fabsf(w) <= ftau);
+      U[t] = make_int2(j, __float_as_int(w * sh));
+      T[t] = make_int2((int)(tri_off(j, p_pad) - j), __float_as_int(w * sh));
     }
     const bool any_big = __any_sync(kFullMask, big);
     __syncwarp();
@@ -507,10 +525,8 @@ __global__ void __launch_bounds__(kCovGWarps * 32) cov_global_kernel(const int32
       for (int t = 0; t < m; ++t) {
         const double va = (double)__ldg(vr + t);
         const int base = T[t].x;
-        for (int u = t + lane; u < m; u += 32) {
-          const long long q = __double2ll_rn(dmul(dmul(va, (double)__ldg(vr + u)), full_s));
-          asm volatile("red.global.add.u64 [%0], %1;" ::"l"(acc + (base + U[u].x)), "l"(q) : "memory");
-        }
+        for (int u = t + lane; u < m; u += 32)
+          cov_add_exact(va, (double)__ldg(vr + u), full_s, wide, acc + (base + U[u].x), tri + (base + U[u].x));
       }
     }
     __syncwarp();
@@ -530,11 +546,11 @@ static int cov_launch_global(const int32_t* idx, const void* val, int val_f64, i
   if (val_f64) {
     cudaFuncSetAttribute(cov_global_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cov_global_kernel<double><<<(unsigned)grid, kCovGWarps * 32, smem, st>>>(idx, (const double*)val, n, m, p_pad,
-                                                                              stats, acc);
+                                                                              stats, acc, tri);
   } else {
     cudaFuncSetAttribute(cov_global_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cov_global_kernel<float><<<(unsigned)grid, kCovGWarps * 32, smem, st>>>(idx, (const float*)val, n, m, p_pad,
-                                                                            stats, acc);
+                                                                            stats, acc, tri);
   }
   if ((rc = check_launch("cov_global_kernel"))) return rc;
   cov_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(acc, 1, total, m, stats, tri);
@@ -612,6 +628,7 @@ static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int
   H.m = m;
   H.p_pad = p_pad;
   H.stats = stats;
+  H.tri = tri;
   H.part = reinterpret_cast<unsigned long long*>(ws);
   H.aligned = (reinterpret_cast<uintptr_t>(idx) % 16 == 0) && (reinterpret_cast<uintptr_t>(val) % 16 == 0);
   const int64_t total = tri_off(p_pad, p_pad);

@@ -75,7 +75,7 @@ def accumulate_moments(sketch: SparseSketch, covariance: bool = True, into: Opti
     return into
 
 
-def stream_moments(source, spec, plan, *, covariance: bool = True, compute: str = "f32", device=None,
+def stream_moments(source, spec, plan, *, covariance: bool = True, compute: str = "f64", device=None,
                    col0: int = 0, into: Optional[Moments] = None) -> Moments:
     """Sketch and accumulate the estimators' partial sums chunk by chunk, without keeping the
     sketch (sketch.py:196-223 then estimators.py:30-66).

@@ -8,7 +8,8 @@ OUT=$ROOT/build/variants/$1
 mkdir -p "$OUT"
 NVCC=${NVCC:-/usr/local/cuda/bin/nvcc}
 FL="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -I $SRC/include $2"
-for s in capi sketch moments cov_tc kmeans kmeans_tc formats dense; do
+SRCS=$(cd $SRC && python -c "from paper_1511_00152_b200._build import SOURCES; print(*[x[:-3] for x in SOURCES])")
+for s in $SRCS; do
   $NVCC $FL -c $SRC/paper_1511_00152_b200/csrc/$s.cu -o $OUT/$s.o &
 done
 wait
