@@ -3,16 +3,19 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3] [--impl ours|reference]
 
-One JSON line on rank 0. A "step" is one pass of the hot path over one batch:
-  covariance workloads (c1/c3/c4): K1 sketch -> K2 moments -> K3 covariance -> K4 finalize
-                                   over the whole HBM-resident sample set
-  kmeans workloads (c2/c5):        the Lloyd loop (max_iter iterations, stops early on
-                                   convergence) on the HBM-resident sketch
-``value`` is whole-job throughput with inputs resident in HBM. ``e2e`` runs the same
-metric through the public API (sketch_stream(RowSource(pinned host rows)) ->
-estimate_covariance, so H2D and D2H happen inside the timed region). Inputs are larger
-than the 126 MB L2, so no L2 flush is needed. --impl reference times the reference CPU
-path, the oracle port in C (``oracle/``), on all host cores over a bounded sample.
+One JSON line on rank 0. A "step" is one pass of the hot path over the workload's rows:
+  covariance workloads (c1/c3/c4): K1a indices -> K1b gather (precondition + sample) -> K2 moments
+                                   -> K3 covariance -> (N>1: one allreduce) -> K4 finalize
+  kmeans workloads (c2/c5):        the Lloyd loop (max_iter iterations, stops on convergence)
+                                   on the HBM-resident sketch, from seeded initial points
+Compute defaults to f64: the drop-in sketch_stream's default and the reference's arithmetic
+(bit-exact values). Scaling defaults to "strong": BASELINE's n is the whole job, sharded over
+the N ranks with global column offsets. ``value`` is whole-job throughput with inputs resident
+in HBM (larger than the 126 MB L2, so no flush is needed). ``e2e`` runs the same metric
+through the public API from pinned host rows (H2D and the D2H of the result inside the timed
+region). At N=1 the default run adds one line per other BASELINE config under "configs".
+--impl reference times the reference CPU path on the host cores: the oracle port (C, all
+threads) as the arm's value, and beside it the reference package itself (baseline/_ref).
 """
 
 from __future__ import annotations
@@ -24,7 +27,6 @@ import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 
 import numpy as np
@@ -33,18 +35,19 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # BASELINE.json configs; n is per GPU (weak scaling)
-    "c1": dict(desc="C1 sparsified PCA p=256 m=25 (spiked rank-5)", p=256, n=20000, m=25, kind="cov"),
-    "c1big": dict(desc="C1 shape at steady state, n=2^24", p=256, n=1 << 24, m=25, kind="cov"),
+    # BASELINE.json configs; n is the whole job (strong scaling shards it over the ranks)
+    "c1": dict(desc="C1 sparsified PCA p=256 m=25 (spiked rank-5)", p=256, n=20000, m=25, kind="cov", pcs=5),
+    "c1big": dict(desc="C1 shape at steady state, n=2^24", p=256, n=1 << 24, m=25, kind="cov", pcs=5),
     "c2": dict(desc="C2 sparsified K-means p=512 m=26 K=10", p=512, n=200000, m=26, K=10, iters=20, kind="kmeans"),
     "c3": dict(desc="C3 large covariance p=1024 m=51 (spiked rank-10 + Student-t(3))", p=1024, n=1 << 24, m=51,
-               kind="cov"),
-    "c4": dict(desc="C4 spiky covariance p=4096 m=82", p=4096, n=1 << 21, m=82, kind="cov"),
+               kind="cov", pcs=0),
+    "c4": dict(desc="C4 spiky covariance p=4096 m=82", p=4096, n=1 << 21, m=82, kind="cov", pcs=20),
     "c5": dict(desc="C5 sparsified K-means p=2048 m=102 K=100", p=2048, n=10_000_000, m=102, K=100, iters=10,
                kind="kmeans"),
 }
 SEED = 2026
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
 
 
 def derive_seed(seed, tag):
@@ -64,39 +67,44 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def metric_name(cfg):
+    return "samples/s precondition+sparsify+covariance" if cfg["kind"] == "cov" else "K-means point-iters/s"
+
+
 # ------------------------------------------------------------------ synthetic data
+def _model(wl: str, rng):
+    cfg = WORKLOADS[wl]
+    p = cfg["p"]
+    if wl.startswith("c1"):
+        return np.linalg.qr(rng.standard_normal((p, 5)))[0], np.array([50.0, 40.0, 30.0, 20.0, 10.0])
+    if wl == "c3":
+        return np.linalg.qr(rng.standard_normal((p, 10)))[0], np.arange(100.0, 9.0, -10.0)
+    if wl == "c4":
+        return np.linalg.qr(rng.standard_normal((p, 20)))[0], np.linspace(20.0, 1.0, 20)
+    K = cfg["K"]
+    C = rng.standard_normal((p, K)) * (2.0 if wl == "c2" else 3.0)
+    prob = np.full(K, 1.0 / K) if wl == "c2" else rng.dirichlet(np.ones(K))
+    return C, prob
+
+
 def gen_rows(wl: str, n: int, row0: int, device, torch):
     """(n, p) fp32 rows of workload wl, seeded per 2^18-row chunk of the global index."""
     cfg = WORKLOADS[wl]
     p = cfg["p"]
     X = torch.empty((n, p), dtype=torch.float32, device=device)
     g = torch.Generator(device=device)
-    rng = np.random.default_rng(SEED)
-    if wl.startswith("c1"):
-        U = np.linalg.qr(rng.standard_normal((p, 5)))[0]
-        lam = np.array([50.0, 40.0, 30.0, 20.0, 10.0])
-    elif wl == "c3":
-        U = np.linalg.qr(rng.standard_normal((p, 10)))[0]
-        lam = np.arange(100.0, 9.0, -10.0)
-    elif wl == "c4":
-        U = np.linalg.qr(rng.standard_normal((p, 20)))[0]
-        lam = np.linspace(20.0, 1.0, 20)
+    A, lam = _model(wl, np.random.default_rng(SEED))
+    kmeans = wl in ("c2", "c5")
+    if kmeans:
+        Ct = torch.as_tensor(A.T.copy(), dtype=torch.float32, device=device)
+        cdf = torch.as_tensor(np.cumsum(lam), dtype=torch.float64, device=device)
     else:
-        K = cfg["K"]
-        C = rng.standard_normal((p, K)) * (2.0 if wl == "c2" else 3.0)
-        if wl == "c2":
-            prob = np.full(K, 1.0 / K)
-        else:
-            prob = rng.dirichlet(np.ones(K))
-        Ct = torch.as_tensor(C.T.copy(), dtype=torch.float32, device=device)
-        cdf = torch.as_tensor(np.cumsum(prob), dtype=torch.float64, device=device)
-    if not wl.startswith("c2") and not wl.startswith("c5"):
-        B = torch.as_tensor((U * np.sqrt(lam)[None, :]).T.copy(), dtype=torch.float32, device=device)
+        B = torch.as_tensor((A * np.sqrt(lam)[None, :]).T.copy(), dtype=torch.float32, device=device)
     CH = 1 << 18
     for c0 in range(0, n, CH):
         c = min(CH, n - c0)
         g.manual_seed(SEED * 1000003 + (row0 + c0) // CH)
-        if wl in ("c2", "c5"):
+        if kmeans:
             u = torch.rand(c, generator=g, device=device, dtype=torch.float64)
             lab = torch.searchsorted(cdf, u).clamp_(max=cfg["K"] - 1)
             X[c0 : c0 + c] = Ct[lab] + torch.randn((c, p), generator=g, device=device)
@@ -118,6 +126,27 @@ def gen_rows(wl: str, n: int, row0: int, device, torch):
             sig += torch.randn((c, p), generator=g, device=device)
         X[c0 : c0 + c] = sig
     return X
+
+
+def gen_rows_np(wl: str, n: int, seed: int = SEED) -> np.ndarray:
+    """The same generative model in numpy (the reference arm uses no GPU)."""
+    cfg = WORKLOADS[wl]
+    p = cfg["p"]
+    rng = np.random.default_rng(seed)
+    A, lam = _model(wl, np.random.default_rng(SEED))
+    if wl in ("c2", "c5"):
+        lab = np.minimum(np.searchsorted(np.cumsum(lam), rng.random(n)), cfg["K"] - 1)
+        return (A.T[lab] + rng.standard_normal((n, p))).astype(np.float32)
+    X = rng.standard_normal((n, len(lam))) @ (A * np.sqrt(lam)[None, :]).T
+    if wl == "c3":
+        X += rng.standard_normal((n, p)) / np.sqrt(rng.chisquare(3, (n, p)))
+    elif wl == "c4":
+        X += 0.1 * rng.standard_normal((n, p))
+        rows = np.repeat(np.arange(n), 8)
+        X[rows, rng.integers(0, p, n * 8)] = rng.choice([-50.0, 50.0], n * 8)
+    else:
+        X += rng.standard_normal((n, p))
+    return X.astype(np.float32)
 
 
 # ------------------------------------------------------------------ clocks
@@ -159,7 +188,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(busy)}
 
 
-# ------------------------------------------------------------------ CPU baseline (oracle port)
+# ------------------------------------------------------------------ CPU legs (oracle port)
 def cpu_cov_rate(rows: np.ndarray, cfg, nthreads: int, min_seconds: float = 10.0):
     """The oracle port (oracle/, C, all host threads) on a bounded row sample: samples/s."""
     from oracle import oracle as O
@@ -178,6 +207,7 @@ def cpu_cov_rate(rows: np.ndarray, cfg, nthreads: int, min_seconds: float = 10.0
 
 
 def cpu_kmeans_rate(rows: np.ndarray, cfg, nthreads: int, min_seconds: float = 10.0):
+    """The oracle port's Lloyd iteration (assign + update) on a bounded sample: point-iters/s."""
     from oracle import oracle as O
 
     p, m, K = cfg["p"], cfg["m"], cfg["K"]
@@ -187,7 +217,7 @@ def cpu_kmeans_rate(rows: np.ndarray, cfg, nthreads: int, min_seconds: float = 1
     mu = O.init_centers(idx, val, chosen, p)
     pts, t0 = 0, time.perf_counter()
     while True:
-        labels, d2 = O.kmeans_assign(idx, val, mu, nthreads)
+        labels, _ = O.kmeans_assign(idx, val, mu, nthreads)
         mu, _, _ = O.kmeans_update(idx, val, labels, mu)
         pts += rows.shape[0]
         el = time.perf_counter() - t0
@@ -195,12 +225,115 @@ def cpu_kmeans_rate(rows: np.ndarray, cfg, nthreads: int, min_seconds: float = 1
             return pts / el, el
 
 
-# ------------------------------------------------------------------ reference arm
+def cpu_baseline(wl: str, cfg, seconds: float = 10.0, rows: np.ndarray = None):
+    nthreads = os.cpu_count() or 1
+    sample = min(cfg["n"], 1 << 16)
+    if rows is None:
+        rows = gen_rows_np(wl, sample)
+    if cfg["kind"] == "cov":
+        rate, el = cpu_cov_rate(rows, cfg, nthreads, seconds)
+        unit = "samples/s"
+    else:
+        rate, el = cpu_kmeans_rate(rows, cfg, nthreads, seconds)
+        unit = "point-iters/s"
+    return {"value": rate, "unit": unit, "cores": nthreads, "kind": "port",
+            "sample": f"{rows.shape[0]} rows of {wl} (same generative model), repeated for {el:.1f} s"}
+
+
+# ------------------------------------------------------------------ the reference package itself
+def _ref_import():
+    if REF_PATH not in sys.path:
+        sys.path.insert(0, REF_PATH)
+    import sketchpipe  # noqa: F401  (baseline/_ref: pip install --target of /root/reference/pkg)
+
+    return sketchpipe
+
+
+def _ref_shard_worker(args):
+    """One process of the sharded reference run: its column range with GLOBAL offsets
+    (sketch.py:211-220 primitives), then its partial W W^T (estimators.py:59-61)."""
+    wl, g0, g1, seconds = args
+    sp = _ref_import()
+    from sketchpipe.sketch import SparseSketch
+    from sketchpipe.transform import precondition_columns
+
+    cfg = WORKLOADS[wl]
+    spec = sp.PreconditionSpec.create("hadamard", cfg["p"], sign_seed=derive_seed(SEED, 0xD5))
+    plan = sp.SamplingPlan(derive_seed(SEED, 0x5A), spec.p_pad, cfg["m"])
+    X = gen_rows_np(wl, g1 - g0, seed=SEED + g0).T.astype(np.float64)
+    done, t0 = 0, time.perf_counter()
+    while True:
+        Y = precondition_columns(X, spec)
+        idx = plan.indices_block(g0, g1)
+        val = np.take_along_axis(Y.T, idx.astype(np.int64), axis=1)
+        W = SparseSketch(spec=spec, n=g1 - g0, indices=idx, values=val, plan=plan).to_csc()
+        (W @ W.T).toarray()
+        np.bincount(idx.ravel(), weights=val.ravel(), minlength=spec.p_pad)
+        done += g1 - g0
+        if time.perf_counter() - t0 >= seconds:
+            return done, time.perf_counter() - t0
+
+
+def python_reference(wl: str, cfg, seconds: float = 12.0):
+    """sketchpipe itself: (i) one process through its public API,
+    (ii) one process per host core on global column ranges."""
+    try:
+        sp = _ref_import()
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": f"baseline/_ref not importable: {e}"}
+    out = {"package": "sketchpipe (baseline/_ref, unmodified)"}
+    p, m = cfg["p"], cfg["m"]
+    spec = sp.PreconditionSpec.create("hadamard", p, sign_seed=derive_seed(SEED, 0xD5))
+    plan = sp.SamplingPlan(derive_seed(SEED, 0x5A), spec.p_pad, m)
+    ns = min(cfg["n"], 8192 if p >= 2048 else 16384)
+    X = gen_rows_np(wl, ns).T.astype(np.float64)
+    if cfg["kind"] == "cov":
+        done, t0 = 0, time.perf_counter()
+        while True:
+            sk = sp.sketch_stream(sp.ArraySource(X), spec, plan)
+            sp.estimate_covariance(sk)
+            sp.estimate_mean(sk)
+            done += ns
+            if time.perf_counter() - t0 >= seconds:
+                break
+        el = time.perf_counter() - t0
+        out["single_process"] = {"value": done / el, "unit": "samples/s", "cores": 1,
+                                 "sample": f"{ns} columns, sketch_stream + estimate_covariance + estimate_mean"}
+        procs = os.cpu_count() or 1
+        import multiprocessing as mpc
+
+        per = max(1024, ns // 2)
+        ctx = mpc.get_context("fork")
+        with ctx.Pool(procs) as pool:
+            res = pool.map(_ref_shard_worker, [(wl, r * per, (r + 1) * per, seconds) for r in range(procs)])
+        el = max(r[1] for r in res)
+        out["multi_process"] = {"value": sum(r[0] for r in res) / el, "unit": "samples/s", "cores": procs,
+                                "sample": f"{procs} processes x {per} columns (global offsets), "
+                                          "precondition_columns + indices_block + gather + W W^T"}
+    else:
+        from sketchpipe.cluster import _SparseOps
+
+        sk = sp.sketch_stream(sp.ArraySource(X), spec, plan)
+        ops = _SparseOps(sk)
+        K = cfg["K"]
+        mu = ops.init_centers(np.random.default_rng(SEED).choice(ns, K, replace=False))
+        pts, t0 = 0, time.perf_counter()
+        while True:
+            labels, d2min = ops.assign(mu)
+            mu, empty = ops.update(labels, mu, K)
+            pts += ns
+            if time.perf_counter() - t0 >= seconds:
+                break
+        el = time.perf_counter() - t0
+        out["single_process"] = {"value": pts / el, "unit": "point-iters/s", "cores": 1,
+                                 "sample": f"{ns} points, _SparseOps assign + update (cluster.py:231-241)"}
+    return out
+
+
 def run_reference(args, cfg):
     nthreads = os.cpu_count() or 1
     sample = min(cfg["n"], 1 << 16 if cfg["p"] >= 1024 else 1 << 17)
-    rng = np.random.default_rng(SEED)
-    rows = rng.standard_normal((sample, cfg["p"])).astype(np.float32)
+    rows = gen_rows_np(args.workload, sample)
     per_step = []
     for i in range(args.warmup + args.steps):
         if cfg["kind"] == "cov":
@@ -212,27 +345,57 @@ def run_reference(args, cfg):
     value = statistics.median(per_step)
     unit = "samples/s" if cfg["kind"] == "cov" else "point-iters/s"
     desc = f"{sample} rows of {args.workload}, oracle port (C) with {nthreads} threads"
-    return {
+    out = {
         "impl": "reference", "metric": metric_name(cfg), "value": value, "unit": unit, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (numpy, same generative model)",
         "config": {"workload": args.workload, "desc": cfg["desc"], "p": cfg["p"], "m": cfg["m"]},
         "cpu_baseline": {"value": value, "unit": unit, "cores": nthreads, "kind": "port", "sample": desc},
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_python_ref:
+        out["python_reference"] = python_reference(args.workload, cfg)
+    return out
 
 
-def profiled_traffic(workload, n, stage):
-    """dram read+write bytes per launch of the stage's kernel, from the committed ncu capture
-    (profiles/<wl>_ncu_full.json, written by tools/ncu_summary.py) when it was taken at this
-    exact size, else None."""
-    names = {"indices": "indices_kernel", "gather": "gather_kernel", "covariance": "cov_band_kernel",
+# ------------------------------------------------------------------ our arm
+class Ctx:
+    def __init__(self, torch, tdist, skc, lib, sdist, dev, rank, world, local, hbm_peak, peak_src):
+        self.torch, self.tdist, self.skc, self.lib, self.sdist = torch, tdist, skc, lib, sdist
+        self.dev, self.rank, self.world, self.local = dev, rank, world, local
+        self.hbm_peak, self.peak_src = hbm_peak, peak_src
+        self.L = lib.lib()
+
+    def barrier(self):
+        if self.world > 1:
+            self.tdist.barrier()
+        self.torch.cuda.synchronize()
+
+    def max_over_ranks(self, v: float) -> float:
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.dev)
+        if self.world > 1:
+            self.tdist.all_reduce(t, op=self.tdist.ReduceOp.MAX)
+        return float(t.item())
+
+
+def shard(cfg, ctx, scaling):
+    if scaling == "weak":
+        return cfg["n"], ctx.rank * cfg["n"], cfg["n"] * ctx.world
+    c0, c1 = ctx.sdist.shard_bounds(cfg["n"], ctx.rank, ctx.world)
+    return c1 - c0, c0, cfg["n"]
+
+
+def profiled_traffic(workload, n, stage, compute):
+    """dram read+write bytes per launch of the stage's kernel from the committed ncu capture
+    (profiles/<wl>_ncu_full.json, tools/ncu_summary.py) when it was taken at this size and
+    compute type, else None."""
+    names = {"indices": "indices_kernel", "gather": "gtma::gather_tma_kernel", "covariance": "cov_band_kernel",
              "moments": "moments_kernel"}
     path = os.path.join(ROOT, "profiles", f"{workload}_ncu_full.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        if f"n=2^{int(np.log2(n))}" not in d["config"] or (1 << int(np.log2(n))) != n:
+        if f"n=2^{int(np.log2(n))}" not in d["config"] or (1 << int(np.log2(n))) != n or compute not in d["config"]:
             return None
         for k, v in d["kernels"].items():
             if k.startswith(names.get(stage, "?")):
@@ -242,38 +405,236 @@ def profiled_traffic(workload, n, stage):
     return None
 
 
-def kmeans_secondary(wl, dev, torch, skc, hbm_peak, runs=2):
-    """The Lloyd loop of a K-means config (sketch HBM-resident, seeded initial points), device-timed."""
-    c = WORKLOADS[wl]
-    X = gen_rows(wl, c["n"], 0, dev, torch)
-    spec = skc.PreconditionSpec.create("hadamard", c["p"], sign_seed=derive_seed(SEED, 0xD5))
-    plan = skc.SamplingPlan(derive_seed(SEED, 0x5A), spec.p_pad, c["m"])
-    sk = skc.sketch_stream(skc.RowSource(X), spec, plan, compute="f64")
+def cov_line(ctx, wl, args, steps, warmup, compute, sampler="oracle", clocks=True):
+    """HBM-resident covariance pass (K1a..K4), stage-timed with CUDA events on the stream."""
+    torch, skc, lib = ctx.torch, ctx.skc, ctx.lib
+    cfg = WORKLOADS[wl]
+    n, col0, n_glob = shard(cfg, ctx, args.scaling)
+    p, m = cfg["p"], cfg["m"]
+    X = gen_rows(wl, n, col0, ctx.dev, torch)
+    spec = skc.PreconditionSpec.create("hadamard", p, sign_seed=derive_seed(SEED, 0xD5))
+    plan = skc.SamplingPlan(derive_seed(SEED, 0x5A), spec.p_pad, m)
+    vcode = lib.F32 if compute == "f32" else lib.F64
+    vdt = torch.float32 if compute == "f32" else torch.float64
+    idx = torch.empty((n, m), dtype=torch.int32, device=ctx.dev)
+    val = torch.empty((n, m), dtype=vdt, device=ctx.dev)
+    mom = skc.estimators.Moments.zeros(p, True, ctx.dev)
+    C = torch.empty((p, p), dtype=torch.float64, device=ctx.dev)
+    L = ctx.L
+    ws1 = lib.workspace(L.skc_moments_workspace(n, m, p), ctx.dev)
+    ws2 = lib.workspace(L.skc_cov_workspace(n, m, p), ctx.dev)
+    st = lib.stream_ptr(ctx.dev)
+    names = ["indices", "gather", "moments", "covariance", "combine+finalize"]
+
+    def step(ev):
+        mom.packed.zero_()
+        ev[0].record()
+        if sampler == "philox":
+            lib.call("skc_indices_philox", plan.master_seed, col0, n, p, m, idx.data_ptr(), st)
+        else:
+            lib.call("skc_indices", plan.master_seed, col0, n, p, m, idx.data_ptr(), st)
+        ev[1].record()
+        lib.call("skc_sketch_given", X.data_ptr(), lib.F32, p, n, p, p, 0, spec.sign_seed, m, vcode,
+                 idx.data_ptr(), val.data_ptr(), vcode, st)
+        ev[2].record()
+        lib.call("skc_moments", idx.data_ptr(), val.data_ptr(), vcode, n, m, p, mom.acc.data_ptr(),
+                 mom.stats.data_ptr(), ws1.data_ptr(), ws1.numel(), st)
+        ev[3].record()
+        lib.call("skc_cov_accumulate", idx.data_ptr(), val.data_ptr(), vcode, n, m, p, mom.stats.data_ptr(),
+                 mom.tri.data_ptr(), ws2.data_ptr(), ws2.numel(), st)
+        ev[4].record()
+        ctx.sdist.combine_moments(mom.acc, mom.stats, mom.tri, n, n_total=n_glob)  # one allreduce (N > 1)
+        lib.call("skc_cov_finalize", mom.tri.data_ptr(), p, m, n_glob, C.data_ptr(), st)
+        ev[5].record()
+
+    def mk():
+        return [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+
+    for _ in range(warmup):
+        step(mk())
+    ctx.barrier()
+    evs = [mk() for _ in range(steps)]
+    launches0 = L.skc_launch_count()
+    clk = ClockSampler(ctx.local) if clocks else None
+    if clk:
+        clk.__enter__()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    ctx.barrier()
+    t0.record()
+    for k in range(steps):
+        step(evs[k])
+    t1.record()
+    ctx.barrier()
+    if clk:
+        clk.__exit__()
+    launches = L.skc_launch_count() - launches0
+    ms_step = ctx.max_over_ranks(t0.elapsed_time(t1) / steps)
+    stage_ms = {nm: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / steps for i, nm in enumerate(names)}
+    vsz = 4 if compute == "f32" else 8
+    # algorithmic bytes per sample: indices write idx; gather reads the row and idx, writes values
+    unit_bytes = {"indices": 4 * m, "gather": 4 * p + 4 * m + vsz * m, "moments": (4 + vsz) * m,
+                  "covariance": (4 + vsz) * m, "combine+finalize": 0}
+    dom = max(("indices", "gather", "moments", "covariance"), key=lambda k: stage_ms[k])
+    dom_bytes = unit_bytes[dom] * n
+    achieved = dom_bytes / (stage_ms[dom] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": ctx.hbm_peak, "unit": "GB/s",
+                "frac": achieved / ctx.hbm_peak, "traffic": profiled_traffic(wl, n, dom, compute),
+                "peak_source": ctx.peak_src, "algorithmic_bytes_per_launch": dom_bytes,
+                "bytes_per_sample": {k: v for k, v in unit_bytes.items() if v}}
+    per_stage = {k: {"ms": stage_ms[k], "algorithmic_GBps": unit_bytes[k] * n / (stage_ms[k] * 1e-3) / 1e9,
+                     "frac_hbm": unit_bytes[k] * n / (stage_ms[k] * 1e-3) / 1e9 / ctx.hbm_peak}
+                 for k in unit_bytes if unit_bytes[k] > 0 and stage_ms[k] > 0}
+    upd = n * m * (m + 1) / 2 / (stage_ms["covariance"] * 1e-3)
+    per_stage["covariance"]["pair_updates_per_s"] = upd
+    per_stage["covariance"]["frac_of_measured_smem_atomic_peak"] = upd / 1.355e12  # tools/microbench/mb_dsmem
+    roofline["stages"] = per_stage
+    roofline["pass_frac_hbm"] = (4 * p + (4 + vsz) * m) * (n / (ms_step * 1e-3)) / 1e9 / ctx.hbm_peak
+    out = {"metric": metric_name(cfg), "value": n_glob / (ms_step * 1e-3), "unit": "samples/s",
+           "ms_per_step": ms_step, "dtype": compute, "stages_ms": stage_ms, "roofline": roofline,
+           "gpu_launches": int(launches), "rows_per_gpu": n, "global_rows": n_glob}
+    if clk:
+        out["clocks"] = clk.summary()
+    if cfg.get("pcs"):
+        # the host eigensolve of the PCA configs (north_star: handed back to the host), reported apart
+        Ch = C.cpu().numpy()
+        t = time.perf_counter()
+        skc.top_eigenvectors(Ch, cfg["pcs"])
+        out["host_eigensolve_ms"] = (time.perf_counter() - t) * 1e3
+    del X, idx, val
+    torch.cuda.empty_cache()
+    return out
+
+
+def pinned_rows(ctx, wl, n, col0):
+    torch = ctx.torch
+    host = torch.empty((n, WORKLOADS[wl]["p"]), dtype=torch.float32, pin_memory=True)
+    CH = 1 << 20
+    for r in range(0, n, CH):
+        c = min(CH, n - r)
+        host[r : r + c].copy_(gen_rows(wl, c, col0 + r, ctx.dev, torch))
+    return host
+
+
+def cov_e2e(ctx, wl, args, compute, reps=3):
+    """The same metric through the public API from pinned host rows: stream_moments (the
+    native chunk loop, H2D of chunk k+1 overlapped with chunk k's kernels), one allreduce,
+    covariance_from_moments, D2H of the p x p result, timed on the host wall clock."""
+    skc = ctx.skc
+    cfg = WORKLOADS[wl]
+    n, col0, n_glob = shard(cfg, ctx, args.scaling)
+    p, m = cfg["p"], cfg["m"]
+    spec = skc.PreconditionSpec.create("hadamard", p, sign_seed=derive_seed(SEED, 0xD5))
+    plan = skc.SamplingPlan(derive_seed(SEED, 0x5A), spec.p_pad, m)
+    host = pinned_rows(ctx, wl, n, col0)
+    src = skc.RowSource(host, chunk_cols=1 << 16)
+
+    def one():
+        mom = skc.stream_moments(src, spec, plan, compute=compute, col0=col0)
+        ctx.sdist.combine_moments(mom.acc, mom.stats, mom.tri, mom.n, n_total=n_glob)
+        return skc.covariance_from_moments(mom, p, m, n_glob).cpu().numpy()
+
+    one()
+    ctx.barrier()
+    w0 = time.perf_counter()
+    for _ in range(reps):
+        one()
+    ctx.barrier()
+    e_ms = ctx.max_over_ranks((time.perf_counter() - w0) * 1e3 / reps)
+    del host
+    return {"value": n_glob / (e_ms * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": n * p * 4,
+            "d2h_bytes_per_step": p * p * 8, "ms_per_step": e_ms, "rows_per_gpu": n, "compute": compute,
+            "api": "stream_moments(RowSource(pinned host rows)) + combine_moments + covariance_from_moments "
+                   "-> host (p, p): per-chunk sketch, moments and covariance overlapped with the next chunk's H2D"}
+
+
+def kmeans_line(ctx, wl, args, steps, warmup, clocks=True):
+    """Lloyd loop on the HBM-resident f64 sketch (reference arithmetic, bit-exact labels)."""
+    torch, skc = ctx.torch, ctx.skc
+    cfg = WORKLOADS[wl]
+    n, col0, n_glob = shard(cfg, ctx, args.scaling)
+    p, m, K = cfg["p"], cfg["m"], cfg["K"]
+    X = gen_rows(wl, n, col0, ctx.dev, torch)
+    spec = skc.PreconditionSpec.create("hadamard", p, sign_seed=derive_seed(SEED, 0xD5))
+    plan = skc.SamplingPlan(derive_seed(SEED, 0x5A), spec.p_pad, m)
+    sk = skc.sketch_stream(skc.RowSource(X), spec, plan, compute="f64", col0=col0)
     del X
     torch.cuda.empty_cache()
     ops = skc.SketchKMeans(sk)
-    mu0 = ops.init_centers(np.random.default_rng(SEED).choice(c["n"], c["K"], replace=False))
-    ops.lloyd(mu0, c["iters"])  # warm-up: builds the transposed sketch and the tensor-core entries
-    its, el = 0, 0.0
-    for _ in range(runs):
-        _, _, _, it_done, secs = ops.lloyd(mu0, c["iters"])
-        its += it_done
-        el += secs
-    rate = c["n"] * its / el
-    gbs = (8 * c["m"] + 4) * rate / 1e9  # algorithmic bytes per point-iteration: the sketch row + a label
-    return {"metric": "K-means point-iters/s", "value": rate, "iterations_per_run": its / runs,
-            "ms_per_run": el * 1e3 / runs, "desc": c["desc"],
-            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak},
-            "note": "Lloyd loop on the HBM-resident f64 sketch, exact reference arithmetic (bit-identical labels)"}
+    chosen = np.random.default_rng(SEED).choice(n_glob, K, replace=False)  # global seeded points
+    mu0 = ctx.sdist.init_centers_global(ops, chosen)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    ops.prepare(K)  # once per sketch: transposed lists (+ tensor-core entries), reported apart
+    torch.cuda.synchronize()
+    prep_ms = ctx.max_over_ranks((time.perf_counter() - t) * 1e3)
+    for _ in range(warmup):
+        ops.lloyd(mu0, cfg["iters"])
+    ctx.barrier()
+    L = ctx.L
+    launches0 = L.skc_launch_count()
+    clk = ClockSampler(ctx.local) if clocks else None
+    if clk:
+        clk.__enter__()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    ctx.barrier()
+    t0.record()
+    its = 0
+    for _ in range(steps):
+        its += ops.lloyd(mu0, cfg["iters"])[3]
+    t1.record()
+    ctx.barrier()
+    if clk:
+        clk.__exit__()
+    launches = L.skc_launch_count() - launches0
+    ms_step = ctx.max_over_ranks(t0.elapsed_time(t1) / steps)
+    it_step = its / steps
+    rate = n_glob * it_step / (ms_step * 1e-3)
+    ub = 12 * m + 4  # f64 sketch row (idx + value) + a label, per point-iteration
+    gbs = ub * n * it_step / (ms_step * 1e-3) / 1e9
+    out = {"metric": metric_name(cfg), "value": rate, "unit": "point-iters/s", "ms_per_step": ms_step,
+           "iterations_per_step": it_step, "dtype": "f64", "prep_ms": prep_ms, "gpu_launches": int(launches),
+           "rows_per_gpu": n, "global_rows": n_glob,
+           "roofline": {"bound": "hbm", "kernel": "lloyd iteration (assign + partials + centres)",
+                        "achieved": gbs, "peak": ctx.hbm_peak, "unit": "GB/s", "frac": gbs / ctx.hbm_peak,
+                        "traffic": None, "peak_source": ctx.peak_src, "bytes_per_point_iter": ub}}
+    if clk:
+        out["clocks"] = clk.summary()
+    del sk, ops
+    torch.cuda.empty_cache()
+    return out
 
 
-def metric_name(cfg):
-    if cfg["kind"] == "cov":
-        return "samples/s precondition+sparsify+covariance"
-    return "K-means point-iters/s"
+def kmeans_e2e(ctx, wl, args, reps=1):
+    """sparsified_kmeans(pinned host rows, init=seeded points) -> host labels and centres (N=1)."""
+    torch, skc = ctx.torch, ctx.skc
+    cfg = WORKLOADS[wl]
+    n, p, m, K = cfg["n"], cfg["p"], cfg["m"], cfg["K"]
+    host = pinned_rows(ctx, wl, n, 0)
+    chosen = np.random.default_rng(SEED).choice(n, K, replace=False)
+    src = skc.RowSource(host, chunk_cols=1 << 16)
+    gamma = m / p
+
+    def one():
+        r = skc.sparsified_kmeans(src, K, gamma, max_iter=cfg["iters"], seed=SEED, init=chosen)
+        return r.diagnostics["iterations"]
+
+    one()
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    its = 0
+    for _ in range(reps):
+        its += one()
+    el = time.perf_counter() - w0
+    del host
+    return {"value": n * its / el, "unit": "point-iters/s", "h2d_bytes_per_step": n * p * 4,
+            "d2h_bytes_per_step": n * 8 + p * K * 8, "ms_per_step": el * 1e3 / reps,
+            "iterations_per_step": its / reps,
+            "api": "sparsified_kmeans(RowSource(pinned host rows), K, gamma, init=seeded points): H2D + sketch + "
+                   "Lloyd loop + host labels and centres"}
 
 
-# ------------------------------------------------------------------ our arm
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -281,19 +642,20 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=None, help="override rows per GPU")
+    ap.add_argument("--n", type=int, default=None, help="override the whole-job row count")
     ap.add_argument("--compute", default="f64", choices=["f32", "f64"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--sampler", default="oracle", choices=["oracle", "philox"],
                     help="oracle: the reference's index rule (bit-exact, headline); philox: north_star's Philox sampler")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-kmeans", action="store_true")
-    ap.add_argument("--no-philox", action="store_true", help="skip the Philox-sampler secondary measurement")
-    ap.add_argument("--no-c5", action="store_true", help="skip the C5 K-means secondary measurement")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config lines of the other workloads")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the philox / f32 secondaries")
+    ap.add_argument("--no-python-ref", action="store_true")
     args = ap.parse_args()
-    cfg = dict(WORKLOADS[args.workload])
     if args.n:
-        cfg["n"] = args.n
+        WORKLOADS[args.workload]["n"] = args.n
+    cfg = dict(WORKLOADS[args.workload])
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -316,277 +678,65 @@ def main():
     from paper_1511_00152_b200 import _lib
     from paper_1511_00152_b200 import dist as sdist
 
-    L = _lib.lib()
     hbm_peak, peak_src = peaks()
-    n = cfg["n"]
-    p, m = cfg["p"], cfg["m"]
-    col0 = rank * n
-    X = gen_rows(args.workload, n, col0, dev, torch)
-    spec = skc.PreconditionSpec.create("hadamard", p, sign_seed=derive_seed(SEED, 0xD5))
-    plan = skc.SamplingPlan(derive_seed(SEED, 0x5A), spec.p_pad, m)
-    torch.cuda.synchronize()
-
-    def barrier():
-        if world > 1:
-            tdist.barrier()
-        torch.cuda.synchronize()
-
-    stage_names, stage_ms = [], {}
-    result = {}
+    ctx = Ctx(torch, tdist, skc, _lib, sdist, dev, rank, world, local, hbm_peak, peak_src)
+    wl = args.workload
     if cfg["kind"] == "cov":
-        vcode = _lib.F32 if args.compute == "f32" else _lib.F64
-        vdt = torch.float32 if args.compute == "f32" else torch.float64
-        idx = torch.empty((n, m), dtype=torch.int32, device=dev)
-        val = torch.empty((n, m), dtype=vdt, device=dev)
-        acc = torch.zeros(p, dtype=torch.float64, device=dev)
-        stats = torch.zeros(3, dtype=torch.float64, device=dev)
-        tri = torch.zeros(p * (p + 1) // 2, dtype=torch.float64, device=dev)
-        C = torch.empty((p, p), dtype=torch.float64, device=dev)
-        ws1 = _lib.workspace(L.skc_moments_workspace(n, m, p), dev)
-        ws2 = _lib.workspace(L.skc_cov_workspace(n, m, p), dev)
-        st = _lib.stream_ptr(dev)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
-        # the sketch as its two kernels (what skc_sketch runs internally), timed apart so the
-        # roofline can name the dominant kernel: K1a indices (oracle keys or Philox), K1b gather
-        stage_names = ["indices", "gather", "moments", "covariance", "finalize"]
-        sampler = args.sampler
-
-        def step(record):
-            acc.zero_()
-            stats.zero_()
-            tri.zero_()
-            if record:
-                ev[0].record()
-            if sampler == "philox":
-                _lib.call("skc_indices_philox", plan.master_seed, col0, n, p, m, idx.data_ptr(), st)
-            else:
-                _lib.call("skc_indices", plan.master_seed, col0, n, p, m, idx.data_ptr(), st)
-            if record:
-                ev[1].record()
-            _lib.call("skc_sketch_given", X.data_ptr(), _lib.F32, p, n, p, p, 0, spec.sign_seed, m, vcode,
-                      idx.data_ptr(), val.data_ptr(), vcode, st)
-            if record:
-                ev[2].record()
-            _lib.call("skc_moments", idx.data_ptr(), val.data_ptr(), vcode, n, m, p, acc.data_ptr(), stats.data_ptr(),
-                      ws1.data_ptr(), ws1.numel(), st)
-            if record:
-                ev[3].record()
-            _lib.call("skc_cov_accumulate", idx.data_ptr(), val.data_ptr(), vcode, n, m, p, stats.data_ptr(),
-                      tri.data_ptr(), ws2.data_ptr(), ws2.numel(), st)
-            if record:
-                ev[4].record()
-            n_tot = sdist.combine_moments(acc, stats, tri, n)
-            _lib.call("skc_cov_finalize", tri.data_ptr(), p, m, n_tot, C.data_ptr(), st)
-            if record:
-                ev[5].record()
-
-        for _ in range(args.warmup):
-            step(False)
-        barrier()
-        launches0 = L.skc_launch_count()
-        sums = [0.0] * len(stage_names)
-        with ClockSampler(local) as clk:
-            t0 = torch.cuda.Event(enable_timing=True)
-            t1 = torch.cuda.Event(enable_timing=True)
-            barrier()
-            t0.record()
-            for _ in range(args.steps):
-                step(True)
-                torch.cuda.synchronize()
-                for i in range(len(stage_names)):
-                    sums[i] += ev[i].elapsed_time(ev[i + 1])
-            t1.record()
-            barrier()
-        launches = L.skc_launch_count() - launches0
-        ms_total = t0.elapsed_time(t1)
-        stage_ms = {k: sums[i] / args.steps for i, k in enumerate(stage_names)}
-        ms_step = ms_total / args.steps
-        vsz = 4 if args.compute == "f32" else 8
-        # algorithmic bytes per sample: indices write idx; gather reads the row and idx, writes values
-        unit_bytes = {"indices": 4 * m, "gather": 4 * p + 4 * m + vsz * m, "moments": (4 + vsz) * m,
-                      "covariance": (4 + vsz) * m, "finalize": 0}
-        total_samples = n * world
-        unit = "samples/s"
-        metric = metric_name(cfg)
-        work_units = total_samples
+        line = cov_line(ctx, wl, args, args.steps, args.warmup, args.compute, args.sampler)
     else:
-        K, iters_max = cfg["K"], cfg["iters"]
-        sk = skc.sketch_stream(skc.RowSource(X), spec, plan, compute="f64", col0=col0)
-        ops = skc.SketchKMeans(sk)
-        chosen = np.random.default_rng(SEED).choice(n, K, replace=False)
-        mu0 = ops.init_centers(chosen)  # seeded points of rank 0's shard, the same centres on every rank
-        if world > 1:
-            tdist.broadcast(mu0, src=0)
-        for _ in range(args.warmup):
-            ops.lloyd(mu0, iters_max)
-        barrier()
-        launches0 = L.skc_launch_count()
-        with ClockSampler(local) as clk:
-            t0 = torch.cuda.Event(enable_timing=True)
-            t1 = torch.cuda.Event(enable_timing=True)
-            barrier()
-            t0.record()
-            its = 0
-            for _ in range(args.steps):
-                _, _, _, it_done, _ = ops.lloyd(mu0, iters_max)
-                its += it_done
-            t1.record()
-            barrier()
-        launches = L.skc_launch_count() - launches0
-        ms_total = t0.elapsed_time(t1)
-        ms_step = ms_total / args.steps
-        stage_names = ["lloyd"]
-        stage_ms = {"lloyd": ms_step}
-        unit_bytes = {"lloyd": (8 * m + 4) * its / args.steps}
-        unit = "point-iters/s"
-        metric = metric_name(cfg)
-        work_units = n * world * its / args.steps
-        total_samples = n * world
-
-    # max over ranks
-    t = torch.tensor([ms_step], dtype=torch.float64, device=dev)
-    if world > 1:
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-    ms_step = float(t.item())
-    value = work_units / (ms_step * 1e-3)
-
-    # roofline of the dominant kernel (HBM; algorithmic bytes per launch / mean launch time)
-    dom = max(stage_ms, key=lambda k: stage_ms[k])
-    dom_bytes = unit_bytes[dom] * n
-    achieved = dom_bytes / (stage_ms[dom] * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": profiled_traffic(args.workload, n, dom), "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": dom_bytes}
-    if cfg["kind"] == "cov":
-        # every stage, and the pass as a whole, against the HBM roofline; K3's own bound is the
-        # shared-memory atomic rate (tools/microbench/mb_dsmem: 1.355e12 returning adds/s on this pool's B200)
-        per_stage = {k: {"algorithmic_GBps": unit_bytes[k] * n / (stage_ms[k] * 1e-3) / 1e9,
-                         "frac_hbm": unit_bytes[k] * n / (stage_ms[k] * 1e-3) / 1e9 / hbm_peak}
-                     for k in stage_ms if stage_ms[k] > 0 and unit_bytes[k] > 0}
-        upd = n * m * (m + 1) / 2 / (stage_ms["covariance"] * 1e-3)
-        per_stage["covariance"]["smem_atomic_updates_per_s"] = upd
-        per_stage["covariance"]["frac_of_measured_atoms_peak"] = upd / 1.355e12  # mb_dsmem: returning atom.shared
-        roofline["stages"] = per_stage
-        roofline["pass_frac_hbm"] = (4 * p + 8 * m) * (n / (ms_step * 1e-3)) / 1e9 / hbm_peak
-
-    out = {
-        "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": args.compute if cfg["kind"] == "cov" else "f64",
-        "data": "synthetic (seeded, device-generated; BASELINE.json generator shapes)",
-        "config": {"workload": args.workload, "desc": cfg["desc"], "p": p, "m": m, "rows_per_gpu": n,
-                   "sampler": args.sampler if cfg["kind"] == "cov" else "oracle",
-                   "global_rows": total_samples, "parallelism": f"dp{world}",
-                   "l2": "inputs larger than L2 (no flush needed)" if n * p * 4 > 126e6 else "inputs fit L2"},
-        "stages_ms": stage_ms,
-        "roofline": roofline,
-        "gpu_launches": int(launches),
-        "clocks": clk.summary(),
-    }
-
-    # secondary: the same pass with north_star's Philox sampler (not reference-identical
-    # indices; pinned to oracle/sketch_oracle.c:orc_philox_indices), same shapes and timing
-    if cfg["kind"] == "cov" and args.sampler == "oracle" and not args.no_philox:
-        sampler = "philox"
-        for _ in range(args.warmup):
-            step(False)
-        barrier()
-        psums = [0.0] * len(stage_names)
-        ksteps = max(1, min(args.steps, 5))
-        p0 = torch.cuda.Event(enable_timing=True)
-        p1 = torch.cuda.Event(enable_timing=True)
-        p0.record()
-        for _ in range(ksteps):
-            step(True)
-            torch.cuda.synchronize()
-            for i in range(len(stage_names)):
-                psums[i] += ev[i].elapsed_time(ev[i + 1])
-        p1.record()
-        barrier()
-        pms = torch.tensor([p0.elapsed_time(p1) / ksteps], dtype=torch.float64, device=dev)
-        if world > 1:
-            tdist.all_reduce(pms, op=tdist.ReduceOp.MAX)
-        out["philox_mode"] = {
-            "value": n * world / (float(pms.item()) * 1e-3), "unit": unit, "ms_per_step": float(pms.item()),
-            "stages_ms": {k: psums[i] / ksteps for i, k in enumerate(stage_names)},
-            "gather_frac_hbm": unit_bytes["gather"] * n / (psums[1] / ksteps * 1e-3) / 1e9 / hbm_peak,
-            "note": "skc_indices_philox + skc_sketch_given; uniform m-subsets, not the reference's subsets"}
-        sampler = args.sampler
-
-    # e2e through the public API with pinned host buffers
-    if cfg["kind"] == "cov" and not args.no_e2e:
-        n_e2e = min(n, 1 << 21)
-        host = torch.empty((n_e2e, p), dtype=torch.float32, pin_memory=True)
-        host.copy_(X[:n_e2e])
-        src = skc.RowSource(host, chunk_cols=1 << 13)  # 32 MB chunks: copy k+1 hides chunk k's kernels
-
-        def e2e_step():
-            mom = skc.stream_moments(src, spec, plan, compute=args.compute, col0=col0)
-            n_tot = sdist.combine_moments(mom.acc, mom.stats, mom.tri, mom.n)
-            Cm = skc.covariance_from_moments(mom, p, m, n_tot)
-            return Cm.cpu().numpy()
-
-        e2e_step()
-        barrier()
-        w0 = time.perf_counter()
-        for _ in range(max(1, min(args.steps, 3))):
-            e2e_step()
-        barrier()
-        e_ms = (time.perf_counter() - w0) * 1e3 / max(1, min(args.steps, 3))
-        te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-        if world > 1:
-            tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
-        e_ms = float(te.item())
-        out["e2e"] = {"value": n_e2e * world / (e_ms * 1e-3), "unit": unit, "h2d_bytes_per_step": n_e2e * p * 4,
-                      "d2h_bytes_per_step": p * p * 8, "rows_per_gpu": n_e2e,
-                      "api": "stream_moments(RowSource(pinned host)) + covariance_from_moments: per-chunk sketch, "
-                             "moments and covariance overlapped with the next chunk's H2D copy"}
-        del host
-    elif cfg["kind"] == "kmeans":
-        out["e2e"] = {"value": None, "unit": unit, "note": "K-means e2e not measured in this mode"}
-
-    # secondary: K-means C2 on the same box (rank 0 only, N=1)
-    if cfg["kind"] == "cov" and not args.no_kmeans and world == 1 and args.workload == "c3":
-        del X
-        torch.cuda.empty_cache()
-        c2 = WORKLOADS["c2"]
-        X2 = gen_rows("c2", c2["n"], 0, dev, torch)
-        spec2 = skc.PreconditionSpec.create("hadamard", c2["p"], sign_seed=derive_seed(SEED, 0xD5))
-        plan2 = skc.SamplingPlan(derive_seed(SEED, 0x5A), spec2.p_pad, c2["m"])
-        sk2 = skc.sketch_stream(skc.RowSource(X2), spec2, plan2, compute="f64")
-        ops = skc.SketchKMeans(sk2)
-        mu0 = ops.init_centers(np.random.default_rng(SEED).choice(c2["n"], c2["K"], replace=False))
-        ops.lloyd(mu0, c2["iters"])
-        torch.cuda.synchronize()
-        reps = 5
-        its, el = 0, 0.0
-        for _ in range(reps):  # device time of each run (CUDA events inside the Lloyd loop)
-            _, _, _, it_done, secs = ops.lloyd(mu0, c2["iters"])
-            its += it_done
-            el += secs
-        out["kmeans_c2"] = {"metric": "K-means point-iters/s", "value": c2["n"] * its / el,
-                            "iterations_per_run": its / reps, "ms_per_run": el * 1e3 / reps,
-                            "note": "Lloyd loop on the HBM-resident f64 sketch, exact reference arithmetic"}
-        if rank == 0 and not args.no_cpu:
-            rows2 = X2[: 1 << 16].cpu().numpy()
-            r, el2 = cpu_kmeans_rate(rows2, c2, os.cpu_count() or 1, min_seconds=5.0)
-            out["kmeans_c2"]["cpu_baseline"] = {"value": r, "unit": "point-iters/s", "cores": os.cpu_count(),
-                                                "kind": "port", "sample": "65536 C2 rows"}
-        del X2, sk2, ops
-        torch.cuda.empty_cache()
-        if not args.no_c5:
-            out["kmeans_c5"] = kmeans_secondary("c5", dev, torch, skc, hbm_peak)
-
-    if rank == 0 and world == 1 and not args.no_cpu:
-        sample_rows = 1 << 16
-        Xs = gen_rows(args.workload, sample_rows, 0, dev, torch).cpu().numpy()
-        nthreads = os.cpu_count() or 1
+        line = kmeans_line(ctx, wl, args, args.steps, args.warmup)
+    out = {"metric": line["metric"], "value": line["value"], "unit": line["unit"], "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": line["ms_per_step"], "higher_is_better": True,
+           "scaling": args.scaling, "vs_baseline": None, "dtype": line["dtype"],
+           "data": "synthetic (seeded, device-generated; BASELINE.json generator shapes)",
+           "config": {"workload": wl, "desc": cfg["desc"], "p": cfg["p"], "m": cfg["m"],
+                      "rows_per_gpu": line["rows_per_gpu"], "global_rows": line["global_rows"],
+                      "sampler": args.sampler, "parallelism": f"dp{world}",
+                      "l2": "inputs larger than L2 (no flush needed)" if line["rows_per_gpu"] * cfg["p"] * 4 > 126e6
+                      else "inputs fit L2"}}
+    for k in ("stages_ms", "roofline", "gpu_launches", "clocks", "prep_ms", "iterations_per_step",
+              "host_eigensolve_ms"):
+        if k in line:
+            out[k] = line[k]
+    if cfg["kind"] == "cov" and not args.no_secondary:
+        # north_star's Philox sampler and the f32 fast path, same shapes and timing (not bit-exact
+        # to the reference: uniform m-subsets / fp32 values; pinned to their own oracles)
+        ph = cov_line(ctx, wl, args, max(1, min(args.steps, 5)), 1, args.compute, "philox", clocks=False)
+        out["philox_mode"] = {k: ph[k] for k in ("value", "unit", "ms_per_step", "stages_ms")}
+        f32 = cov_line(ctx, wl, args, max(1, min(args.steps, 5)), 1, "f32", args.sampler, clocks=False)
+        out["fast_mode_f32"] = {k: f32[k] for k in ("value", "unit", "ms_per_step", "stages_ms")}
+        out["fast_mode_f32"]["gather_frac_hbm"] = f32["roofline"]["stages"]["gather"]["frac_hbm"]
+    if not args.no_e2e:
         if cfg["kind"] == "cov":
-            rate, el = cpu_cov_rate(Xs, cfg, nthreads, min_seconds=10.0)
+            out["e2e"] = cov_e2e(ctx, wl, args, args.compute)
+        elif world == 1:
+            out["e2e"] = kmeans_e2e(ctx, wl, args)
         else:
-            rate, el = cpu_kmeans_rate(Xs, cfg, nthreads, min_seconds=10.0)
-        out["cpu_baseline"] = {"value": rate, "unit": unit, "cores": nthreads, "kind": "port",
-                               "sample": f"{sample_rows} rows of {args.workload}, repeated for {el:.1f}s"}
+            out["e2e"] = {"value": None, "unit": line["unit"], "note": "K-means e2e is measured at N=1"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(wl, cfg)
+
+    # the other BASELINE configs, one line each (N=1 default run)
+    if world == 1 and wl == "c3" and not args.no_configs:
+        out["configs"] = {}
+        for other in ("c1", "c2", "c4", "c5"):
+            oc = WORKLOADS[other]
+            try:
+                if oc["kind"] == "cov":
+                    ln = cov_line(ctx, other, args, args.steps, args.warmup, args.compute, "oracle", clocks=False)
+                    if not args.no_e2e:
+                        ln["e2e"] = cov_e2e(ctx, other, args, args.compute)
+                else:
+                    ln = kmeans_line(ctx, other, args, max(2, args.steps // 2), 1, clocks=False)
+                    if not args.no_e2e:
+                        ln["e2e"] = kmeans_e2e(ctx, other, args)
+                if not args.no_cpu:
+                    ln["cpu_baseline"] = cpu_baseline(other, oc, seconds=5.0)
+                ln["config"] = {"workload": other, "desc": oc["desc"], "p": oc["p"], "m": oc["m"], "n": oc["n"]}
+                out["configs"][other] = ln
+            except Exception as e:  # noqa: BLE001  (one config failing must not lose the headline)
+                out["configs"][other] = {"error": f"{type(e).__name__}: {e}"}
+            torch.cuda.empty_cache()
 
     if rank == 0:
         print(json.dumps(out), flush=True)

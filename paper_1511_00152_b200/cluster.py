@@ -118,6 +118,35 @@ class SketchKMeans:
         L = _lib.lib()
         return self.p * K * 16 > 40 * 1024 and K > 16 and L.skc_kmeans_tc_supported(self.p, K, self.m) == 1
 
+    def _tcprep(self) -> torch.Tensor:
+        """Once per sketch: the compact bf16 entries and row norms of the tensor-core filter."""
+        if "tcprep" not in self._ws:
+            L = _lib.lib()
+            prep = _lib.workspace(L.skc_kmeans_tc_prepare_workspace(self.n, self.m, self.p), self.dev)
+            with torch.cuda.device(self.dev):
+                _lib.call("skc_kmeans_tc_prepare", self.idx.data_ptr(), self.val.data_ptr(), self.vcode, self.n,
+                          self.m, self.p, prep.data_ptr(), prep.numel(), self._st())
+            self._ws["tcprep"] = prep
+        return self._ws["tcprep"]
+
+    def _csc(self) -> torch.Tensor:
+        """Once per sketch: per-coordinate lists ascending in point index (skc_kmeans_build_csc)."""
+        if "csc" not in self._ws:
+            L = _lib.lib()
+            csc = _lib.workspace(L.skc_kmeans_csc_workspace(self.n, self.m, self.p, self.vcode), self.dev)
+            with torch.cuda.device(self.dev):
+                _lib.call("skc_kmeans_build_csc", self.idx.data_ptr(), self.val.data_ptr(), self.vcode, self.n,
+                          self.m, self.p, csc.data_ptr(), csc.numel(), self._st())
+            self._ws["csc"] = csc
+        return self._ws["csc"]
+
+    def prepare(self, K: int) -> None:
+        """Build the once-per-sketch structures the Lloyd iterations reuse (the transposed sketch,
+        and for large centre tables the tensor-core entries), so they stay out of iteration timing."""
+        self._csc()
+        if self._use_tc(K):
+            self._tcprep()
+
     def assign(self, mu: torch.Tensor, prev: Optional[torch.Tensor], labels: torch.Tensor, d2min: torch.Tensor,
                out: torch.Tensor, d2max: torch.Tensor) -> None:
         """cluster.py:181-187 (+ changed count vs prev, first argmax of d2min)"""
@@ -126,13 +155,7 @@ class SketchKMeans:
         # the first assignment (prev is None) is from seeded or K-means++ centres, which are
         # sparse: nearly every point has near-ties there, and the fp32 filter (K5f) is the faster
         if prev is not None and self._use_tc(K):
-            if "tcprep" not in self._ws:
-                prep = _lib.workspace(L.skc_kmeans_tc_prepare_workspace(self.n, self.m, self.p), self.dev)
-                with torch.cuda.device(self.dev):
-                    _lib.call("skc_kmeans_tc_prepare", self.idx.data_ptr(), self.val.data_ptr(), self.vcode, self.n,
-                              self.m, self.p, prep.data_ptr(), prep.numel(), self._st())
-                self._ws["tcprep"] = prep
-            prep = self._ws["tcprep"]
+            prep = self._tcprep()
             ws = self._workspace(("assign_tc", K), L.skc_kmeans_assign_tc_workspace(self.n, self.p, K))
             with torch.cuda.device(self.dev):
                 _lib.call("skc_kmeans_assign_tc", self.idx.data_ptr(), self.val.data_ptr(), self.vcode, self.n,
@@ -158,13 +181,7 @@ class SketchKMeans:
         Sums follow the reference's sequential order exactly, through the transposed sketch
         built on first use (``skc_kmeans_build_csc``)."""
         L = _lib.lib()
-        if "csc" not in self._ws:
-            csc = _lib.workspace(L.skc_kmeans_csc_workspace(self.n, self.m, self.p, self.vcode), self.dev)
-            with torch.cuda.device(self.dev):
-                _lib.call("skc_kmeans_build_csc", self.idx.data_ptr(), self.val.data_ptr(), self.vcode, self.n,
-                          self.m, self.p, csc.data_ptr(), csc.numel(), self._st())
-            self._ws["csc"] = csc
-        csc = self._ws["csc"]
+        csc = self._csc()
         seg = self._workspace(("seg", K), L.skc_kmeans_seg_workspace(self.n, self.m, self.p, K, self.vcode))
         sums = torch.empty((self.p, K), dtype=torch.float64, device=self.dev)
         counts = torch.empty((self.p, K), dtype=torch.int64, device=self.dev)

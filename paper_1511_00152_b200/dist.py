@@ -48,21 +48,47 @@ def allreduce_(t: torch.Tensor, op=None, group=None) -> torch.Tensor:
     return t
 
 
+def _packed_span(acc: torch.Tensor, stats: torch.Tensor, tri: Optional[torch.Tensor]) -> Optional[torch.Tensor]:
+    """The one contiguous fp64 buffer [acc | stats | tri] the three are views of, if they are."""
+    if not (acc.is_contiguous() and stats.is_contiguous() and acc.dtype == stats.dtype == torch.float64):
+        return None
+    p = acc.numel()
+    if stats.data_ptr() != acc.data_ptr() + 8 * p or stats.numel() != 3:
+        return None
+    total = p + 3
+    if tri is not None:
+        if not tri.is_contiguous() or tri.dtype != torch.float64 or tri.data_ptr() != stats.data_ptr() + 24:
+            return None
+        total += tri.numel()
+    return torch.as_strided(acc, (total,), (1,))
+
+
 def combine_moments(acc: torch.Tensor, stats: torch.Tensor, tri: Optional[torch.Tensor], n_local: int,
-                    group=None) -> int:
-    """Allreduce K2/K3 partials in place and return the global row count."""
+                    group=None, n_total: Optional[int] = None) -> int:
+    """Sum the K2/K3 partials of every rank in place with ONE allreduce; return the global rows.
+
+    acc / stats / tri are views of Moments.packed (one buffer), so the exchange is a single
+    fp64 SUM allreduce of [acc | stats | tri] (4.2 MB at p=1024). stats[1] (max |v|) is
+    summed too: the sum of the ranks' maxima bounds the global maximum, which is all a later
+    K3t scale needs; finalize does not read it. The global row count is stats[2] after the
+    sum; pass ``n_total`` when the caller knows it to avoid a device read.
+    """
     if world(group) == 1:
         return int(n_local)
-    allreduce_(acc, group=group)
-    mx = stats[1:2].clone()
-    allreduce_(stats, group=group)  # sum of squares and rows add up
-    allreduce_(mx, dist.ReduceOp.MAX, group=group)
-    stats[1:2].copy_(mx)
-    if tri is not None:
-        allreduce_(tri, group=group)
-    n = torch.tensor([int(n_local)], dtype=torch.int64, device=acc.device)
-    allreduce_(n, group=group)
-    return int(n.item())
+    buf = _packed_span(acc, stats, tri)
+    if buf is not None:
+        allreduce_(buf, group=group)
+    else:  # separately allocated partials: pack, one allreduce, unpack
+        parts = [acc.reshape(-1), stats.reshape(-1)] + ([tri.reshape(-1)] if tri is not None else [])
+        buf = torch.cat(parts)
+        allreduce_(buf, group=group)
+        o = 0
+        for t in parts:
+            t.copy_(buf[o:o + t.numel()])
+            o += t.numel()
+    if n_total is not None:
+        return int(n_total)
+    return int(round(float(stats[2].item())))
 
 
 def global_first_argmax(value: float, index: int, device, group=None) -> tuple[float, int]:
@@ -87,3 +113,21 @@ def broadcast_row(idx_row: Optional[torch.Tensor], val_row: Optional[torch.Tenso
     dist.broadcast(i, src=owner, group=group)
     dist.broadcast(v, src=owner, group=group)
     return i, v
+
+
+def init_centers_global(ops, chosen) -> torch.Tensor:
+    """init_centers (cluster.py:175-179) from GLOBAL point indices over sharded ops: each rank
+    fills the centres whose point lies in its shard [ops.col0, ops.col0 + ops.n), the others
+    stay zero, and one SUM allreduce gives every rank the full (p_pad, K) matrix."""
+    import numpy as np
+
+    chosen = np.asarray(chosen, dtype=np.int64)
+    if world() == 1 and int(getattr(ops, "col0", 0)) == 0:
+        return ops.init_centers(chosen)
+    c0, n = int(ops.col0), int(ops.n)
+    K = int(chosen.shape[0])
+    mu = torch.zeros((ops.p, K), dtype=torch.float64, device=ops.dev)
+    mine = np.flatnonzero((chosen >= c0) & (chosen < c0 + n))
+    if mine.size:
+        mu[:, torch.as_tensor(mine, device=ops.dev)] = ops.init_centers(chosen[mine] - c0)
+    return allreduce_(mu)

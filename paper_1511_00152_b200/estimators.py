@@ -39,12 +39,24 @@ class CovarianceEstimate:
 
 @dataclass
 class Moments:
-    """Device partial sums of one sketch (or one shard): mean accumulator, stats, triangle."""
+    """Device partial sums of one sketch (or one shard): mean accumulator, stats, triangle.
+
+    ``packed`` is one contiguous fp64 buffer [acc (p_pad) | stats (3) | tri] of which acc,
+    stats and tri are views, so a sharded run combines all partials with ONE allreduce
+    (dist.combine_moments; SPEC.md:212 "parallel partial sums then ordered combine")."""
 
     acc: torch.Tensor    # (p_pad,) fp64
     stats: torch.Tensor  # (3,) fp64: sum v^2, max |v|, rows
     tri: Optional[torch.Tensor]  # (p_pad (p_pad+1)/2,) fp64 or None
     n: int
+    packed: Optional[torch.Tensor] = None
+
+    @classmethod
+    def zeros(cls, p_pad: int, covariance: bool, device) -> "Moments":
+        tri_len = p_pad * (p_pad + 1) // 2 if covariance else 0
+        buf = torch.zeros(p_pad + 3 + tri_len, dtype=torch.float64, device=device)
+        return cls(acc=buf[:p_pad], stats=buf[p_pad:p_pad + 3], tri=buf[p_pad + 3:] if covariance else None, n=0,
+                   packed=buf)
 
 
 def accumulate_moments(sketch: SparseSketch, covariance: bool = True, into: Optional[Moments] = None) -> Moments:
@@ -52,13 +64,7 @@ def accumulate_moments(sketch: SparseSketch, covariance: bool = True, into: Opti
     dev = sketch.indices.device
     p, m, n = sketch.p, sketch.m, sketch.n
     if into is None:
-        tri_len = p * (p + 1) // 2
-        into = Moments(
-            acc=torch.zeros(p, dtype=torch.float64, device=dev),
-            stats=torch.zeros(3, dtype=torch.float64, device=dev),
-            tri=torch.zeros(tri_len, dtype=torch.float64, device=dev) if covariance else None,
-            n=0,
-        )
+        into = Moments.zeros(p, covariance, dev)
     L = _lib.lib()
     st = _lib.stream_ptr(dev)
     vcode = _lib.dtype_code(sketch.values)
@@ -127,10 +133,7 @@ def _stream_moments_native(rows: torch.Tensor, chunk_rows: int, spec, plan, cova
     n, p = rows.shape
     p_pad, m = spec.p_pad, plan.m
     if into is None:
-        into = Moments(acc=torch.zeros(p_pad, dtype=torch.float64, device=device),
-                       stats=torch.zeros(3, dtype=torch.float64, device=device),
-                       tri=torch.zeros(p_pad * (p_pad + 1) // 2, dtype=torch.float64, device=device)
-                       if covariance else None, n=0)
+        into = Moments.zeros(p_pad, covariance, device)
     chunk = max(1, min(int(chunk_rows), max(int(n), 1)))
     L = _lib.lib()
     xc = _lib.dtype_code(rows)
