@@ -21,6 +21,7 @@ threads) as the arm's value, and beside it the reference package itself (baselin
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -721,6 +722,8 @@ def main():
         out["configs"] = {}
         for other in ("c1", "c2", "c4", "c5"):
             oc = WORKLOADS[other]
+            gc.collect()
+            torch.cuda.empty_cache()
             try:
                 if oc["kind"] == "cov":
                     ln = cov_line(ctx, other, args, args.steps, args.warmup, args.compute, "oracle", clocks=False)
@@ -735,7 +738,9 @@ def main():
                 ln["config"] = {"workload": other, "desc": oc["desc"], "p": oc["p"], "m": oc["m"], "n": oc["n"]}
                 out["configs"][other] = ln
             except Exception as e:  # noqa: BLE001  (one config failing must not lose the headline)
-                out["configs"][other] = {"error": f"{type(e).__name__}: {e}"}
+                out["configs"][other] = {"error": f"{type(e).__name__}: {str(e)[:200]}",
+                                         "device_bytes_in_use": torch.cuda.memory_allocated(),
+                                         "device_bytes_reserved": torch.cuda.memory_reserved()}
             torch.cuda.empty_cache()
 
     if rank == 0:

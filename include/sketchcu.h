@@ -43,6 +43,8 @@ int skc_abi_version(void);
 int32_t skc_max_p_pad(void);
 /* Number of kernels this library has launched in the process (for launch accounting). */
 uint64_t skc_launch_count(void);
+/* Add kernels a replayed CUDA graph ran (skc_kmeans_lloyd) to skc_launch_count. */
+void skc_count_launches(uint64_t kernels);
 
 /* --- L0/L1: signs and transform -------------------------------------------------- */
 
@@ -191,6 +193,23 @@ int skc_kmeans_partials_csc(const void *csc, int32_t val_dtype, int64_t n, int32
  * reads its convergence flag. idx/val are the whole (n, m) sketch. */
 int skc_kmeans_reseed_at(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m,
                          const int64_t *row, const int32_t *empty, int32_t p_pad, int32_t K, double *mu, void *stream);
+
+/* The whole Lloyd loop of _lloyd_iterate (cluster.py:230-241) from centres mu0, device-resident:
+ * ONE CUDA graph with a conditional WHILE node runs the iterations (assign, numpy-order objective,
+ * convergence test on the device, partial sums through csc, centres, reseed) with no host round
+ * trip; it is built once per argument set and relaunched. The kernels are those of the
+ * host-driven loop, so labels, mu and the objective trajectory are bit-identical to it.
+ * csc: from skc_kmeans_build_csc (required). tc_prep: from skc_kmeans_tc_prepare, or NULL (then
+ * every assignment uses skc_kmeans_assign; otherwise iterations 2.. use the tensor-core filter).
+ * ws: skc_kmeans_lloyd_workspace bytes. Outputs (device, =): labels (n) int32 of the last
+ * assignment, mu (p_pad, K) the centres it used (updated when max_iter ends the loop), traj
+ * (max_iter) fp64 objectives of the executed iterations, iters[0] their count. Asynchronous. */
+size_t skc_kmeans_lloyd_workspace(int64_t n, int32_t m, int32_t p_pad, int32_t K, int32_t val_dtype, int32_t use_tc);
+int skc_kmeans_lloyd(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m, int32_t p_pad,
+                     int32_t K, const double *mu0, int32_t max_iter, const void *csc, const void *tc_prep, void *ws,
+                     size_t ws_bytes, int32_t *labels, double *mu, double *traj, int32_t *iters, void *stream);
+/* Kernels in the last skc_kmeans_lloyd graph of this thread: a run launches prologue + (iters - 1) * body. */
+void skc_kmeans_lloyd_graph_kernels(int32_t *prologue, int32_t *body);
 
 /* Row norms ||v_i||^2 of the sketch in numpy's pairwise order (the colsq of
  * cluster.py:148). out: (n) fp64 (=). */

@@ -17,7 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "_lib")
 SO = os.path.join(OUT, "libsketchcu.so")
-SOURCES = ["capi.cu", "sketch.cu", "moments.cu", "cov_tc.cu", "kmeans.cu", "kmeans_tc.cu", "formats.cu", "dense.cu", "gather.cu"]
+SOURCES = ["capi.cu", "sketch.cu", "moments.cu", "cov_tc.cu", "kmeans.cu", "kmeans_tc.cu", "formats.cu", "dense.cu", "gather.cu", "lloyd.cu"]
 HEADERS = [os.path.join(CSRC, "common.cuh"), os.path.join(ROOT, "include", "sketchcu.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -31,6 +31,11 @@ SIGNATURES = {
     "skc_abi_version": (_c.c_int, []),
     "skc_max_p_pad": (_I32, []),
     "skc_launch_count": (_U64, []),
+    "skc_count_launches": (None, [_U64]),
+    "skc_kmeans_lloyd_workspace": (_SZ, [_I64, _I32, _I32, _I32, _I32, _I32]),
+    "skc_kmeans_lloyd": (_c.c_int, [_P, _P, _I32, _I64, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _SZ, _P, _P, _P, _P,
+                                    _P]),
+    "skc_kmeans_lloyd_graph_kernels": (None, [_P, _P]),
     "skc_row_sqnorms": (_c.c_int, [_P, _I32, _I64, _I32, _P, _P]),
     "skc_kmeans_d2_to_point": (_c.c_int, [_P, _P, _I32, _I64, _I32, _I32, _I64, _P, _P, _P, _P]),
     "skc_signs": (_c.c_int, [_U64, _I32, _I32, _P, _P]),

@@ -13,6 +13,7 @@ row) drives the stopping rule of cluster.py:235-236.
 
 from __future__ import annotations
 
+import ctypes
 import os
 import time
 from dataclasses import dataclass, field
@@ -238,6 +239,8 @@ def lloyd_loop(ops, mu0: torch.Tensor, max_iter: int, group=None):
     """
     w = dist.world(group)
     if w == 1 and getattr(ops, "dev", torch.device("cpu")).type == "cuda" and hasattr(ops, "reseed_at"):
+        if isinstance(ops, SketchKMeans) and os.environ.get("SKC_LLOYD", "graph") == "graph":
+            return _lloyd_loop_graph(ops, mu0, max_iter)
         return _lloyd_loop_device(ops, mu0, max_iter)
     mu = mu0.clone()
     n, dev = ops.n, ops.dev
@@ -299,6 +302,57 @@ def lloyd_loop(ops, mu0: torch.Tensor, max_iter: int, group=None):
         e1.synchronize()
         secs = e0.elapsed_time(e1) * 1e-3
     return cur, mu, traj, iters, secs
+
+
+def _lloyd_loop_graph(ops: "SketchKMeans", mu0: torch.Tensor, max_iter: int):
+    """Single-GPU Lloyd loop as one device-resident CUDA graph (``skc_kmeans_lloyd``).
+
+    The iterations, including the convergence test of cluster.py:235-236, run inside a graph
+    with a conditional WHILE node: no host round trip per iteration. The host reads the
+    trajectory and the iteration count once, after the loop. Same kernels, same arithmetic
+    and the same trajectory as lloyd_loop (cluster.py:230-241).
+    """
+    L = _lib.lib()
+    n, m, p, K = ops.n, ops.m, ops.p, int(mu0.shape[1])
+    max_iter = int(max_iter)
+    use_tc = ops._use_tc(K)
+    csc = ops._csc()
+    prep = ops._tcprep() if use_tc else None
+    ws = ops._workspace(("lloyd_ws", K, use_tc), L.skc_kmeans_lloyd_workspace(n, m, p, K, ops.vcode, int(use_tc)))
+    key = ("lloyd_bufs", K, max_iter)
+    bufs = ops._ws.get(key)
+    if bufs is None:
+        bufs = dict(mu0=torch.empty((p, K), dtype=torch.float64, device=ops.dev),
+                    mu=torch.empty((p, K), dtype=torch.float64, device=ops.dev),
+                    labels=torch.empty(n, dtype=torch.int32, device=ops.dev),
+                    res=torch.zeros(max_iter + 1, dtype=torch.float64, device=ops.dev),
+                    host=torch.empty(max_iter + 1, dtype=torch.float64, pin_memory=True))
+        ops._ws[key] = bufs
+    res = bufs["res"]
+    traj_d, iters_d = res[:max_iter], res[max_iter:].view(torch.int32)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.device(ops.dev):
+        e0.record()
+        bufs["mu0"].copy_(mu0)
+        _lib.call("skc_kmeans_lloyd", ops.idx.data_ptr(), ops.val.data_ptr(), ops.vcode, n, m, p, K,
+                  bufs["mu0"].data_ptr(), max_iter, csc.data_ptr(), _lib.ptr(prep), ws.data_ptr(), ws.numel(),
+                  bufs["labels"].data_ptr(), bufs["mu"].data_ptr(), traj_d.data_ptr(), iters_d.data_ptr(),
+                  ops._st())
+        bufs["host"].copy_(res, non_blocking=True)  # the loop's one device-to-host read
+        e1.record()
+        e1.synchronize()
+    host = bufs["host"]
+    iters = int(host[max_iter:].view(torch.int32)[0])
+    traj = [float(v) for v in host[:iters]]
+    pro, body = _c_int32(), _c_int32()
+    L.skc_kmeans_lloyd_graph_kernels(ctypes.byref(pro), ctypes.byref(body))
+    L.skc_count_launches(pro.value + (iters - 1) * body.value)
+    return bufs["labels"].clone(), bufs["mu"].clone(), traj, iters, e0.elapsed_time(e1) * 1e-3
+
+
+def _c_int32():
+    return ctypes.c_int32(0)
 
 
 def _lloyd_loop_device(ops, mu0: torch.Tensor, max_iter: int):

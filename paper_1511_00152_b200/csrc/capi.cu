@@ -18,6 +18,7 @@ int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
+void note_launches(int64_t delta) { g_launches.fetch_add((uint64_t)delta, std::memory_order_relaxed); }
 int check_launch(const char* what) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
@@ -135,6 +136,7 @@ const char* skc_last_error(void) { return g_err.c_str(); }
 int skc_abi_version(void) { return 1; }
 int32_t skc_max_p_pad(void) { return kMaxPad; }
 uint64_t skc_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+void skc_count_launches(uint64_t kernels) { note_launches((int64_t)kernels); }
 
 int skc_signs(uint64_t sign_seed, int32_t p_pad, int32_t kind, double* out, void* stream) {
   int rc = check_spec(kind, p_pad, p_pad);

@@ -1,0 +1,305 @@
+// Device-resident Lloyd loop: the _lloyd_iterate loop body (cluster.py:230-241) from given
+// centres, as ONE CUDA graph with a conditional WHILE node, so the iterations run with no host
+// round trip (the convergence test of cluster.py:235-236 is evaluated on the device).
+//
+// Graph (built once per buffer set, cached, relaunched per call):
+//   copy mu0 -> mu, state = 0
+//   iteration 1 (prologue):   assign (K5/K5f, no previous labels) -> objective (numpy pairwise
+//                             order) -> check -> partials -> centres -> reseed -> commit
+//   WHILE (cond):             assign (K5t filter when prepared, else K5; changed count against
+//                             the previous labels) -> objective -> check -> partials -> centres
+//                             -> reseed -> commit
+//   copy state.it -> iters
+// check (one thread): traj[it] = objective; converged = (it > 1 && changed == 0);
+//   cond = !converged && it < max_iter (cudaGraphSetConditional).
+// The update after the check is speculative; commit keeps it (mu = mu_next, previous labels =
+// current labels) only when the iteration did not converge, which is exactly the reference's
+// "break before update" order. Every kernel is the same one the host-driven loop launches, so
+// labels, centres and the objective trajectory are bit-identical to it.
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "common.cuh"
+
+namespace skc {
+
+size_t assign_ws(int64_t, int32_t, int32_t);
+size_t kmtc_assign_ws(int64_t, int32_t, int32_t);
+size_t pairwise_ws();
+size_t seg_ws(int64_t, int32_t, int32_t, int32_t, int);
+void note_launches(int64_t delta);
+
+namespace {
+
+__global__ void lloyd_check_kernel(const int64_t* __restrict__ out, const double* __restrict__ obj,
+                                   double* __restrict__ traj, int32_t* __restrict__ state, int max_iter, int first,
+                                   cudaGraphConditionalHandle cond) {
+  const int it = state[0] + 1;  // iterations executed, this assignment included
+  traj[it - 1] = *obj;
+  const int conv = (!first && out[0] == 0) ? 1 : 0;
+  state[0] = it;
+  state[1] = conv;
+  cudaGraphSetConditional(cond, (!conv && it < max_iter) ? 1u : 0u);
+}
+
+__global__ void lloyd_commit_kernel(const int32_t* __restrict__ state, const double* __restrict__ mu_next,
+                                    double* __restrict__ mu, int64_t pk, const int32_t* __restrict__ cur,
+                                    int32_t* __restrict__ prev, int64_t n) {
+  if (state[1]) return;  // converged: the centres of the final assignment stay
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pk; i += stride) mu[i] = mu_next[i];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) prev[i] = cur[i];
+}
+
+struct Carve {
+  size_t off = 0;
+  template <typename T>
+  T* take(char* base, size_t count) {
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += (count * sizeof(T) + 255) & ~(size_t)255;
+    return p;
+  }
+};
+
+struct Bufs {
+  int32_t* prev;
+  double* d2min;
+  int64_t* out;
+  double* d2max;
+  double* obj;
+  int32_t* state;
+  double* mu_next;
+  double* sums;
+  int64_t* counts;
+  int64_t* sizes;
+  int32_t* empty;
+  void* aws;
+  size_t aws_bytes;
+  void* pws;
+  size_t pws_bytes;
+  void* sws;
+  size_t sws_bytes;
+};
+
+Bufs carve(char* base, int64_t n, int32_t m, int32_t p_pad, int32_t K, int32_t vdt, bool tc, size_t* total) {
+  Carve c;
+  Bufs b;
+  const size_t pk = (size_t)p_pad * K;
+  b.prev = c.take<int32_t>(base, n);
+  b.d2min = c.take<double>(base, n);
+  b.out = c.take<int64_t>(base, 2);
+  b.d2max = c.take<double>(base, 1);
+  b.obj = c.take<double>(base, 1);
+  b.state = c.take<int32_t>(base, 2);
+  b.mu_next = c.take<double>(base, pk);
+  b.sums = c.take<double>(base, pk);
+  b.counts = c.take<int64_t>(base, pk);
+  b.sizes = c.take<int64_t>(base, K);
+  b.empty = c.take<int32_t>(base, K);
+  size_t a = assign_ws(n, p_pad, K);
+  if (tc) {
+    const size_t t = kmtc_assign_ws(n, p_pad, K);
+    a = t > a ? t : a;
+  }
+  b.aws_bytes = a;
+  b.aws = c.take<char>(base, a);
+  b.pws_bytes = pairwise_ws();
+  b.pws = c.take<char>(base, b.pws_bytes);
+  b.sws_bytes = seg_ws(n, m, p_pad, K, vdt);
+  b.sws = c.take<char>(base, b.sws_bytes);
+  if (total) *total = c.off;
+  return b;
+}
+
+struct Entry {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int prologue_kernels = 0, body_kernels = 0;
+  uint64_t stamp = 0;
+};
+using Key = std::tuple<const void*, const void*, int64_t, int32_t, int32_t, int32_t, int32_t, const void*, int32_t,
+                       const void*, const void*, const void*, size_t, const void*, const void*, const void*,
+                       const void*, int>;
+std::mutex g_mu;
+std::map<Key, Entry> g_cache;
+uint64_t g_stamp = 0;
+thread_local int g_last_prologue = 0, g_last_body = 0;
+
+struct Args {
+  const int32_t* idx;
+  const void* val;
+  int32_t vdt;
+  int64_t n;
+  int32_t m, p_pad, K;
+  const double* mu0;
+  int32_t max_iter;
+  const void* csc;
+  const void* prep;
+  int32_t* labels;
+  double* mu;
+  double* traj;
+  int32_t* iters;
+};
+
+// one iteration's launches on stream s; returns SKC_OK or the first error
+int iteration(const Args& A, const Bufs& B, bool first, cudaGraphConditionalHandle cond, cudaStream_t s) {
+  int rc;
+  const int32_t* prev = first ? nullptr : B.prev;
+  if (!first && A.prep != nullptr)
+    rc = skc_kmeans_assign_tc(A.idx, A.val, A.vdt, A.n, A.m, A.mu, A.p_pad, A.K, prev, A.labels, B.d2min, B.out,
+                              B.d2max, A.prep, B.aws, B.aws_bytes, s);
+  else
+    rc = skc_kmeans_assign(A.idx, A.val, A.vdt, A.n, A.m, A.mu, A.p_pad, A.K, prev, A.labels, B.d2min, B.out,
+                           B.d2max, B.aws, B.aws_bytes, s);
+  if (rc) return rc;
+  if ((rc = skc_pairwise_sum(B.d2min, A.n, B.obj, B.pws, B.pws_bytes, s))) return rc;
+  lloyd_check_kernel<<<1, 1, 0, s>>>(B.out, B.obj, A.traj, B.state, A.max_iter, first ? 1 : 0, cond);
+  if ((rc = check_launch("lloyd_check_kernel"))) return rc;
+  if ((rc = skc_kmeans_partials_csc(A.csc, A.vdt, A.n, A.m, A.p_pad, A.labels, A.K, B.sums, B.counts, B.sizes, B.sws,
+                                    B.sws_bytes, s)))
+    return rc;
+  if ((rc = skc_kmeans_centers(B.sums, B.counts, B.sizes, A.mu, A.p_pad, A.K, B.mu_next, B.empty, s))) return rc;
+  if ((rc = skc_kmeans_reseed_at(A.idx, A.val, A.vdt, A.n, A.m, B.out + 1, B.empty, A.p_pad, A.K, B.mu_next, s)))
+    return rc;
+  const int64_t pk = (int64_t)A.p_pad * A.K;
+  const int64_t work = A.n > pk ? A.n : pk;
+  int64_t blocks = (work + 255) / 256;
+  if (blocks > 4 * (int64_t)sm_count()) blocks = 4 * (int64_t)sm_count();
+  lloyd_commit_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(B.state, B.mu_next, A.mu, pk, A.labels,
+                                                                          B.prev, A.n);
+  return check_launch("lloyd_commit_kernel");
+}
+
+int build(const Args& A, const Bufs& B, Entry& E) {
+  cudaGraph_t g = nullptr;
+  if (cudaGraphCreate(&g, 0) != cudaSuccess) return check_launch("cudaGraphCreate");
+  cudaGraphConditionalHandle cond;
+  if (cudaGraphConditionalHandleCreate(&cond, g, 0, cudaGraphCondAssignDefault) != cudaSuccess) {
+    cudaGraphDestroy(g);
+    return check_launch("cudaGraphConditionalHandleCreate");
+  }
+  cudaStream_t s1 = nullptr, s2 = nullptr;
+  cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+  int rc = SKC_OK;
+  auto done = [&](int code) {
+    cudaStreamDestroy(s1);
+    cudaStreamDestroy(s2);
+    if (code != SKC_OK) cudaGraphDestroy(g);
+    return code;
+  };
+  if (cudaStreamBeginCaptureToGraph(s1, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) != cudaSuccess)
+    return done(check_launch("begin capture"));
+  cudaMemcpyAsync(A.mu, A.mu0, sizeof(double) * A.p_pad * A.K, cudaMemcpyDeviceToDevice, s1);
+  cudaMemsetAsync(B.state, 0, 2 * sizeof(int32_t), s1);
+  const uint64_t l0 = skc_launch_count();
+  rc = iteration(A, B, true, cond, s1);
+  const uint64_t l1 = skc_launch_count();
+  cudaStreamCaptureStatus status;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  cudaGraph_t cg = nullptr;
+  if (rc == SKC_OK && cudaStreamGetCaptureInfo(s1, &status, nullptr, &cg, &deps, &ndeps) != cudaSuccess)
+    rc = check_launch("capture info");
+  cudaGraphNode_t cnode = nullptr;
+  cudaGraph_t body = nullptr;
+  if (rc == SKC_OK) {
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    if (cudaGraphAddNode(&cnode, cg, deps, ndeps, &cp) != cudaSuccess) rc = check_launch("add conditional node");
+    else body = cp.conditional.phGraph_out[0];
+  }
+  if (rc == SKC_OK && cudaStreamUpdateCaptureDependencies(s1, &cnode, 1, cudaStreamSetCaptureDependencies) !=
+                          cudaSuccess)
+    rc = check_launch("update capture dependencies");
+  uint64_t l2 = l1, l3 = l1;
+  if (rc == SKC_OK) {
+    if (cudaStreamBeginCaptureToGraph(s2, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+      rc = check_launch("begin body capture");
+    } else {
+      l2 = skc_launch_count();
+      rc = iteration(A, B, false, cond, s2);
+      l3 = skc_launch_count();
+      cudaGraph_t bo = nullptr;
+      if (cudaStreamEndCapture(s2, &bo) != cudaSuccess && rc == SKC_OK) rc = check_launch("end body capture");
+    }
+  }
+  if (rc == SKC_OK) cudaMemcpyAsync(A.iters, B.state, sizeof(int32_t), cudaMemcpyDeviceToDevice, s1);
+  cudaGraph_t go = nullptr;
+  if (cudaStreamEndCapture(s1, &go) != cudaSuccess && rc == SKC_OK) rc = check_launch("end capture");
+  note_launches(-(int64_t)(skc_launch_count() - l0));  // captured, not executed
+  if (rc != SKC_OK) return done(rc);
+  if (cudaGraphInstantiate(&E.exec, g, 0) != cudaSuccess) return done(check_launch("graph instantiate"));
+  E.graph = g;
+  E.prologue_kernels = (int)(l1 - l0);
+  E.body_kernels = (int)(l3 - l2);
+  return done(SKC_OK);
+}
+
+}  // namespace
+}  // namespace skc
+
+using namespace skc;
+
+extern "C" {
+
+size_t skc_kmeans_lloyd_workspace(int64_t n, int32_t m, int32_t p_pad, int32_t K, int32_t val_dtype, int32_t use_tc) {
+  size_t total = 0;
+  carve(nullptr, n, m, p_pad, K, val_dtype, use_tc != 0, &total);
+  return total;
+}
+
+int skc_kmeans_lloyd(const int32_t* idx, const void* val, int32_t val_dtype, int64_t n, int32_t m, int32_t p_pad,
+                     int32_t K, const double* mu0, int32_t max_iter, const void* csc, const void* tc_prep, void* ws,
+                     size_t ws_bytes, int32_t* labels, double* mu, double* traj, int32_t* iters, void* stream) {
+  if (val_dtype != SKC_F32 && val_dtype != SKC_F64) return fail(SKC_EPARAM, "values must be fp32 or fp64");
+  if (n < 1 || m < 1 || m > p_pad || K < 1) return fail(SKC_EDIM, "bad (n, m, p_pad, K)");
+  if (max_iter < 1) return fail(SKC_EPARAM, "max_iter must be >= 1");
+  if (csc == nullptr) return fail(SKC_EPARAM, "csc (skc_kmeans_build_csc) is required");
+  size_t need = 0;
+  const Bufs B = carve(static_cast<char*>(ws), n, m, p_pad, K, val_dtype, tc_prep != nullptr, &need);
+  if (ws_bytes < need) return fail(SKC_EPARAM, "workspace too small");
+  Args A{idx, val, val_dtype, n, m, p_pad, K, mu0, max_iter, csc, tc_prep, labels, mu, traj, iters};
+  const Key key{idx, val, n, m, p_pad, K, val_dtype, mu0, max_iter, csc, tc_prep, ws, ws_bytes, labels, mu, traj, iters,
+                [] {
+                  int d = 0;
+                  cudaGetDevice(&d);
+                  return d;
+                }()};
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_cache.find(key);
+  if (it == g_cache.end()) {
+    if (g_cache.size() >= 8) {  // evict the least recently used graph
+      auto old = g_cache.begin();
+      for (auto j = g_cache.begin(); j != g_cache.end(); ++j)
+        if (j->second.stamp < old->second.stamp) old = j;
+      cudaGraphExecDestroy(old->second.exec);
+      cudaGraphDestroy(old->second.graph);
+      g_cache.erase(old);
+    }
+    Entry E;
+    const int rc = build(A, B, E);
+    if (rc) return rc;
+    it = g_cache.emplace(key, E).first;
+  }
+  it->second.stamp = ++g_stamp;
+  g_last_prologue = it->second.prologue_kernels;
+  g_last_body = it->second.body_kernels;
+  if (cudaGraphLaunch(it->second.exec, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+    return check_launch("graph launch");
+  return SKC_OK;
+}
+
+// kernels of the last skc_kmeans_lloyd graph on this thread: the prologue (first iteration) and
+// one WHILE-body iteration, for launch accounting (a run launches prologue + (iters-1) * body)
+void skc_kmeans_lloyd_graph_kernels(int32_t* prologue, int32_t* body) {
+  if (prologue) *prologue = g_last_prologue;
+  if (body) *body = g_last_body;
+}
+
+}  // extern "C"
