@@ -430,6 +430,7 @@ def cov_line(ctx, wl, args, steps, warmup, compute, sampler="oracle", clocks=Tru
     def step(ev):
         mom.packed.zero_()
         ev[0].record()
+        # the sketch as the two kernels skc_sketch runs: K1a indices (oracle keys or Philox), K1b gather
         if sampler == "philox":
             lib.call("skc_indices_philox", plan.master_seed, col0, n, p, m, idx.data_ptr(), st)
         else:
@@ -473,10 +474,11 @@ def cov_line(ctx, wl, args, steps, warmup, compute, sampler="oracle", clocks=Tru
     ms_step = ctx.max_over_ranks(t0.elapsed_time(t1) / steps)
     stage_ms = {nm: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / steps for i, nm in enumerate(names)}
     vsz = 4 if compute == "f32" else 8
-    # algorithmic bytes per sample: indices write idx; gather reads the row and idx, writes values
+    # algorithmic bytes per sample: the index kernel writes idx; the gather reads the row and idx
+    # and writes values; K2 / K3 read the (index, value) pairs
     unit_bytes = {"indices": 4 * m, "gather": 4 * p + 4 * m + vsz * m, "moments": (4 + vsz) * m,
                   "covariance": (4 + vsz) * m, "combine+finalize": 0}
-    dom = max(("indices", "gather", "moments", "covariance"), key=lambda k: stage_ms[k])
+    dom = max((k for k in unit_bytes if unit_bytes[k] > 0), key=lambda k: stage_ms[k])
     dom_bytes = unit_bytes[dom] * n
     achieved = dom_bytes / (stage_ms[dom] * 1e-3) / 1e9
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": ctx.hbm_peak, "unit": "GB/s",

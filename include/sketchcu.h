@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-enum { SKC_OK = 0, SKC_EDIM = 1, SKC_EPARAM = 2, SKC_ECUDA = 3 };
+enum { SKC_OK = 0, SKC_EDIM = 1, SKC_EPARAM = 2, SKC_ECUDA = 3, SKC_ENCCL = 4 };
 /* transform kinds, transform.py:81-84 (DCT is outside the GPU hot path: SKC_EPARAM) */
 enum { SKC_KIND_HADAMARD = 0, SKC_KIND_DCT = 1, SKC_KIND_NONE = 2 };
 enum { SKC_F32 = 0, SKC_F64 = 1 };
@@ -277,6 +277,31 @@ int skc_dense_assign(const void *X, int32_t x_dtype, int64_t ld, int64_t n, int3
 size_t skc_dense_sums_workspace(int64_t n, int32_t p, int32_t K);
 int skc_dense_sums(const void *X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, const int32_t *labels, int32_t K,
                    double *sums, int64_t *counts, void *ws, void *stream);
+
+/* ---- sample-sharded exchange (SURVEY 8(e); SPEC.md:212, :352 ordered combine of partials) ----
+ * Rank r holds global columns [col0, col0 + n) and runs every entry point above on its shard
+ * with that col0. Per pass, ONE fp64 SUM allreduce of the packed moments buffer
+ * [acc (p_pad) | stats (3) | triangle] (skc_moments_packed_len; stats[1] becomes the sum of the
+ * ranks' maxima, an upper bound that is all a later K3t scale needs). Per Lloyd iteration, ONE
+ * allreduce of the packed K-means exchange (skc_kmeans_pack_exchange: the partials of
+ * skc_kmeans_partials*, the changed count and objective, and per rank its max d2min with the
+ * global row of its first argmax, from which every rank picks the reseed point), then
+ * skc_kmeans_unpack_exchange -> skc_kmeans_centers. NCCL is dlopen'ed ("libnccl.so.2"); comm is
+ * an ncclComm_t (void*); NCCL failures return SKC_ENCCL. */
+int skc_nccl_get_unique_id(void *id_out /* 128 bytes: ncclUniqueId */);
+int skc_nccl_comm_init_rank(void **comm_out, int32_t nranks, const void *id, int32_t rank);
+int skc_nccl_comm_destroy(void *comm);
+/* In-place fp64 SUM allreduce on `stream` (ncclAllReduce). */
+int skc_allreduce_sum_f64(double *buf, size_t count, void *comm, void *stream);
+size_t skc_moments_packed_len(int32_t p_pad, int32_t covariance);
+size_t skc_kmeans_exchange_len(int32_t p_pad, int32_t K, int32_t world);
+/* buf (skc_kmeans_exchange_len doubles, =): sums, counts (as exact fp64), sizes, out[0]
+ * (changed), *objective, and this rank's slot (d2max[0], col0 + out[1]); other slots zero. */
+int skc_kmeans_pack_exchange(const double *sums, const int64_t *counts, const int64_t *sizes, const int64_t *out,
+                             const double *d2max, const double *objective, int32_t p_pad, int32_t K, int32_t rank,
+                             int32_t world, int64_t col0, double *buf, void *stream);
+int skc_kmeans_unpack_exchange(const double *buf, int32_t p_pad, int32_t K, double *sums, int64_t *counts,
+                               int64_t *sizes, void *stream);
 
 #ifdef __cplusplus
 }

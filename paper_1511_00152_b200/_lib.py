@@ -12,13 +12,13 @@ import threading
 
 import torch
 
-from .errors import DeviceError, DimensionError, ParameterError
+from .errors import CommError, DeviceError, DimensionError, ParameterError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # SKC_LIB selects an alternative build of the same library (kernel A/B experiments)
 SO_PATH = os.environ.get("SKC_LIB") or os.path.join(_HERE, "_lib", "libsketchcu.so")
 
-SKC_OK, SKC_EDIM, SKC_EPARAM, SKC_ECUDA = 0, 1, 2, 3
+SKC_OK, SKC_EDIM, SKC_EPARAM, SKC_ECUDA, SKC_ENCCL = 0, 1, 2, 3, 4
 KIND_CODES = {"hadamard": 0, "dct": 1, "none": 2}
 F32, F64 = 0, 1
 
@@ -78,6 +78,14 @@ SIGNATURES = {
                                       _P, _P, _P, _P, _SZ, _P]),
     "skc_sketch_pack_records": (_c.c_int, [_P, _P, _I32, _I64, _I32, _P, _P]),
     "skc_sketch_unpack_records": (_c.c_int, [_P, _I64, _I32, _P, _P, _P]),
+    "skc_nccl_get_unique_id": (_c.c_int, [_P]),
+    "skc_nccl_comm_init_rank": (_c.c_int, [_P, _I32, _P, _I32]),
+    "skc_nccl_comm_destroy": (_c.c_int, [_P]),
+    "skc_allreduce_sum_f64": (_c.c_int, [_P, _SZ, _P, _P]),
+    "skc_moments_packed_len": (_SZ, [_I32, _I32]),
+    "skc_kmeans_exchange_len": (_SZ, [_I32, _I32, _I32]),
+    "skc_kmeans_pack_exchange": (_c.c_int, [_P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I64, _P, _P]),
+    "skc_kmeans_unpack_exchange": (_c.c_int, [_P, _I32, _I32, _P, _P, _P, _P]),
     "skc_dense_assign_workspace": (_c.c_size_t, [_I32, _I32]),
     "skc_dense_assign": (_c.c_int, [_P, _I32, _I64, _I64, _I32, _P, _I32, _P, _P, _P, _P]),
     "skc_dense_sums_workspace": (_c.c_size_t, [_I64, _I32, _I32]),
@@ -122,6 +130,8 @@ def check(rc: int) -> None:
         raise DimensionError(msg)
     if rc == SKC_EPARAM:
         raise ParameterError(msg)
+    if rc == SKC_ENCCL:
+        raise CommError(msg)
     raise DeviceError(msg)
 
 

@@ -242,18 +242,16 @@ def lloyd_loop(ops, mu0: torch.Tensor, max_iter: int, group=None):
         if isinstance(ops, SketchKMeans) and os.environ.get("SKC_LLOYD", "graph") == "graph":
             return _lloyd_loop_graph(ops, mu0, max_iter)
         return _lloyd_loop_device(ops, mu0, max_iter)
+    if w > 1:
+        return _lloyd_loop_sharded(ops, mu0, max_iter, group)
     mu = mu0.clone()
     n, dev = ops.n, ops.dev
-    n_global = n
-    if w > 1:
-        t = torch.tensor([n], dtype=torch.int64, device=dev)
-        n_global = int(dist.allreduce_(t, group=group).item())
     lab = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(2)]
     d2min = torch.empty(n, dtype=torch.float64, device=dev)
     out = torch.zeros(2, dtype=torch.int64, device=dev)
     d2max = torch.zeros(1, dtype=torch.float64, device=dev)
     obj = torch.zeros(1, dtype=torch.float64, device=dev)
-    stage = torch.empty(4, dtype=torch.float64, device=dev)
+    stage = torch.empty(2, dtype=torch.float64, device=dev)
     traj, iters, prev = [], 0, None
     cur = lab[0]
     timed = dev.type == "cuda"
@@ -265,37 +263,100 @@ def lloyd_loop(ops, mu0: torch.Tensor, max_iter: int, group=None):
         cur = lab[it % 2]
         ops.assign(mu, prev, cur, d2min, out, d2max)
         ops.objective(d2min, obj)
-        stage[0:2].copy_(out)  # changed, local argmax row (exact below 2^53)
-        stage[2:3].copy_(obj)
-        stage[3:4].copy_(d2max)
-        if w > 1:
-            red = stage[0:1].clone()
-            dist.allreduce_(red, group=group)
-            obj_sum = stage[2:3].clone()
-            dist.allreduce_(obj_sum, group=group)
-            stage[0:1].copy_(red)
-            stage[2:3].copy_(obj_sum)
+        stage[0:1].copy_(out[0:1])  # changed (exact below 2^53)
+        stage[1:2].copy_(obj)
         host = stage.cpu()  # the one device-to-host read of the iteration
-        changed, arg_local, objective, vmax = int(host[0]), int(host[1]), float(host[2]), float(host[3])
+        changed, objective = int(host[0]), float(host[1])
         traj.append(objective)
         iters += 1
         if prev is not None and changed == 0:
             break
         prev = cur
         mu, _, empty = ops.update(cur, mu, group)
-        # reseed point: global first argmax of d2min (cluster.py:213)
-        if w > 1:
-            g_local = ops.col0 + arg_local if arg_local >= 0 else -1
-            _, g = dist.global_first_argmax(vmax, g_local, dev, group)
-            owner = dist.owner_of(g, n_global, w)
-            row = g - ops.col0
-            mine = dist.rank(group) == owner
-            idx_row, val_row = dist.broadcast_row(ops.idx[row] if mine else None, ops.val[row] if mine else None,
-                                                  ops.m, ops.val.dtype, owner, dev, group)
+        r = max(int(out[1]), 0)  # reseed point: first argmax of d2min (cluster.py:213)
+        ops.reseed(mu, empty, ops.idx[r], ops.val[r])
+    secs = 0.0
+    if timed:
+        e1.record()
+        e1.synchronize()
+        secs = e0.elapsed_time(e1) * 1e-3
+    return cur, mu, traj, iters, secs
+
+
+def _lloyd_loop_sharded(ops, mu0: torch.Tensor, max_iter: int, group=None):
+    """cluster.py:230-241 over a sample-sharded sketch; every rank follows the same trajectory.
+
+    Per iteration ONE SUM allreduce of the packed exchange (``skc_kmeans_pack_exchange``
+    layout): [sums | counts | sizes | changed | objective | per rank (max d2min, global row of
+    its first argmax)]. The partial sums are formed speculatively before the convergence test,
+    as the single-GPU graph does; a converged iteration discards them. Only an iteration that
+    empties a cluster adds one more allreduce, of the reseed row (SPEC.md:212, :352 ordered
+    combine; the owner of the global first argmax is found from every rank's actual range).
+    """
+    w, me = dist.world(group), dist.rank(group)
+    mu = mu0.clone()
+    n, dev, p, m = ops.n, ops.dev, ops.p, ops.m
+    K = int(mu.shape[1])
+    pk = p * K
+    ranges = dist.shard_ranges(int(ops.col0), n, dev, group)
+    lab = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(2)]
+    d2min = torch.empty(n, dtype=torch.float64, device=dev)
+    out = torch.zeros(2, dtype=torch.int64, device=dev)
+    d2max = torch.zeros(1, dtype=torch.float64, device=dev)
+    obj = torch.zeros(1, dtype=torch.float64, device=dev)
+    buf = torch.zeros(2 * pk + K + 2 + 2 * w, dtype=torch.float64, device=dev)
+    on_gpu = dev.type == "cuda" and isinstance(ops, SketchKMeans)
+    traj, iters, prev = [], 0, None
+    cur = lab[0]
+    timed = dev.type == "cuda"
+    if timed:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+    for it in range(max_iter):
+        cur = lab[it % 2]
+        ops.assign(mu, prev, cur, d2min, out, d2max)
+        ops.objective(d2min, obj)
+        sums, counts, sizes = ops.partials(cur, K)
+        if on_gpu:
+            with torch.cuda.device(dev):
+                _lib.call("skc_kmeans_pack_exchange", sums.data_ptr(), counts.data_ptr(), sizes.data_ptr(),
+                          out.data_ptr(), d2max.data_ptr(), obj.data_ptr(), p, K, me, w, int(ops.col0),
+                          buf.data_ptr(), _lib.stream_ptr(dev))
         else:
-            r = max(arg_local, 0)
-            idx_row, val_row = ops.idx[r], ops.val[r]
-        ops.reseed(mu, empty, idx_row, val_row)
+            buf.zero_()
+            buf[:pk] = sums.reshape(-1)
+            buf[pk:2 * pk] = counts.reshape(-1).to(torch.float64)
+            buf[2 * pk:2 * pk + K] = sizes.to(torch.float64)
+            buf[2 * pk + K] = out[0].to(torch.float64)
+            buf[2 * pk + K + 1] = obj[0]
+            slot = 2 * pk + K + 2 + 2 * me
+            buf[slot] = d2max[0]
+            buf[slot + 1] = float(int(ops.col0) + int(out[1])) if int(out[1]) >= 0 else -1.0
+        dist.allreduce_(buf, group=group)  # the one collective of the iteration
+        host = buf[2 * pk:].cpu()  # the one device-to-host read: sizes, changed, objective, slots
+        changed, objective = int(host[K]), float(host[K + 1])
+        traj.append(objective)
+        iters += 1
+        if prev is not None and changed == 0:
+            break
+        prev = cur
+        sums_g = buf[:pk].view(p, K)
+        counts_g = buf[pk:2 * pk].view(p, K).to(torch.int64)
+        sizes_g = buf[2 * pk:2 * pk + K].to(torch.int64)
+        mu, empty = ops.centers(sums_g, counts_g, sizes_g, mu)
+        if bool((host[:K] == 0).any()):
+            # reseed point: global first argmax of d2min (cluster.py:213, np.argmax semantics)
+            slots = host[K + 2:].view(w, 2)
+            vmax = float(slots[:, 0].max())
+            g = min(int(slots[q, 1]) for q in range(w) if float(slots[q, 0]) == vmax and slots[q, 1] >= 0)
+            owner = next(q for q, (c0, nq) in enumerate(ranges) if c0 <= g < c0 + nq)
+            row = torch.zeros(2 * m, dtype=torch.float64, device=dev)
+            if me == owner:
+                row[:m] = ops.idx[g - ranges[me][0]].to(torch.float64)
+                row[m:] = ops.val[g - ranges[me][0]].to(torch.float64)
+            dist.allreduce_(row, group=group)
+            ops.reseed(mu, empty, row[:m].to(torch.int32), row[m:].to(ops.val.dtype))
     secs = 0.0
     if timed:
         e1.record()

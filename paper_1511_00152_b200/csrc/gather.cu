@@ -433,16 +433,19 @@ static int launch_logp(int logp, const float* X, int64_t ld, const Params& P, cu
 // Returns SKC_OK / an error code, or -1 when the shape is not eligible (the caller then
 // uses the cp.async kernels of sketch.cu). Eligible: fp32 rows, p == p_pad in [32, 4096],
 // 16-byte aligned base and row stride, n < 2^31. SKC_GATHER=old disables it (A/B runs).
-int gather_tma_launch(const void* X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, int32_t p_pad,
-                      int32_t use_signs, uint64_t sign_seed, int32_t m, int32_t compute_dtype, const int32_t* idx_in,
-                      void* val_out, int32_t val_dtype, cudaStream_t st) {
+bool gather_tma_eligible(const void* X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, int32_t p_pad) {
   static const bool off = [] {
     const char* e = getenv("SKC_GATHER");
     return e != nullptr && e[0] == 'o';
   }();
-  if (off || X == nullptr || x_dtype != SKC_F32 || p != p_pad || p_pad < 32 || p_pad > 4096 || n <= 0 ||
-      n >= ((int64_t)1 << 31) || (reinterpret_cast<uintptr_t>(X) % 16) != 0 || ((ld * 4) % 16) != 0 || ld < p)
-    return -1;
+  return !(off || X == nullptr || x_dtype != SKC_F32 || p != p_pad || p_pad < 32 || p_pad > 4096 || n <= 0 ||
+           n >= ((int64_t)1 << 31) || (reinterpret_cast<uintptr_t>(X) % 16) != 0 || ((ld * 4) % 16) != 0 || ld < p);
+}
+
+int gather_tma_launch(const void* X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, int32_t p_pad,
+                      int32_t use_signs, uint64_t sign_seed, int32_t m, int32_t compute_dtype, const int32_t* idx_in,
+                      void* val_out, int32_t val_dtype, cudaStream_t st) {
+  if (!gather_tma_eligible(X, x_dtype, ld, n, p, p_pad)) return -1;
   int logp = 0;
   while ((1 << logp) < p_pad) ++logp;
   gtma::Params P{};

@@ -583,7 +583,8 @@ static int tc_min_m(int32_t p_pad) {
 
 // 'b' banded scatter (K3), 'g' global L2 scatter (K3g), 't' tensor cores (K3t).
 // SKC_COV_PATH=b|g|t forces a path where it applies.
-static char cov_path(int32_t m, int32_t p_pad) {
+constexpr int64_t kCovSmallRows = (int64_t)1 << 18;  // below: the band partials' reduce dominates (C1: 0.29 vs 0.05 ms)
+static char cov_path(int32_t m, int32_t p_pad, int64_t n) {
   const int cap = band_capacity(m, p_pad);
   const bool tc = covtc_supported(p_pad);
   if (const char* f = getenv("SKC_COV_PATH")) {
@@ -593,11 +594,12 @@ static char cov_path(int32_t m, int32_t p_pad) {
   }
   if (tc && (m >= tc_min_m(p_pad) || cap < p_pad)) return 't';
   if (cap < p_pad) return 'g';
+  if (n < kCovSmallRows && (size_t)kCovGWarps * 2 * m * sizeof(int2) <= 200 * 1024) return 'g';
   return make_bands(p_pad, cap, nullptr) > kCovGlobalBands ? 'g' : 'b';
 }
 
 int cov_check(int32_t p_pad, int32_t m) {
-  const char path = cov_path(m, p_pad);
+  const char path = cov_path(m, p_pad, kCovSmallRows);
   if (path == 't') return SKC_OK;
   if (path == 'g') return (size_t)kCovGWarps * 2 * m * sizeof(int2) <= 200 * 1024
                               ? SKC_OK
@@ -608,7 +610,7 @@ int cov_check(int32_t p_pad, int32_t m) {
 }
 
 size_t cov_ws(int64_t n, int32_t m, int32_t p_pad) {
-  const char path = cov_path(m, p_pad);
+  const char path = cov_path(m, p_pad, n);
   if (path == 't') return covtc_ws(n, m, p_pad);
   if (path == 'g') return (size_t)tri_off(p_pad, p_pad) * sizeof(unsigned long long);
   const int nb = make_bands(p_pad, band_capacity(m, p_pad), nullptr);
@@ -655,7 +657,7 @@ int cov_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int3
                const double* stats, double* tri, void* ws, cudaStream_t st) {
   if (n == 0) return SKC_OK;
   // path: banded shared-memory accumulation, or (many bands) the L2-resident global path
-  const char path = cov_path(m, p_pad);
+  const char path = cov_path(m, p_pad, n);
   if (path == 't') return covtc_launch(idx, val, val_f64, n, m, p_pad, stats, tri, ws, st);
   if (path == 'g') return cov_launch_global(idx, val, val_f64, n, m, p_pad, stats, tri, ws, st);
   // the kernel addresses a group's rows with 32-bit element offsets: split huge inputs

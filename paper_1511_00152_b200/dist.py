@@ -131,3 +131,15 @@ def init_centers_global(ops, chosen) -> torch.Tensor:
     if mine.size:
         mu[:, torch.as_tensor(mine, device=ops.dev)] = ops.init_centers(chosen[mine] - c0)
     return allreduce_(mu)
+
+
+def shard_ranges(col0: int, n: int, device, group=None) -> list:
+    """Every rank's global column range [(col0, n)], from one allreduce (ranks may be uneven)."""
+    w = world(group)
+    if w == 1:
+        return [(int(col0), int(n))]
+    t = torch.zeros((w, 2), dtype=torch.int64, device=device)
+    t[rank(group), 0] = int(col0)
+    t[rank(group), 1] = int(n)
+    allreduce_(t, group=group)
+    return [(int(a), int(b)) for a, b in t.cpu().tolist()]

@@ -3,7 +3,8 @@
 Each rank sketches a contiguous column shard with its global offset (col0). Its partial
 sums are computed by the CPU oracle, which stands in for the device kernels here. The
 product's exchange logic then combines them: ``dist.combine_moments``, and
-``cluster.lloyd_loop`` with its allreduces, global first-argmax and reseed-row broadcast.
+``cluster.lloyd_loop`` with its one packed allreduce per iteration (partials, changed count,
+objective and every rank's (max d2min, global argmax) slot) and the reseed-row exchange.
 The sharded results must equal the unsharded oracle run: sketch bytes and labels
 exactly, sums to fp64 reduction-order tolerance.
 """
@@ -64,24 +65,21 @@ class OracleShardOps:
     def objective(self, d2min, obj):
         obj[0] = self.O.pairwise_sum(d2min.numpy())
 
-    def update(self, labels, mu_prev, group=None):
-        from paper_1511_00152_b200 import dist
-
-        K = mu_prev.shape[1]
+    def partials(self, labels, K):
         lab = labels.numpy().astype(np.int64)
         flat = self.idx_np.astype(np.int64) * K + lab[:, None]
         sums = torch.from_numpy(np.bincount(flat.ravel(), weights=self.val_np.ravel(), minlength=self.p * K)
                                 .reshape(self.p, K))
         counts = torch.from_numpy(np.bincount(flat.ravel(), minlength=self.p * K).reshape(self.p, K))
         sizes = torch.from_numpy(np.bincount(lab, minlength=K).astype(np.int64))
-        for t in (sums, counts, sizes):
-            dist.allreduce_(t, group=group)
+        return sums, counts, sizes
+
+    def centers(self, sums, counts, sizes, mu_prev):
         mu = mu_prev.clone()
         c = counts.to(torch.float64)
         upd = (counts > 0) & (sizes[None, :] > 0)
         mu[upd] = sums[upd] / c[upd]
-        empty = (sizes == 0).to(torch.int32)
-        return mu, counts, empty
+        return mu, (sizes == 0).to(torch.int32)
 
     def reseed(self, mu, empty, idx_row, val_row):
         for k in torch.nonzero(empty).flatten().tolist():
