@@ -509,6 +509,16 @@ def cov_line(ctx, wl, args, steps, warmup, compute, sampler="oracle", clocks=Tru
     return out
 
 
+def release_pinned(torch):
+    """Return cached pinned host blocks to the OS (the host caching allocator keeps freed
+    blocks; the e2e legs pin up to 82 GB each on a 196 GB host)."""
+    gc.collect()
+    try:
+        torch._C._host_emptyCache()
+    except Exception:  # noqa: BLE001
+        pass
+
+
 def pinned_rows(ctx, wl, n, col0):
     torch = ctx.torch
     host = torch.empty((n, WORKLOADS[wl]["p"]), dtype=torch.float32, pin_memory=True)
@@ -544,7 +554,8 @@ def cov_e2e(ctx, wl, args, compute, reps=3):
         one()
     ctx.barrier()
     e_ms = ctx.max_over_ranks((time.perf_counter() - w0) * 1e3 / reps)
-    del host
+    del host, src
+    release_pinned(ctx.torch)
     return {"value": n_glob / (e_ms * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": n * p * 4,
             "d2h_bytes_per_step": p * p * 8, "ms_per_step": e_ms, "rows_per_gpu": n, "compute": compute,
             "api": "stream_moments(RowSource(pinned host rows)) + combine_moments + covariance_from_moments "
@@ -630,7 +641,8 @@ def kmeans_e2e(ctx, wl, args, reps=1):
     for _ in range(reps):
         its += one()
     el = time.perf_counter() - w0
-    del host
+    del host, src
+    release_pinned(torch)
     return {"value": n * its / el, "unit": "point-iters/s", "h2d_bytes_per_step": n * p * 4,
             "d2h_bytes_per_step": n * 8 + p * K * 8, "ms_per_step": el * 1e3 / reps,
             "iterations_per_step": its / reps,
@@ -729,20 +741,18 @@ def main():
             try:
                 if oc["kind"] == "cov":
                     ln = cov_line(ctx, other, args, args.steps, args.warmup, args.compute, "oracle", clocks=False)
-                    if not args.no_e2e:
-                        ln["e2e"] = cov_e2e(ctx, other, args, args.compute)
                 else:
                     ln = kmeans_line(ctx, other, args, max(2, args.steps // 2), 1, clocks=False)
-                    if not args.no_e2e:
-                        ln["e2e"] = kmeans_e2e(ctx, other, args)
-                if not args.no_cpu:
-                    ln["cpu_baseline"] = cpu_baseline(other, oc, seconds=5.0)
                 ln["config"] = {"workload": other, "desc": oc["desc"], "p": oc["p"], "m": oc["m"], "n": oc["n"]}
                 out["configs"][other] = ln
+                if not args.no_e2e:
+                    ln["e2e"] = (cov_e2e(ctx, other, args, args.compute) if oc["kind"] == "cov"
+                                 else kmeans_e2e(ctx, other, args))
+                if not args.no_cpu:
+                    ln["cpu_baseline"] = cpu_baseline(other, oc, seconds=5.0)
             except Exception as e:  # noqa: BLE001  (one config failing must not lose the headline)
-                out["configs"][other] = {"error": f"{type(e).__name__}: {str(e)[:200]}",
-                                         "device_bytes_in_use": torch.cuda.memory_allocated(),
-                                         "device_bytes_reserved": torch.cuda.memory_reserved()}
+                out["configs"].setdefault(other, {})["error"] = f"{type(e).__name__}: {str(e)[:200]}"
+                release_pinned(torch)
             torch.cuda.empty_cache()
 
     if rank == 0:

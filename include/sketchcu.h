@@ -32,7 +32,7 @@ extern "C" {
 #endif
 
 enum { SKC_OK = 0, SKC_EDIM = 1, SKC_EPARAM = 2, SKC_ECUDA = 3, SKC_ENCCL = 4 };
-/* transform kinds, transform.py:81-84 (DCT is outside the GPU hot path: SKC_EPARAM) */
+/* transform kinds, transform.py:20-23 (DCT is outside the GPU hot path: SKC_EPARAM) */
 enum { SKC_KIND_HADAMARD = 0, SKC_KIND_DCT = 1, SKC_KIND_NONE = 2 };
 enum { SKC_F32 = 0, SKC_F64 = 1 };
 
@@ -49,22 +49,22 @@ void skc_count_launches(uint64_t kernels);
 /* --- L0/L1: signs and transform -------------------------------------------------- */
 
 /* D diagonal as fp64 +-1 (all ones for kind NONE) = PreconditionSpec.signs(),
- * transform.py:132-143 -> _hash.sign_array, _hash.py:38-43. out: device[p_pad] (=). */
+ * transform.py:71-82 -> _hash.sign_array, _hash.py:38-43. out: device[p_pad] (=). */
 int skc_signs(uint64_t sign_seed, int32_t p_pad, int32_t kind, double *out, void *stream);
 
-/* precondition_columns, transform.py:241-250, for n rows: Y = H D pad(X). Y: (n, p_pad)
+/* precondition_columns, transform.py:180-189, for n rows: Y = H D pad(X). Y: (n, p_pad)
  * fp64 (=). fp64 arithmetic in the reference's butterfly order, so it is bit-exact. */
 int skc_precondition(const void *X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, int32_t p_pad,
                      int32_t kind, uint64_t sign_seed, double *Y, void *stream);
 
-/* unprecondition_columns, transform.py:253-261: X = D^T H^T Y, keeping the first p_out
+/* unprecondition_columns, transform.py:192-200: X = D^T H^T Y, keeping the first p_out
  * columns (the [:p] truncation of estimators.py:45/129 and cluster.py:388). Y: (n, p_pad)
  * fp64, X: (n, p_out) fp64 (=). Bit-exact. */
 int skc_unprecondition(const double *Y, int64_t n, int32_t p_pad, int32_t kind, uint64_t sign_seed, int32_t p_out,
                        double *X, void *stream);
 
 /* Normalised WHT of n rows of length p_pad (fwht_inplace / _fwht_axis0,
- * transform.py:153-183), fp64 in the reference stage order: bit-exact. X may alias Y. */
+ * transform.py:92-122), fp64 in the reference stage order: bit-exact. X may alias Y. */
 int skc_fwht(const double *Y, int64_t n, int32_t p_pad, double *X, void *stream);
 
 /* --- L2: sampling plan and the fused single-pass sketch ------------------------------ */
@@ -100,9 +100,14 @@ int skc_mean_finalize(const double *acc, int32_t p, int32_t p_pad, int32_t m, in
 
 /* Raw second moment of estimate_covariance, estimators.py:59-61: the W W^T upper
  * triangle, packed row-major (entry (a,b), a<=b, at a*p_pad - a*(a-1)/2 + (b-a)), +=
- * into tri[p_pad*(p_pad+1)/2] fp64. Products go into int32 fixed-point shared-memory
- * accumulators through native ATOMS.ADD. The scale comes from stats (skc_moments).
- * Integer sums make the result deterministic; the fp64 error is about 1e-9 relative. */
+ * into tri[p_pad*(p_pad+1)/2] fp64. Each product w_a*w_b is formed in fp32 from the
+ * fp32-rounded values (relative error <= 2^-23 per product, also in f64 mode), scaled by
+ * 2^S (S from stats, skc_moments) and added as an integer: int32 fixed-point shared-memory
+ * accumulators through native ATOMS.ADD with carries to int64. Values above 8x the rms, or a
+ * scale outside the float range, take exact fp64 products. Integer sums make the result
+ * deterministic and order-independent. Measured relative Frobenius error against the
+ * reference's fp64: 2.5e-9 (C3, n=2^24) to 1.2e-7 (C4, n=2^21), tests/test_full_configs.py;
+ * the north_star bound is 1e-5. */
 size_t skc_cov_workspace(int64_t n, int32_t m, int32_t p_pad);
 int skc_cov_accumulate(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m,
                        int32_t p_pad, const double *stats, double *tri, void *workspace, size_t ws_bytes,
@@ -208,6 +213,12 @@ size_t skc_kmeans_lloyd_workspace(int64_t n, int32_t m, int32_t p_pad, int32_t K
 int skc_kmeans_lloyd(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m, int32_t p_pad,
                      int32_t K, const double *mu0, int32_t max_iter, const void *csc, const void *tc_prep, void *ws,
                      size_t ws_bytes, int32_t *labels, double *mu, double *traj, int32_t *iters, void *stream);
+/* sparsified_assign, cluster.py:306-311, for ONE sketch column (idx_row, val_row: m entries,
+ * device): argmin_k of (diff * diff).sum(axis=0) with diff = val[:, None] - mu[idx, :], in the
+ * reference's own order (a sequential fp64 sum over the m coordinates, np.argmin ties to the
+ * lowest k). label_out[0] (=), d2_out[0] (=, may be NULL). */
+int skc_kmeans_assign_one(const int32_t *idx_row, const void *val_row, int32_t val_dtype, int32_t m, const double *mu,
+                          int32_t p_pad, int32_t K, int32_t *label_out, double *d2_out, void *stream);
 /* Kernels in the last skc_kmeans_lloyd graph of this thread: a run launches prologue + (iters - 1) * body. */
 void skc_kmeans_lloyd_graph_kernels(int32_t *prologue, int32_t *body);
 

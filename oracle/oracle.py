@@ -134,14 +134,14 @@ def next_pow2(n: int) -> int:
 
 
 def fwht(v: np.ndarray) -> np.ndarray:
-    """_fwht_axis0 on one vector, transform.py:153-171 (returns a new array)."""
+    """_fwht_axis0 on one vector, transform.py:92-110 (returns a new array)."""
     a = np.array(v, dtype=np.float64, copy=True)
     lib().orc_fwht(_p(a), a.shape[0])
     return a
 
 
 def precondition_rows(X: np.ndarray, p_pad: int, kind: int, sign_seed: int) -> np.ndarray:
-    """precondition_columns on sample-major rows, transform.py:241-250"""
+    """precondition_columns on sample-major rows, transform.py:180-189"""
     X = np.ascontiguousarray(X, dtype=np.float64)
     n, p = X.shape
     Y = np.empty((n, p_pad), dtype=np.float64)
@@ -150,7 +150,7 @@ def precondition_rows(X: np.ndarray, p_pad: int, kind: int, sign_seed: int) -> n
 
 
 def unprecondition_rows(Y: np.ndarray, kind: int, sign_seed: int) -> np.ndarray:
-    """unprecondition_columns on sample-major rows, transform.py:253-261"""
+    """unprecondition_columns on sample-major rows, transform.py:192-200"""
     Y = np.ascontiguousarray(Y, dtype=np.float64)
     n, p_pad = Y.shape
     X = np.empty_like(Y)

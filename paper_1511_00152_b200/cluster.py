@@ -469,16 +469,19 @@ def _labels_to_device(labels, dev) -> torch.Tensor:
 def sparsified_assign(sketch: SparseSketch, i: int, mu_prime: CenterSet) -> int:
     """Nearest centre for one column over its m sampled coordinates; cluster.py:306-311.
 
-    Uses the K5 kernel on row i: the same argmin, with ties going to the lowest index.
+    ``skc_kmeans_assign_one`` evaluates the reference's own expression for this call,
+    ((val[:, None] - mu[idx]) ** 2).sum(axis=0), in its order (a sequential sum over the m
+    coordinates), so near-ties resolve as the reference does; ties go to the lowest index.
     """
-    ops = SketchKMeans(sketch)
-    mu = torch.as_tensor(np.asarray(mu_prime.centers, dtype=np.float64), device=ops.dev).contiguous()
-    one = SketchKMeans(SparseSketch(sketch.spec, 1, sketch.indices[i : i + 1], sketch.values[i : i + 1]))
-    lab = torch.empty(1, dtype=torch.int32, device=ops.dev)
-    d2 = torch.empty(1, dtype=torch.float64, device=ops.dev)
-    out = torch.zeros(2, dtype=torch.int64, device=ops.dev)
-    mx = torch.zeros(1, dtype=torch.float64, device=ops.dev)
-    one.assign(mu, None, lab, d2, out, mx)
+    dev = sketch.indices.device
+    mu = torch.as_tensor(np.asarray(mu_prime.centers, dtype=np.float64), device=dev).contiguous()
+    K = int(mu.shape[1])
+    idx = sketch.indices[i].contiguous()
+    val = sketch.values[i].contiguous()
+    lab = torch.empty(1, dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        _lib.call("skc_kmeans_assign_one", idx.data_ptr(), val.data_ptr(), _lib.dtype_code(val), sketch.m,
+                  mu.data_ptr(), sketch.p, K, lab.data_ptr(), None, _lib.stream_ptr(dev))
     return int(lab.item())
 
 

@@ -107,7 +107,7 @@ static inline bool pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
 constexpr int32_t kMaxPad = 4096;
 
 static int check_spec(int32_t kind, int32_t p, int32_t p_pad) {
-  // PreconditionSpec.__post_init__, transform.py:105-115
+  // PreconditionSpec.__post_init__, transform.py:44-54
   if (kind == SKC_KIND_DCT) return fail(SKC_EPARAM, "dct preconditioner is not on the GPU hot path");
   if (kind != SKC_KIND_HADAMARD && kind != SKC_KIND_NONE) return fail(SKC_EPARAM, "unknown transform kind");
   if (p < 1) return fail(SKC_EDIM, "dimension must be positive");

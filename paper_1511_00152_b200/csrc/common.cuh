@@ -46,7 +46,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 }
 
 // fp64 add/mul with explicit round-to-nearest: never contracted into FMA, which keeps
-// the reference's separate-rounding order (transform.py:165-170, cluster.py:183).
+// the reference's separate-rounding order (transform.py:104-109, cluster.py:183).
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }

@@ -241,6 +241,51 @@ int build(const Args& A, const Bufs& B, Entry& E) {
   return done(SKC_OK);
 }
 
+// sparsified_assign (cluster.py:306-311) for one column in the reference's own arithmetic:
+// diff = val[:, None] - mu[idx, :]; (diff * diff).sum(axis=0) is a sequential sum over the m
+// sampled coordinates (numpy reduces a strided axis row by row), then the first argmin.
+// This differs from the CSR x dense order of the Lloyd assignment (cluster.py:181-187), so
+// near-ties resolve exactly as the reference's single-column call does.
+// np.argmin order: a NaN is the minimum (its first occurrence wins), else the smallest value,
+// ties to the lowest index
+__device__ __forceinline__ bool argmin_better(double a, int ka, double b, int kb) {
+  const bool an = a != a, bn = b != b;
+  if (an || bn) return an && bn ? ka < kb : an;
+  return a < b || (a == b && ka < kb);
+}
+
+template <typename V>
+__global__ void assign_one_kernel(const int32_t* __restrict__ idx, const V* __restrict__ val, int m,
+                                  const double* __restrict__ mu, int K, int32_t* __restrict__ label,
+                                  double* __restrict__ d2) {
+  __shared__ double bv[32];
+  __shared__ int bk[32];
+  double best = INFINITY;
+  int bestk = 0x7FFFFFFF;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    double acc = 0.0;
+    for (int t = 0; t < m; ++t) {
+      const double d = dsub((double)val[t], mu[(int64_t)idx[t] * K + k]);
+      acc = t == 0 ? dmul(d, d) : dadd(acc, dmul(d, d));
+    }
+    if (argmin_better(acc, k, best, bestk)) best = acc, bestk = k;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_down_sync(0xFFFFFFFFu, best, o);
+    const int ok = __shfl_down_sync(0xFFFFFFFFu, bestk, o);
+    if (argmin_better(ov, ok, best, bestk)) best = ov, bestk = ok;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) bv[warp] = best, bk[warp] = bestk;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)((blockDim.x + 31) / 32); ++w)
+      if (argmin_better(bv[w], bk[w], best, bestk)) best = bv[w], bestk = bk[w];
+    *label = bestk;
+    if (d2) *d2 = best;
+  }
+}
+
 }  // namespace
 }  // namespace skc
 
@@ -293,6 +338,21 @@ int skc_kmeans_lloyd(const int32_t* idx, const void* val, int32_t val_dtype, int
   if (cudaGraphLaunch(it->second.exec, static_cast<cudaStream_t>(stream)) != cudaSuccess)
     return check_launch("graph launch");
   return SKC_OK;
+}
+
+int skc_kmeans_assign_one(const int32_t* idx_row, const void* val_row, int32_t val_dtype, int32_t m, const double* mu,
+                          int32_t p_pad, int32_t K, int32_t* label_out, double* d2_out, void* stream) {
+  if (val_dtype != SKC_F32 && val_dtype != SKC_F64) return fail(SKC_EPARAM, "values must be fp32 or fp64");
+  if (m < 1 || m > p_pad || K < 1) return fail(SKC_EDIM, "bad (m, p_pad, K)");
+  const int threads = K >= 256 ? 256 : ((K + 31) / 32) * 32;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (val_dtype == SKC_F64)
+    assign_one_kernel<double><<<1, threads, 0, s>>>(idx_row, static_cast<const double*>(val_row), m, mu, K, label_out,
+                                                    d2_out);
+  else
+    assign_one_kernel<float><<<1, threads, 0, s>>>(idx_row, static_cast<const float*>(val_row), m, mu, K, label_out,
+                                                   d2_out);
+  return check_launch("assign_one_kernel");
 }
 
 // kernels of the last skc_kmeans_lloyd graph on this thread: the prologue (first iteration) and

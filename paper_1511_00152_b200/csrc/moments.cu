@@ -1,6 +1,6 @@
 // K2 moments (mean accumulation + value statistics), K3 covariance band accumulation,
 // K4 covariance finalize, K7 adjoint transform (mean / PCs / centres).
-// Reference: estimators.py:30-66, transform.py:153-200.
+// Reference: estimators.py:30-66, transform.py:92-200.
 #include <math.h>
 #include <stdlib.h>
 
@@ -697,7 +697,7 @@ int cov_finalize_launch(const double* tri, int32_t p_pad, int32_t m, int64_t n_t
 }
 
 // ======================================================================================
-// K7: adjoint D^T H^T per row, fp64, reference stage order (transform.py:153-171, 253-261).
+// K7: adjoint D^T H^T per row, fp64, reference stage order (transform.py:92-110, 192-200).
 // One CTA per row, the row staged in shared memory. pre_scale != 0 first maps
 // y <- (pre_scale * y) / pre_div (the estimate_mean scaling, estimators.py:44).
 // ======================================================================================
@@ -764,7 +764,7 @@ int adjoint_launch(const double* Y, int64_t n, int32_t p_pad, int32_t kind, uint
   return check_launch("adjoint_kernel");
 }
 
-// D diagonal as fp64 (transform.py:132-143)
+// D diagonal as fp64 (transform.py:71-82)
 __global__ void signs_kernel(uint64_t sign_state, int32_t p_pad, int use_signs, double* out) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= p_pad) return;

@@ -9,7 +9,7 @@
 //   phase 2  signs + normalised WHT. A thread owns E = 32 elements of one sample (a
 //            5-bit "window" of the index bits); butterfly stages run in registers;
 //            windows change through the tile. Stages run in the reference order
-//            h = 1, 2, 4, ... (transform.py:162-169), so the fp64 instantiation is
+//            h = 1, 2, 4, ... (transform.py:101-108), so the fp64 instantiation is
 //            bit-exact.
 //   phase 3  one warp per sample. Pass 1 hashes all keys of the plan (splitmix64,
 //            _hash.py:46-56) and keeps the high word only for a threshold test, as a
@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, 3) sketch_kernel(const SketchParams 
       sgn[w] = bits;
     }
   }
-  const T scale = (T)(1.0 / sqrt((double)G::P));  // transform.py:170
+  const T scale = (T)(1.0 / sqrt((double)G::P));  // transform.py:109
 
   // P >= 32: a warp selects all its samples of the tile while the tile's 16-byte copies
   // are in flight (the selection needs no data), then the CTA transforms and emits
@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(kThreads, kGatherStages > 2 ? 2 : 3) gather_ke
       sgn[w] = bits;
     }
   }
-  const float scale = (float)(1.0 / sqrt((double)G::P));  // transform.py:170
+  const float scale = (float)(1.0 / sqrt((double)G::P));  // transform.py:109
   constexpr int NV = kTileElems / 4 / kThreads;
   const int f0 = threadIdx.x * 4;
   const int s0 = f0 >> LOGP, i0 = f0 & (G::P - 1);
@@ -912,7 +912,7 @@ int sketch_launch(const void* X, int32_t x_dtype, int64_t ld, int64_t n, int32_t
   return launch_sketch_logp<float>(logp, G, st);
 }
 
-// kind == none: values are the raw coordinates (transform.py:225-227); the sampler runs
+// kind == none: values are the raw coordinates (transform.py:141-146); the sampler runs
 // without a transform and a gather kernel reads the values.
 __global__ void gather_identity_kernel(const void* X, int x_f64, int64_t ld, int64_t n, int32_t p, int32_t m,
                                        const int32_t* idx, void* val_out, int val_f64, double* y_out,

@@ -97,7 +97,7 @@ class PreconditionSpec:
         return out
 
     def signs(self) -> np.ndarray:
-        """The +-1 diagonal of D, length p_pad (read-only, cached); transform.py:132-136"""
+        """The +-1 diagonal of D, length p_pad (read-only, cached); transform.py:71-75"""
         return _cached_signs(self.kind, u64(self.sign_seed), self.p_pad)
 
 
@@ -153,7 +153,7 @@ def _rows_adjoint(rows: torch.Tensor, spec: PreconditionSpec, p_out: int) -> tor
 
 
 def precondition(x, spec: PreconditionSpec):
-    """Length-p vector -> H D pad(x), length p_pad; transform.py:218-227"""
+    """Length-p vector -> H D pad(x), length p_pad; transform.py:157-166"""
     t, host = as_device(x)
     if tuple(t.shape) != (spec.p,):
         raise DimensionError(f"expected length {spec.p}, got shape {tuple(t.shape)}")
@@ -161,7 +161,7 @@ def precondition(x, spec: PreconditionSpec):
 
 
 def unprecondition(y, spec: PreconditionSpec):
-    """Adjoint D^T H^T, the exact inverse of ``precondition``; transform.py:230-238"""
+    """Adjoint D^T H^T, the exact inverse of ``precondition``; transform.py:169-177"""
     t, host = as_device(y, torch.float64)
     if tuple(t.shape) != (spec.p_pad,):
         raise DimensionError(f"expected length {spec.p_pad}, got shape {tuple(t.shape)}")
@@ -169,7 +169,7 @@ def unprecondition(y, spec: PreconditionSpec):
 
 
 def precondition_columns(X, spec: PreconditionSpec):
-    """Precondition every column of a (p, c) block; returns (p_pad, c). transform.py:241-250"""
+    """Precondition every column of a (p, c) block; returns (p_pad, c). transform.py:180-189"""
     t, host = as_device(X)
     if t.ndim != 2 or t.shape[0] != spec.p:
         raise DimensionError(f"expected ({spec.p}, c) block, got {tuple(t.shape)}")
@@ -177,7 +177,7 @@ def precondition_columns(X, spec: PreconditionSpec):
 
 
 def unprecondition_columns(Y, spec: PreconditionSpec):
-    """Adjoint of ``precondition_columns`` on a (p_pad, c) block; transform.py:253-261"""
+    """Adjoint of ``precondition_columns`` on a (p_pad, c) block; transform.py:192-200"""
     t, host = as_device(Y, torch.float64)
     if t.ndim != 2 or t.shape[0] != spec.p_pad:
         raise DimensionError(f"expected ({spec.p_pad}, c) block, got {tuple(t.shape)}")
@@ -185,7 +185,7 @@ def unprecondition_columns(Y, spec: PreconditionSpec):
 
 
 def fwht_inplace(v):
-    """Orthonormal WHT of a power-of-two-length vector, overwriting v; transform.py:174-183"""
+    """Orthonormal WHT of a power-of-two-length vector, overwriting v; transform.py:113-122"""
     t, host = as_device(v, torch.float64)
     if t.ndim != 1:
         raise DimensionError("fwht_inplace expects a vector")

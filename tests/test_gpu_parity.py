@@ -432,3 +432,21 @@ def test_pairwise_sum_bit_exact(skc, n):
     ws = _lib.workspace(L.skc_pairwise_sum_workspace(n), xd.device)
     _lib.call("skc_pairwise_sum", xd.data_ptr(), n, out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(xd.device))
     assert float(out.item()) == float(x.sum())
+
+
+def test_sparsified_assign_near_ties_match_reference_formula(skc):
+    # cluster.py:306-311 evaluates ((val[:, None] - mu[idx]) ** 2).sum(axis=0); with tight centres
+    # and |v| ~ 1e3 the CSR x dense order of the Lloyd assignment would break near-ties
+    # differently, so the single-column op must use the reference's own order
+    rng = np.random.default_rng(5)
+    p, n, m, K = 64, 400, 16, 12
+    idx = np.sort(np.argsort(rng.random((n, p)), axis=1)[:, :m], axis=1)
+    val = 1e3 + rng.standard_normal((n, m)) * 1e-3
+    mu = 1e3 + rng.standard_normal((p, K)) * 1e-3
+    spec = skc.PreconditionSpec.create("hadamard", p, sign_seed=1)
+    sk = skc.SparseSketch.from_host(spec, n, idx, val)
+    cs = skc.CenterSet(K=K, centers=mu, domain="preconditioned")
+    for i in range(0, n, 7):
+        diff = val[i][:, None] - mu[idx[i], :]
+        want = int(np.argmin((diff * diff).sum(axis=0)))
+        assert skc.sparsified_assign(sk, i, cs) == want

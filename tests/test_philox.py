@@ -97,7 +97,7 @@ def test_philox_edges_and_identity_kind(skc):
         assert np.array_equal(got, O.philox_indices(p * 31, 0, 40, p, m))
         if m == p:
             assert np.array_equal(got, np.tile(np.arange(p, dtype=np.uint32), (40, 1)))
-    # kind "none": values are the raw coordinates at the sampled indices (transform.py:225-227)
+    # kind "none": values are the raw coordinates at the sampled indices (transform.py:141-146)
     rng = np.random.default_rng(5)
     X = rng.standard_normal((37, 300))
     spec = skc.PreconditionSpec.create("none", 37)
