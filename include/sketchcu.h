@@ -289,6 +289,16 @@ size_t skc_dense_sums_workspace(int64_t n, int32_t p, int32_t K);
 int skc_dense_sums(const void *X, int32_t x_dtype, int64_t ld, int64_t n, int32_t p, const int32_t *labels, int32_t K,
                    double *sums, int64_t *counts, void *ws, void *stream);
 
+/* ---- device top-k eigensolve --------------------------------------
+ * top_eigenvectors(C, k), estimators.py:69-81, on the device: the k largest eigenpairs of
+ * 0.5 * (C + C^T) (C: p x p fp64, device) by cuSOLVER syevdx over the index range [p-k+1, p]
+ * (only k eigenvectors are formed). V: (p, k) row-major, columns in descending eigenvalue order
+ * (the reference's V[:, ::-1][:, :k]); w: (k) descending eigenvalues, may be NULL (=).
+ * Eigenvector signs are arbitrary, as in LAPACK. ws: skc_top_eigenvectors_workspace bytes. */
+size_t skc_top_eigenvectors_workspace(int32_t p, int32_t k);
+int skc_top_eigenvectors(const double *C, int32_t p, int32_t k, double *V, double *w, void *ws, size_t ws_bytes,
+                         void *stream);
+
 /* ---- sample-sharded exchange (SURVEY 8(e); SPEC.md:212, :352 ordered combine of partials) ----
  * Rank r holds global columns [col0, col0 + n) and runs every entry point above on its shard
  * with that col0. Per pass, ONE fp64 SUM allreduce of the packed moments buffer

@@ -17,7 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "_lib")
 SO = os.path.join(OUT, "libsketchcu.so")
-SOURCES = ["capi.cu", "sketch.cu", "moments.cu", "cov_tc.cu", "kmeans.cu", "kmeans_tc.cu", "formats.cu", "dense.cu", "gather.cu", "lloyd.cu", "comm.cu"]
+SOURCES = ["capi.cu", "sketch.cu", "moments.cu", "cov_tc.cu", "kmeans.cu", "kmeans_tc.cu", "formats.cu", "dense.cu", "gather.cu", "lloyd.cu", "comm.cu", "eig.cu"]
 HEADERS = [os.path.join(CSRC, "common.cuh"), os.path.join(ROOT, "include", "sketchcu.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -52,7 +52,7 @@ def build(verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(_compile, SOURCES))
     if _newer(SO, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", SO, *objs, "-lcudart", "-ldl"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", SO, *objs, "-lcudart", "-ldl", "-lcusolver"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")

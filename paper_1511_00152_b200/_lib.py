@@ -79,6 +79,8 @@ SIGNATURES = {
                                       _P, _P, _P, _P, _SZ, _P]),
     "skc_sketch_pack_records": (_c.c_int, [_P, _P, _I32, _I64, _I32, _P, _P]),
     "skc_sketch_unpack_records": (_c.c_int, [_P, _I64, _I32, _P, _P, _P]),
+    "skc_top_eigenvectors_workspace": (_SZ, [_I32, _I32]),
+    "skc_top_eigenvectors": (_c.c_int, [_P, _I32, _I32, _P, _P, _P, _SZ, _P]),
     "skc_nccl_get_unique_id": (_c.c_int, [_P]),
     "skc_nccl_comm_init_rank": (_c.c_int, [_P, _I32, _P, _I32]),
     "skc_nccl_comm_destroy": (_c.c_int, [_P]),

@@ -186,15 +186,16 @@ def top_eigenvectors(C, k: int, solver: str = "host"):
     """Eigenvectors of the k largest eigenvalues as columns; estimators.py:69-81.
 
     ``solver="host"`` (default) runs LAPACK ``eigh`` through numpy, exactly as the reference.
-    ``solver="device"`` keeps C on the GPU and runs cuSOLVER ``syevd`` (``torch.linalg.eigh``),
-    returning a CUDA tensor: the same eigenpairs up to each vector's sign, within the
-    eigensolver's rounding. Both check symmetry as the reference does.
+    ``solver="device"`` keeps C on the GPU and computes only the k largest eigenpairs
+    (``skc_top_eigenvectors``: cuSOLVER syevdx over an index range), returning a CUDA tensor:
+    the same eigenvectors up to each one's sign, within the eigensolver's rounding (SURVEY 8(f)
+    row 2). Both check symmetry as the reference does.
     """
     if solver not in ("host", "device"):
         raise ParameterError(f"unknown solver {solver!r}")
     if solver == "device":
         Cd = C if isinstance(C, torch.Tensor) else torch.as_tensor(np.asarray(C, dtype=np.float64))
-        Cd = Cd.to(dtype=torch.float64, device=Cd.device if Cd.is_cuda else default_device())
+        Cd = Cd.to(dtype=torch.float64, device=Cd.device if Cd.is_cuda else default_device()).contiguous()
         if Cd.ndim != 2 or Cd.shape[0] != Cd.shape[1]:
             raise ParameterError("expected a square matrix")
         p = Cd.shape[0]
@@ -203,8 +204,13 @@ def top_eigenvectors(C, k: int, solver: str = "host"):
         scale = max(float(Cd.abs().max()), 1e-300)
         if float((Cd - Cd.T).abs().max()) > SYMMETRY_RTOL * scale:
             raise ParameterError("matrix is not symmetric within tolerance")
-        _, V = torch.linalg.eigh(0.5 * (Cd + Cd.T))
-        return V.flip(1)[:, :k].contiguous()
+        L = _lib.lib()
+        V = torch.empty((p, k), dtype=torch.float64, device=Cd.device)
+        with torch.cuda.device(Cd.device):
+            ws = _lib.workspace(L.skc_top_eigenvectors_workspace(p, k), Cd.device)
+            _lib.call("skc_top_eigenvectors", Cd.data_ptr(), p, k, V.data_ptr(), None, ws.data_ptr(), ws.numel(),
+                      _lib.stream_ptr(Cd.device))
+        return V
     C = C.cpu().numpy() if isinstance(C, torch.Tensor) else np.asarray(C, dtype=np.float64)
     if C.ndim != 2 or C.shape[0] != C.shape[1]:
         raise ParameterError("expected a square matrix")
