@@ -49,21 +49,26 @@ __device__ double pw_rec(const double* a, int64_t n) {
   return dadd(pw_rec(a, n2), pw_rec(a + n2, n - n2));
 }
 
-constexpr int kPwDeep = 14;  // subtrees at depth 14: one thread each, 64 blocks
+constexpr int kPwDeep = 14;  // deepest split level handled by the combine (2^14 subtrees)
 
+// numpy's tree is cut at depth D (runtime, <= kPwDeep, about log2(n / 128)) into 2^D paths.
 // res[t]: the sum of path t's subtree; ld[t]: the depth at which path t reaches a leaf (<= 128
-// elements), kPwDeep if it does not. Node t of depth d (stored at t << (kPwDeep - d)) is an internal
-// node of numpy's tree exactly when ld[t << (kPwDeep - d)] > d.
-__global__ void __launch_bounds__(256) pairwise_leaves_kernel(const double* __restrict__ x, int64_t n,
+// elements), D if it does not. Node t of depth d (stored at t << (D - d)) is an internal node of
+// numpy's tree exactly when ld[t << (D - d)] > d. Eight lanes share a path: a leaf's eight
+// accumulators r[k] = a[k] + a[k+8] + ... run one per lane (coalesced 64-byte steps), then
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by shuffles and the tail by lane 0 -- pw_leaf's order.
+__global__ void __launch_bounds__(256) pairwise_leaves_kernel(const double* __restrict__ x, int64_t n, int D,
                                                               double* __restrict__ res, uint8_t* __restrict__ ld) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;  // path of depth kPwDeep
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = gt >> 3, k = gt & 7;  // path, lane within the path's group
+  if (t >= (1 << D)) return;           // whole groups exit together (8 | 256)
   int64_t off = 0, len = n;
   bool active = true;
-  int leafd = kPwDeep;
-  for (int d = 0; d < kPwDeep; ++d) {
-    const int bit = (t >> (kPwDeep - 1 - d)) & 1;
+  int leafd = D;
+  for (int d = 0; d < D; ++d) {
+    const int bit = (t >> (D - 1 - d)) & 1;
     if (len <= 128) {  // leaf above the split depth: owned by the all-zero suffix path
-      if (leafd == kPwDeep) leafd = d;
+      if (leafd == D) leafd = d;
       if (bit) active = false;
       continue;
     }
@@ -76,27 +81,47 @@ __global__ void __launch_bounds__(256) pairwise_leaves_kernel(const double* __re
       len = n2;
     }
   }
-  res[t] = active ? pw_rec(x + off, len) : 0.0;
-  ld[t] = (uint8_t)leafd;
+  double r = 0.0;
+  const double* a = x + off;
+  const unsigned gmask = 0xFFu << (threadIdx.x & 24);
+  if (active && len <= 128 && len >= 8) {
+    r = a[k];
+    const int64_t body = len - (len % 8);
+    for (int64_t i = 8 + k; i < body; i += 8) r = dadd(r, a[i]);
+    const double r1 = __shfl_down_sync(gmask, r, 1, 8);
+    const double s01 = dadd(r, r1);
+    const double s23 = __shfl_down_sync(gmask, s01, 2, 8);
+    const double q = dadd(s01, s23);
+    const double q2 = __shfl_down_sync(gmask, q, 4, 8);
+    if (k == 0) {
+      r = dadd(q, q2);
+      for (int64_t i = body; i < len; ++i) r = dadd(r, a[i]);
+    }
+  } else if (k == 0 && active) {
+    r = len <= 128 ? pw_leaf(a, len) : pw_rec(a, len);
+  }
+  if (k == 0) {
+    res[t] = active ? r : 0.0;
+    ld[t] = (uint8_t)leafd;
+  }
 }
 
-// The 2^kPwDeep subtree sums are combined in shared memory (128 KB), level by level; whether a
-// node is internal comes from ld (one lookup instead of re-walking its path).
+// The 2^D subtree sums are combined in shared memory, level by level; whether a node is internal
+// comes from ld (one lookup instead of re-walking its path).
 __global__ void __launch_bounds__(1024) pairwise_combine_kernel(const double* __restrict__ gres,
-                                                                const uint8_t* __restrict__ gld, int64_t n,
+                                                                const uint8_t* __restrict__ gld, int D,
                                                                 double* __restrict__ out) {
   extern __shared__ double res[];
   uint8_t* ld = reinterpret_cast<uint8_t*>(res + (1 << kPwDeep));
-  for (int t = threadIdx.x; t < (1 << kPwDeep); t += blockDim.x) res[t] = gres[t], ld[t] = gld[t];
+  for (int t = threadIdx.x; t < (1 << D); t += blockDim.x) res[t] = gres[t], ld[t] = gld[t];
   __syncthreads();
-  for (int d = kPwDeep - 1; d >= 0; --d) {
-    const int sh = kPwDeep - d;
+  for (int d = D - 1; d >= 0; --d) {
+    const int sh = D - d;
     for (int t = threadIdx.x; t < (1 << d); t += blockDim.x)
       if (ld[t << sh] > d) res[t << sh] = dadd(res[(2 * t) << (sh - 1)], res[(2 * t + 1) << (sh - 1)]);
     __syncthreads();
   }
   if (threadIdx.x == 0) out[0] = res[0];
-  (void)n;
 }
 
 size_t pairwise_ws() { return ((size_t)1 << kPwDeep) * (sizeof(double) + 1); }
@@ -104,12 +129,15 @@ size_t pairwise_ws() { return ((size_t)1 << kPwDeep) * (sizeof(double) + 1); }
 int pairwise_launch(const double* x, int64_t n, double* out, void* ws, cudaStream_t st) {
   double* res = reinterpret_cast<double*>(ws);
   uint8_t* ld = reinterpret_cast<uint8_t*>(res + (1 << kPwDeep));
-  pairwise_leaves_kernel<<<(1 << kPwDeep) / 256, 256, 0, st>>>(x, n, res, ld);
+  int D = 0;
+  while (D < kPwDeep && ((int64_t)128 << D) < n) ++D;  // leaves of <= ~128 elements at depth <= D
+  const int threads = 8 << D;
+  pairwise_leaves_kernel<<<(threads + 255) / 256, 256, 0, st>>>(x, n, D, res, ld);
   int rc = check_launch("pairwise_leaves_kernel");
   if (rc) return rc;
   const size_t smem = ((size_t)1 << kPwDeep) * (sizeof(double) + 1);
   cudaFuncSetAttribute(pairwise_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  pairwise_combine_kernel<<<1, 1024, smem, st>>>(res, ld, n, out);
+  pairwise_combine_kernel<<<1, 1024, smem, st>>>(res, ld, D, out);
   return check_launch("pairwise_combine_kernel");
 }
 
@@ -293,6 +321,125 @@ __global__ void __launch_bounds__(kAsgWarps * 32, 4)
         mx = s_mx[w];
         a = s_arg[w];
       }
+    }
+    blk_changed[blockIdx.x] = c;
+    blk_max[blockIdx.x] = mx;
+    blk_arg[blockIdx.x] = a;
+  }
+}
+
+// K5s: the exact assignment for small K (K <= 16, e.g. C2), one point per thread. The thread
+// keeps K accumulators in registers (K independent fp64 chains hide the add latency) and reads
+// the point's table rows as 16-byte vectors from L1: d2[k] = (sum_t v_t * (-2 mu[j_t,k]) then
+// + sum_t mu[j_t,k]^2, t ascending: csr_matvecs' axpy order, cluster.py:181-187) + colsq (numpy
+// pairwise order), first minimum over k, clipped at 0: the same arithmetic as km_assign_kernel,
+// so labels and d2min are bit-identical. Tables: [p][KC] planes, KC = K rounded up to even.
+__global__ void km_tables_pad_kernel(const double* __restrict__ mu, int p, int K, int KC, double* __restrict__ tx,
+                                     double* __restrict__ ty) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)p * KC) return;
+  const int j = (int)(e / KC), k = (int)(e % KC);
+  const double v = k < K ? mu[(int64_t)j * K + k] : 0.0;
+  tx[e] = dmul(-2.0, v);
+  ty[e] = dmul(v, v);
+}
+
+__device__ __forceinline__ double colsq_pairwise(const int32_t* __restrict__ ir, const void* val, int64_t base, int m,
+                                                 bool f64) {
+  (void)ir;
+  auto ld = [&](int t) -> double {
+    return f64 ? __ldg(reinterpret_cast<const double*>(val) + base + t)
+               : (double)__ldg(reinterpret_cast<const float*>(val) + base + t);
+  };
+  if (m < 8) {
+    double c = 0.0;
+    for (int t = 0; t < m; ++t) c = dadd(c, dmul(ld(t), ld(t)));
+    return c;
+  }
+  if (m <= 128) {
+    double r[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = dmul(ld(k), ld(k));
+    int t = 8;
+    for (; t < m - (m % 8); t += 8)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[k] = dadd(r[k], dmul(ld(t + k), ld(t + k)));
+    double c = dadd(dadd(dadd(r[0], r[1]), dadd(r[2], r[3])), dadd(dadd(r[4], r[5]), dadd(r[6], r[7])));
+    for (; t < m; ++t) c = dadd(c, dmul(ld(t), ld(t)));
+    return c;
+  }
+  return -1.0;  // m > 128: the caller takes km_assign_kernel
+}
+
+constexpr int kSmallThreads = 256;
+template <typename V, int KC>
+__global__ void __launch_bounds__(kSmallThreads, 2) km_assign_small_kernel(
+    const int32_t* __restrict__ idx, const void* __restrict__ val, int64_t n, int m, const double* __restrict__ tx,
+    const double* __restrict__ ty, int K, const int32_t* __restrict__ prev, int32_t* __restrict__ labels,
+    double* __restrict__ d2min, int64_t* __restrict__ blk_changed, double* __restrict__ blk_max,
+    int64_t* __restrict__ blk_arg) {
+  constexpr bool F64 = sizeof(V) == 8;
+  int64_t changed = 0;
+  double bmax = -1.0;
+  int64_t barg = -1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int32_t* ir = idx + i * m;
+    const V* vr = reinterpret_cast<const V*>(val) + i * m;
+    double acc[KC];
+#pragma unroll
+    for (int k = 0; k < KC; ++k) acc[k] = 0.0;
+    for (int t = 0; t < m; ++t) {
+      const double v = (double)__ldg(vr + t);
+      const double2* row = reinterpret_cast<const double2*>(tx + (size_t)__ldg(ir + t) * KC);
+#pragma unroll
+      for (int c = 0; c < KC / 2; ++c) {
+        const double2 a = __ldg(row + c);
+        acc[2 * c] = dadd(acc[2 * c], dmul(v, a.x));
+        acc[2 * c + 1] = dadd(acc[2 * c + 1], dmul(v, a.y));
+      }
+    }
+    for (int t = 0; t < m; ++t) {
+      const double2* row = reinterpret_cast<const double2*>(ty + (size_t)__ldg(ir + t) * KC);
+#pragma unroll
+      for (int c = 0; c < KC / 2; ++c) {
+        const double2 b = __ldg(row + c);
+        acc[2 * c] = dadd(acc[2 * c], b.x);
+        acc[2 * c + 1] = dadd(acc[2 * c + 1], b.y);
+      }
+    }
+    const double colsq = colsq_pairwise(ir, val, i * m, m, F64);
+    double best = dadd(acc[0], colsq);
+    int bk = 0;
+#pragma unroll
+    for (int k = 1; k < KC; ++k) {
+      const double d = dadd(acc[k], colsq);
+      if (k < K && d < best) best = d, bk = k;
+    }
+    const double dm = best > 0.0 ? best : 0.0;  // np.clip(.., 0, None)
+    labels[i] = bk;
+    d2min[i] = dm;
+    if (prev != nullptr) changed += prev[i] != bk;
+    if (dm > bmax) bmax = dm, barg = i;  // ascending i per thread: keeps the first max
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t oc = __shfl_xor_sync(kFM, changed, o), oa = __shfl_xor_sync(kFM, barg, o);
+    const double om = __shfl_xor_sync(kFM, bmax, o);
+    changed += oc;
+    if (oa >= 0 && (om > bmax || (om == bmax && (barg < 0 || oa < barg)))) bmax = om, barg = oa;
+  }
+  __shared__ int64_t s_ch[kSmallThreads / 32], s_arg[kSmallThreads / 32];
+  __shared__ double s_mx[kSmallThreads / 32];
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) s_ch[warp] = changed, s_mx[warp] = bmax, s_arg[warp] = barg;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t c = 0, a = -1;
+    double mx = -1.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      c += s_ch[w];
+      if (s_arg[w] >= 0 && (s_mx[w] > mx || (s_mx[w] == mx && (a < 0 || s_arg[w] < a)))) mx = s_mx[w], a = s_arg[w];
     }
     blk_changed[blockIdx.x] = c;
     blk_max[blockIdx.x] = mx;
@@ -610,10 +757,12 @@ static int assign_grid(int64_t n) {
   return (int)(g < 1 ? 1 : g);
 }
 
+// tables: 2 p_pad * K doubles ([-2 mu] and [mu * mu] planes), or the padded planes of K5s
+static size_t assign_tab_doubles(int32_t p_pad, int32_t K) { return (size_t)2 * p_pad * ((K + 1) & ~1); }
 size_t assign_ws(int64_t n, int32_t p_pad, int32_t K) {
-  // [double2 table][per-block changed/max/arg][fp32 table for K5f]
-  return (size_t)2 * p_pad * K * sizeof(double) + (size_t)assign_grid(n) * 24 + (size_t)p_pad * ((K + 3) & ~3) * 4 +
-         128;
+  // [tables][per-block changed/max/arg][fp32 table for K5f]
+  return assign_tab_doubles(p_pad, K) * sizeof(double) + (size_t)assign_grid(n) * 24 +
+         (size_t)p_pad * ((K + 3) & ~3) * 4 + 128;
 }
 // K5f instead of K5 when the packed table does not fit the shared-memory budget (SKC_ASSIGN_EXACT=1
 // keeps K5, for A/B runs and the bit-equality test)
@@ -653,7 +802,47 @@ int assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, i
   double* tx = reinterpret_cast<double*>(ws);  // [-2 mu] plane, then the [mu * mu] plane
   double* ty = tx + (size_t)p_pad * K;
   const int G = assign_grid(n);
-  int64_t* bch = reinterpret_cast<int64_t*>(ty + (size_t)p_pad * K);
+  int64_t* bch = reinterpret_cast<int64_t*>(tx + assign_tab_doubles(p_pad, K));
+  // K5s for small tables: one point per thread (SKC_ASSIGN_SMALL=0 keeps the warp kernel)
+  static const bool small_on = [] {
+    const char* e = getenv("SKC_ASSIGN_SMALL");
+    return !(e && e[0] == '0');
+  }();
+  if (n > 0 && small_on && K <= 16 && m <= 128 && !use_filter(p_pad, K)) {
+    const int KC = (K + 1) & ~1;
+    double* tx2 = tx;
+    double* ty2 = tx + (size_t)p_pad * KC;
+    const int64_t tot = (int64_t)p_pad * KC;
+    km_tables_pad_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(mu, p_pad, K, KC, tx2, ty2);
+    int rc = check_launch("km_tables_pad_kernel");
+    if (rc) return rc;
+    int64_t Gs = (n + kSmallThreads - 1) / kSmallThreads;
+    if (Gs > G) Gs = G;  // the per-block arrays hold G entries
+    auto go = [&](auto kern) {
+      kern<<<(unsigned)Gs, kSmallThreads, 0, st>>>(idx, val, n, m, tx2, ty2, K, prev, labels, d2min, bch,
+                                         reinterpret_cast<double*>(bch + G), reinterpret_cast<int64_t*>(bch + 2 * G));
+    };
+#define SKC_SMALL_CASE(KK)                                                              \
+  case KK:                                                                              \
+    if (val_f64) go(km_assign_small_kernel<double, KK>);                                \
+    else go(km_assign_small_kernel<float, KK>);                                         \
+    break;
+    switch (KC) {
+      SKC_SMALL_CASE(2)
+      SKC_SMALL_CASE(4)
+      SKC_SMALL_CASE(6)
+      SKC_SMALL_CASE(8)
+      SKC_SMALL_CASE(10)
+      SKC_SMALL_CASE(12)
+      SKC_SMALL_CASE(14)
+      SKC_SMALL_CASE(16)
+    }
+#undef SKC_SMALL_CASE
+    if ((rc = check_launch("km_assign_small_kernel"))) return rc;
+    km_assign_reduce_kernel<<<1, 1024, 0, st>>>(bch, reinterpret_cast<double*>(bch + G),
+                                                reinterpret_cast<int64_t*>(bch + 2 * G), (int)Gs, out, d2max);
+    return check_launch("km_assign_reduce_kernel");
+  }
   double* bmx = reinterpret_cast<double*>(bch + G);
   int64_t* barg = reinterpret_cast<int64_t*>(bmx + G);
   const int64_t total = (int64_t)p_pad * K;
