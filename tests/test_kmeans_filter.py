@@ -163,3 +163,30 @@ def test_filters_at_extreme_scales(skc, monkeypatch, scale):
         assert np.array_equal(a[0], b[0]), "labels"
         assert np.array_equal(a[1], b[1]), "d2min"
         assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3]), "changed / farthest point"
+
+
+@pytest.mark.parametrize("p,m,K,n,compute,init", [
+    (2048, 102, 100, 20000, "f64", "points"),  # C5 shape: the first iteration from seeded points
+    (1024, 51, 33, 9001, "f32", "points"),     # fp32 values, ragged K and n
+    (512, 26, 256, 4000, "f64", "points"),     # the largest K of K5f
+    (2048, 102, 100, 5000, "f64", "dense"),    # dense centres
+])
+def test_first_iteration_filter_equals_exact(skc, monkeypatch, p, m, K, n, compute, init):
+    """The first Lloyd assignment (no previous labels) from seeded points, whose centres are
+    sketch columns (nearly every point has near-ties): K5f's outputs equal K5's bit for bit."""
+    rng = np.random.default_rng(p + 3 * K + n)
+    C = rng.standard_normal((p, K)) * 3.0
+    lab = rng.integers(0, K, n)
+    X = (C[:, lab] + rng.standard_normal((p, n))).astype(np.float32)
+    spec = skc.PreconditionSpec.create("hadamard", p, 3)
+    sk = skc.sketch_stream(X, spec, skc.SamplingPlan(4, spec.p_pad, m), compute=compute)
+    dev = sk.indices.device
+    if init == "points":
+        mu = skc.SketchKMeans(sk).init_centers(rng.choice(n, K, replace=False))
+    else:
+        mu = torch.as_tensor(rng.standard_normal((spec.p_pad, K)), device=dev)
+    a = _assign(skc, sk, mu, None, True, monkeypatch)
+    b = _assign(skc, sk, mu, None, False, monkeypatch)
+    assert np.array_equal(a[0], b[0]), "labels"
+    assert np.array_equal(a[1], b[1]), "d2min"
+    assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3]), "changed / farthest point"
