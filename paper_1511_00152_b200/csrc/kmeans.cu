@@ -857,7 +857,6 @@ int assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, i
     const size_t smem = filt_warp_bytes(m, K) * kFiltWarps;
     int Gf = (int)((n + kFiltWarps - 1) / kFiltWarps);
     if (Gf > G) Gf = G;  // the per-block arrays hold G entries
-
     const int nb = (K4 + 127) / 128;
     auto go = [&](auto kern) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1314,47 +1313,15 @@ __global__ void __launch_bounds__(kTileThreads, SKC_TILE_MINB) km_tile_walk_kern
   const uint32_t ltm = lanemask_lt();
   double acc[(kTileMaxK + kTileThreads - 1) / kTileThreads] = {0.0};
   int64_t cntk[(kTileMaxK + kTileThreads - 1) / kTileThreads] = {0};
-  // software pipeline: tile t+1's rows and values load into registers while tile t is sorted,
-  // and its labels are gathered while tile t's chains are summed
-  constexpr int kPer = kTileE / kTileThreads;
-  int nrow[kPer];
-  double nval[kPer];
-  uint8_t nlab[kPer];
-  auto load_rv = [&](int64_t t0) {
-    const int L = (int)min((int64_t)kTileE, b - t0);
-#pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-      const int e = tid + q * kTileThreads;
-      nrow[q] = e < L ? __ldg(rows + t0 + e) : 0;
-      nval[q] = e < L ? (double)__ldg(vals + t0 + e) : 0.0;
-    }
-  };
-  auto load_lab = [&](int64_t t0) {
-    const int L = (int)min((int64_t)kTileE, b - t0);
-#pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-      const int e = tid + q * kTileThreads;
-      nlab[q] = e < L ? (uint8_t)__ldg(labels + nrow[q]) : 0;
-    }
-  };
-  if (a < b) {
-    load_rv(a);
-    load_lab(a);
-  }
   for (int64_t t0 = a; t0 < b; t0 += kTileE) {
     const int L = (int)min((int64_t)kTileE, b - t0);
     for (int q = tid; q < kTileWarps * K; q += kTileThreads) wc[q] = 0;
-    // stage: this tile's values and labels from registers
-#pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-      const int e = tid + q * kTileThreads;
-      if (e < L) {
-        tv[e] = nval[q];
-        tl[e] = nlab[q];
-      }
+    // stage: values and gathered labels (all loads of a thread in flight together)
+#pragma unroll 4
+    for (int e = tid; e < L; e += kTileThreads) {
+      tv[e] = (double)__ldg(vals + t0 + e);
+      tl[e] = (uint8_t)__ldg(labels + __ldg(rows + t0 + e));
     }
-    const bool more = t0 + kTileE < b;
-    if (more) load_rv(t0 + kTileE);
     __syncthreads();
     // per-warp label counts over the warp's contiguous sub-range
     const int s0 = (int)((int64_t)L * warp / kTileWarps), s1 = (int)((int64_t)L * (warp + 1) / kTileWarps);
@@ -1405,7 +1372,6 @@ __global__ void __launch_bounds__(kTileThreads, SKC_TILE_MINB) km_tile_walk_kern
       __syncwarp();
     }
     __syncthreads();
-    if (more) load_lab(t0 + kTileE);  // in flight during the chains
     // chains: thread k adds label k's run in order (loads ahead of the dependent adds)
 #pragma unroll
     for (int u = 0; u < (kTileMaxK + kTileThreads - 1) / kTileThreads; ++u) {
