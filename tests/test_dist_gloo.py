@@ -106,15 +106,39 @@ def _worker(rank, world, port, outdir):
     C = O.cov_acc(idx, val, p_pad)
     tri = torch.from_numpy(C[np.triu_indices(p_pad)].copy())
     n_tot = dist.combine_moments(acc, stats, tri, c1 - c0)
-    # --- K-means: sharded Lloyd loop; a duplicated start point forces an empty cluster ---
+    # the same partials in one packed Moments buffer: exactly ONE collective for the pass
+    from paper_1511_00152_b200.estimators import Moments
+
+    calls = []
+    real_allreduce = dist.allreduce_
+
+    def counting_allreduce(t, op=None, group=None):
+        calls.append(t.numel())
+        return real_allreduce(t, op=op, group=group)
+
+    dist.allreduce_ = counting_allreduce
+    mom = Moments.zeros(p_pad, True, torch.device("cpu"))
+    mom.acc.copy_(torch.from_numpy(O.mean_acc(idx, val, p_pad)))
+    mom.stats.copy_(torch.tensor([float((val * val).sum()), float(np.abs(val).max()), float(c1 - c0)]))
+    mom.tri.copy_(torch.from_numpy(C[np.triu_indices(p_pad)].copy()))
+    n_packed = dist.combine_moments(mom.acc, mom.stats, mom.tri, c1 - c0)
+    pass_calls = list(calls)
+    # --- K-means: sharded Lloyd loop on UNEVEN shards (the reseed owner comes from every rank's
+    # actual range); a duplicated start point forces an empty cluster ---
     K = 6
     idx_full, val_full = O.sketch(X.T.copy(), p_pad, O.HADAMARD, ss, ms, m)
+    u0, u1 = (0, 1000) if rank == 0 else (1000, n)
     chosen = [5, 5, 100, 2000, 2999, 1500]
     mu0 = torch.from_numpy(O.init_centers(idx_full, val_full, chosen, p_pad))
-    ops = OracleShardOps(idx, val, c0, p_pad)
+    ops = OracleShardOps(idx_full[u0:u1], val_full[u0:u1], u0, p_pad)
+    calls.clear()
     labels, mu, traj, iters, _ = lloyd_loop(ops, mu0, 30, None)
+    loop_calls = list(calls)
+    dist.allreduce_ = real_allreduce
     np.savez(os.path.join(outdir, f"r{rank}.npz"), idx=idx, val=val, acc=acc.numpy(), stats=stats.numpy(),
-             tri=tri.numpy(), n_tot=n_tot, labels=labels.numpy(), mu=mu.numpy(), traj=np.array(traj), iters=iters)
+             tri=tri.numpy(), n_tot=n_tot, labels=labels.numpy(), mu=mu.numpy(), traj=np.array(traj), iters=iters,
+             packed=mom.packed.numpy(), n_packed=n_packed, pass_calls=np.array(pass_calls),
+             loop_calls=np.array(loop_calls), shard=np.array([u0, u1]))
     tdist.barrier()
     tdist.destroy_process_group()
 
@@ -163,3 +187,33 @@ def test_sharded_lloyd_matches_single_process(sharded):
     assert np.allclose(sharded[0]["traj"], traj, rtol=1e-12)
     assert np.allclose(sharded[0]["mu"], mu, rtol=1e-12, atol=1e-12)
     assert np.array_equal(sharded[0]["mu"], sharded[1]["mu"])
+
+
+def test_one_collective_per_pass_and_per_iteration(sharded):
+    """SPEC.md:212/:352 combine: the packed moments take ONE allreduce per pass; the Lloyd loop
+    takes ONE per iteration (the packed exchange), plus one per iteration that empties a
+    cluster (the reseed row), plus one at the start (every rank's range)."""
+    for r in sharded:
+        assert list(r["pass_calls"]) == [64 + 3 + 64 * 65 // 2]
+        assert np.allclose(r["packed"][:64], sharded[0]["acc"], rtol=1e-12, atol=1e-12)
+        assert int(r["n_packed"]) == int(r["n_tot"])
+        calls = list(r["loop_calls"])
+        it = int(r["iters"])
+        exchange = 2 * 64 * 6 + 6 + 2 + 2 * 2  # sums, counts, sizes, changed, objective, 2 rank slots
+        assert calls[0] == 4  # shard_ranges: (col0, n) of the 2 ranks
+        assert calls.count(exchange) == it
+        reseeds = [c for c in calls[1:] if c != exchange]
+        assert all(c == 2 * 12 for c in reseeds) and len(reseeds) >= 1  # the forced empty cluster
+
+
+def test_uneven_shards_lloyd_matches_single_process(sharded):
+    from oracle import oracle as O
+
+    X = _data()
+    idx, val = O.sketch(X.T.copy(), 64, O.HADAMARD, 11, 12, 12)
+    mu0 = O.init_centers(idx, val, [5, 5, 100, 2000, 2999, 1500], 64)
+    lo, muo, to, io = O.lloyd(idx, val, mu0, 30)
+    labels = np.concatenate([r["labels"] for r in sharded])
+    assert [tuple(r["shard"]) for r in sharded] == [(0, 1000), (1000, 3001)]
+    assert np.array_equal(labels, lo) and int(sharded[0]["iters"]) == io
+    assert np.allclose(sharded[0]["mu"], muo, rtol=1e-12, atol=1e-12)
