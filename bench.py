@@ -28,6 +28,7 @@ import statistics
 import subprocess
 import sys
 import tempfile
+import threading
 import time
 
 import numpy as np
@@ -152,41 +153,84 @@ def gen_rows_np(wl: str, n: int, seed: int = SEED) -> np.ndarray:
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    def __init__(self, index: int):
-        self.index = index
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        self.p = None
+    """SM clock and throttle reasons sampled DURING the timed region.
+
+    NVML polled every 5 ms from a thread (short regions still get samples), else the
+    recipe's ``nvidia-smi --query-gpu=... -lms 100`` line."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
+
+    def __init__(self, index: int, pci_bus_id: str = None):
+        self.index, self.pci = index, pci_bus_id
+        self.rows, self.max_mhz, self.source = [], None, None
+        self.stop = threading.Event()
+        self.thread = self.p = self.f = None
+
+    def _nvml_loop(self, N, h):
+        bits = [(name, getattr(N, const, 0)) for name, const in self.REASONS]
+        while not self.stop.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                util = N.nvmlDeviceGetUtilizationRates(h).gpu
+                self.rows.append((float(sm), [name for name, b in bits if r & b], int(util)))
+            except Exception:
+                pass
+            self.stop.wait(0.005)
 
     def __enter__(self):
         try:
+            import pynvml as N
+
+            N.nvmlInit()
+            h = (N.nvmlDeviceGetHandleByPciBusId(self.pci) if self.pci else N.nvmlDeviceGetHandleByIndex(self.index))
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            self.source = "nvml 5 ms"
+            self.thread = threading.Thread(target=self._nvml_loop, args=(N, h), daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.thread = None
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
             self.p = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}",
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu",
                  "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+            self.source = "nvidia-smi 100 ms"
         except Exception:
             self.p = None
         return self
 
     def __exit__(self, *a):
+        if self.thread is not None:
+            self.stop.set()
+            self.thread.join()
         if self.p is not None:
             self.p.terminate()
             self.p.wait()
+            self.f.flush()
+            self.f.seek(0)
+            for r in (r.split(",") for r in self.f.read().strip().splitlines()):
+                if len(r) < 8 or not r[0].strip().replace(".", "").isdigit():
+                    continue
+                if self.max_mhz is None and r[1].strip().replace(".", "").isdigit():
+                    self.max_mhz = float(r[1])
+                util = int(r[7]) if r[7].strip().isdigit() else 1
+                self.rows.append((float(r[0]), [self.REASONS[i][0] for i in range(4) if r[3 + i].strip() == "Active"],
+                                  util))
 
     def summary(self):
-        self.f.flush()
-        self.f.seek(0)
-        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.count(",") >= 7]
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        busy = [r for r in rows if r[7].strip().isdigit() and int(r[7]) > 0] or rows
-        sm = [float(r[0]) for r in busy if r[0].strip().replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in busy for i in range(4) if r[3 + i].strip() == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(rows[0][1]) if rows[0][1].strip().replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(busy)}
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"], "source": self.source}
+        busy = [r for r in self.rows if r[2] > 0] or self.rows
+        return {"sm_mhz": statistics.median(r[0] for r in busy), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted({x for r in busy for x in r[1]}), "samples": len(busy), "source": self.source}
 
 
 # ------------------------------------------------------------------ CPU legs (oracle port)
@@ -366,6 +410,11 @@ class Ctx:
         self.dev, self.rank, self.world, self.local = dev, rank, world, local
         self.hbm_peak, self.peak_src = hbm_peak, peak_src
         self.L = lib.lib()
+        try:
+            pr = torch.cuda.get_device_properties(dev)
+            self.pci = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+        except Exception:
+            self.pci = None
 
     def barrier(self):
         if self.world > 1:
@@ -457,7 +506,7 @@ def cov_line(ctx, wl, args, steps, warmup, compute, sampler="oracle", clocks=Tru
     ctx.barrier()
     evs = [mk() for _ in range(steps)]
     launches0 = L.skc_launch_count()
-    clk = ClockSampler(ctx.local) if clocks else None
+    clk = ClockSampler(ctx.local, ctx.pci) if clocks else None
     if clk:
         clk.__enter__()
     t0 = torch.cuda.Event(enable_timing=True)
@@ -587,7 +636,7 @@ def kmeans_line(ctx, wl, args, steps, warmup, clocks=True):
     ctx.barrier()
     L = ctx.L
     launches0 = L.skc_launch_count()
-    clk = ClockSampler(ctx.local) if clocks else None
+    clk = ClockSampler(ctx.local, ctx.pci) if clocks else None
     if clk:
         clk.__enter__()
     t0 = torch.cuda.Event(enable_timing=True)
@@ -621,33 +670,37 @@ def kmeans_line(ctx, wl, args, steps, warmup, clocks=True):
 
 
 def kmeans_e2e(ctx, wl, args, reps=1):
-    """sparsified_kmeans(pinned host rows, init=seeded points) -> host labels and centres (N=1)."""
+    """sparsified_kmeans(pinned host rows of this rank's shard, init=seeded global points) ->
+    host labels and centres; under torchrun every rank passes its shard (col0 from rank order)
+    and the public API runs the sharded Lloyd loop. Host wall clock, max over ranks."""
     torch, skc = ctx.torch, ctx.skc
     cfg = WORKLOADS[wl]
-    n, p, m, K = cfg["n"], cfg["p"], cfg["m"], cfg["K"]
-    host = pinned_rows(ctx, wl, n, 0)
-    chosen = np.random.default_rng(SEED).choice(n, K, replace=False)
+    n, col0, n_glob = shard(cfg, ctx, args.scaling)
+    p, m, K = cfg["p"], cfg["m"], cfg["K"]
+    host = pinned_rows(ctx, wl, n, col0)
+    chosen = np.random.default_rng(SEED).choice(n_glob, K, replace=False)
     src = skc.RowSource(host, chunk_cols=1 << 16)
     gamma = m / p
 
     def one():
-        r = skc.sparsified_kmeans(src, K, gamma, max_iter=cfg["iters"], seed=SEED, init=chosen)
+        r = skc.sparsified_kmeans(src, K, gamma, max_iter=cfg["iters"], seed=SEED, init=chosen, col0=col0)
         return r.diagnostics["iterations"]
 
     one()
-    torch.cuda.synchronize()
+    ctx.barrier()
     w0 = time.perf_counter()
     its = 0
     for _ in range(reps):
         its += one()
-    el = time.perf_counter() - w0
+    ctx.barrier()
+    el = ctx.max_over_ranks(time.perf_counter() - w0)
     del host, src
     release_pinned(torch)
-    return {"value": n * its / el, "unit": "point-iters/s", "h2d_bytes_per_step": n * p * 4,
+    return {"value": n_glob * its / el, "unit": "point-iters/s", "h2d_bytes_per_step": n * p * 4,
             "d2h_bytes_per_step": n * 8 + p * K * 8, "ms_per_step": el * 1e3 / reps,
-            "iterations_per_step": its / reps,
+            "iterations_per_step": its / reps, "rows_per_gpu": n,
             "api": "sparsified_kmeans(RowSource(pinned host rows), K, gamma, init=seeded points): H2D + sketch + "
-                   "Lloyd loop + host labels and centres"}
+                   "Lloyd loop + host labels and centres (per-rank bytes; every rank its shard)"}
 
 
 def main():
@@ -684,17 +737,24 @@ def main():
     import torch
     import torch.distributed as tdist
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; SKC_DIST_BACKEND=gloo (with fewer GPUs than ranks, ranks share devices)
+    # exercises the multi-rank path on a single-GPU box -- a code check, not a timing
+    backend = os.environ.get("SKC_DIST_BACKEND", "nccl")
+    local_dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        tdist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=dev)
+        else:
+            tdist.init_process_group(backend)
     import paper_1511_00152_b200 as skc
     from paper_1511_00152_b200 import _lib
     from paper_1511_00152_b200 import dist as sdist
 
     hbm_peak, peak_src = peaks()
-    ctx = Ctx(torch, tdist, skc, _lib, sdist, dev, rank, world, local, hbm_peak, peak_src)
+    ctx = Ctx(torch, tdist, skc, _lib, sdist, dev, rank, world, local_dev, hbm_peak, peak_src)
     wl = args.workload
     if cfg["kind"] == "cov":
         line = cov_line(ctx, wl, args, args.steps, args.warmup, args.compute, args.sampler)
@@ -724,10 +784,8 @@ def main():
     if not args.no_e2e:
         if cfg["kind"] == "cov":
             out["e2e"] = cov_e2e(ctx, wl, args, args.compute)
-        elif world == 1:
-            out["e2e"] = kmeans_e2e(ctx, wl, args)
         else:
-            out["e2e"] = {"value": None, "unit": line["unit"], "note": "K-means e2e is measured at N=1"}
+            out["e2e"] = kmeans_e2e(ctx, wl, args)
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(wl, cfg)
 

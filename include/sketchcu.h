@@ -233,6 +233,14 @@ int skc_row_sqnorms(const void *val, int32_t val_dtype, int64_t n, int32_t m, do
 int skc_kmeans_d2_to_point(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m,
                            int32_t p_pad, int64_t c, const double *colsq, double *dense, double *out, void *stream);
 
+/* skc_kmeans_d2_to_point for a point c held by ANOTHER shard (sharded K-means++ seeding):
+ * the caller supplies W[:, c] densified (dense: device[p_pad], e.g. from the allreduced
+ * init_centers column) and colsq[c] (dense_sq: device[1]). Same arithmetic, so the global
+ * D^2 vector equals the unsharded one bit for bit. out: (n) fp64 (=). */
+int skc_kmeans_d2_to_dense(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m,
+                           int32_t p_pad, const double *dense, const double *dense_sq, const double *colsq,
+                           double *out, void *stream);
+
 /* ---- Philox sampler and supplied-index sketching -----------------------------------
  * north_star's counter-based alternative to the reference hash (not reference-identical;
  * restated bit for bit by oracle/sketch_oracle.c:orc_philox_indices). Column g = col0 + i

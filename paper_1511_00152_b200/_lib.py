@@ -39,6 +39,7 @@ SIGNATURES = {
     "skc_kmeans_assign_one": (_c.c_int, [_P, _P, _I32, _I32, _P, _I32, _I32, _P, _P, _P]),
     "skc_row_sqnorms": (_c.c_int, [_P, _I32, _I64, _I32, _P, _P]),
     "skc_kmeans_d2_to_point": (_c.c_int, [_P, _P, _I32, _I64, _I32, _I32, _I64, _P, _P, _P, _P]),
+    "skc_kmeans_d2_to_dense": (_c.c_int, [_P, _P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P]),
     "skc_signs": (_c.c_int, [_U64, _I32, _I32, _P, _P]),
     "skc_precondition": (_c.c_int, [_P, _I32, _I64, _I64, _I32, _I32, _I32, _U64, _P, _P]),
     "skc_unprecondition": (_c.c_int, [_P, _I64, _I32, _I32, _U64, _I32, _P, _P]),

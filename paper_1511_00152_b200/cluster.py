@@ -503,18 +503,19 @@ def sparsified_update_centers(sketch: SparseSketch, assignments: Assignments, K:
 
 
 def _initial_centers(ops: SketchKMeans, K: int, init, restart: int, seed: int) -> torch.Tensor:
+    """Point indices are global (col0-relative shards under torch.distributed)."""
     if init is None:
         from .kmeanspp import kmeanspp_select
 
         chosen = kmeanspp_select(ops, K, seed, restart)
-        return ops.init_centers(chosen)
+        return dist.init_centers_global(ops, chosen)
     if isinstance(init, CenterSet):
         return torch.as_tensor(np.asarray(init.centers, dtype=np.float64), device=ops.dev).contiguous()
     arr = np.asarray(init)
     if arr.ndim == 1:  # K chosen point indices (init_centers semantics)
         if arr.shape[0] != K:
             raise ParameterError(f"init lists {arr.shape[0]} points, K={K}")
-        return ops.init_centers(arr.astype(np.int64))
+        return dist.init_centers_global(ops, arr.astype(np.int64))
     if arr.ndim == 2 and arr.shape == (ops.p, K):
         return torch.as_tensor(arr.astype(np.float64), device=ops.dev).contiguous()
     raise ParameterError("init must be K point indices or a (p_pad, K) centre matrix")
@@ -523,7 +524,8 @@ def _initial_centers(ops: SketchKMeans, K: int, init, restart: int, seed: int) -
 def _sparsified_on_sketch(sketch: SparseSketch, K: int, max_iter: int = 100, n_init: int = 20, seed: int = 0,
                           init=None) -> KMeansResult:
     """cluster.py:375-404. ``init`` (K point indices or centres) replaces K-means++ and
-    runs a single restart."""
+    runs a single restart. On a sharded sketch (world > 1) every rank follows the same
+    restarts and trajectory; the labels are this rank's shard, the rest is global."""
     ops = SketchKMeans(sketch)
     restarts = 1 if init is not None else int(n_init)
     best, iter_seconds, iters_total = None, 0.0, 0
@@ -535,7 +537,7 @@ def _sparsified_on_sketch(sketch: SparseSketch, K: int, max_iter: int = 100, n_i
         if best is None or traj[-1] < best[2][-1]:
             best = (labels.clone(), mu, traj, iters)
     labels, mu, traj, iters = best
-    _, counts, _ = ops.update(labels, mu)
+    _, counts, _ = ops.update(labels, mu)  # sums the shards' counts under world > 1
     spec = sketch.spec
     back = unprecondition_columns(mu, spec)[: spec.p]
     mu_h = mu.cpu().numpy()
@@ -559,15 +561,22 @@ def _sparsified_on_sketch(sketch: SparseSketch, K: int, max_iter: int = 100, n_i
 
 def sparsified_kmeans(source, K: int, gamma: float, max_iter: int = 100, n_init: int = 20, seed: int = 0,
                       kind: str = "hadamard", chunk_cols: int = 8192, *, init=None, compute: str = "f64",
-                      device=None) -> KMeansResult:
-    """One-pass sparsified K-means; cluster.py:342-372"""
+                      device=None, col0: Optional[int] = None) -> KMeansResult:
+    """One-pass sparsified K-means; cluster.py:342-372.
+
+    Under torch.distributed (world > 1) ``source`` is this rank's shard of the columns, at
+    global offset ``col0`` (default: shards concatenated in rank order). ``init`` point
+    indices are global; the returned labels are the shard's, centres and objective global."""
     source = as_source(source, chunk_cols=chunk_cols)
-    if K > source.n:
-        raise ParameterError(f"K={K} exceeds number of points n={source.n}")
+    c0, n_total = dist.shard_offset(source.n)
+    if col0 is not None:
+        c0 = int(col0)
+    if K > n_total:
+        raise ParameterError(f"K={K} exceeds number of points n={n_total}")
     spec = PreconditionSpec.create(kind, source.p, sign_seed=derive_seed(seed, _TAG_RUN_SIGN))
     plan = plan_for(spec, gamma, master_seed=derive_seed(seed, _TAG_RUN_SAMPLE))
     t0 = time.perf_counter()
-    sketch = sketch_stream(source, spec, plan, compute=compute, device=device)
+    sketch = sketch_stream(source, spec, plan, compute=compute, device=device, col0=c0)
     torch.cuda.synchronize(sketch.indices.device)
     sketch_seconds = time.perf_counter() - t0
     result = _sparsified_on_sketch(sketch, K, max_iter=max_iter, n_init=n_init, seed=seed, init=init)
@@ -577,7 +586,7 @@ def sparsified_kmeans(source, K: int, gamma: float, max_iter: int = 100, n_init:
 
 def sparsified_kmeans_two_pass(source, K: int, gamma: float, max_iter: int = 100, n_init: int = 20, seed: int = 0,
                                kind: str = "hadamard", chunk_cols: int = 8192, *, compute: str = "f64",
-                               device=None) -> KMeansResult:
+                               device=None, col0: Optional[int] = None) -> KMeansResult:
     """Sparsified K-means plus one pass over the raw rows; cluster.py:407-456.
 
     The second pass runs on the GPU as the raw chunks stream in (pinned copies overlapped
@@ -585,11 +594,13 @@ def sparsified_kmeans_two_pass(source, K: int, gamma: float, max_iter: int = 100
     centre (first argmin of (|x|^2 - 2 <x, mu>) + |mu|^2, clipped objective) and
     ``skc_dense_sums`` accumulates the exact original-domain means of the first-pass
     clusters. Nothing further is iterated. Each chunk's objective is a numpy-order pairwise
-    sum, and the chunk sums add in chunk order, as the reference does.
+    sum, and the chunk sums add in chunk order, as the reference does. Sharded (world > 1):
+    each rank passes its shard as in ``sparsified_kmeans``; the cluster sums and counts are
+    allreduced and the chunk objectives add in rank order.
     """
     source = as_source(source, chunk_cols=chunk_cols)
     first = sparsified_kmeans(source, K, gamma, max_iter=max_iter, n_init=n_init, seed=seed, kind=kind,
-                              chunk_cols=chunk_cols, compute=compute, device=device)
+                              chunk_cols=chunk_cols, compute=compute, device=device, col0=col0)
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     mu_hat = np.asarray(first.centers.centers, dtype=np.float64)  # (p, K)
     p, n = source.p, source.n
@@ -628,9 +639,9 @@ def sparsified_kmeans_two_pass(source, K: int, gamma: float, max_iter: int = 100
         pw = _lib.workspace(L.skc_pairwise_sum_workspace(max((c for _, c in spans), default=1)), dev)
         for t, (a, c) in enumerate(spans):
             _lib.call("skc_pairwise_sum", d2min[a:].data_ptr(), c, obj_dev[t:].data_ptr(), pw.data_ptr(), pw.numel(), st)
-    obj = 0.0
-    for v in obj_dev.cpu().numpy()[: len(spans)]:
-        obj += float(v)
+        dist.allreduce_(sums)  # sharded (world > 1): every rank's first-pass cluster sums
+        dist.allreduce_(counts)
+    obj = dist.ordered_sum(obj_dev.cpu().numpy()[: len(spans)].tolist())  # chunk order, then rank order
     cnt = counts.cpu().numpy()
     mu2 = sums.cpu().numpy().T.copy()  # (p, K)
     nz = cnt > 0

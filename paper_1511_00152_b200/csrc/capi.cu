@@ -95,6 +95,8 @@ int kmtc_prepare_launch(const int32_t*, const void*, int, int64_t, int32_t, int3
 size_t kmtc_assign_ws(int64_t, int32_t, int32_t);
 int kmtc_assign_launch(const int32_t*, const void*, int, int64_t, int32_t, const double*, int32_t, int32_t,
                        const int32_t*, int32_t*, double*, int64_t*, double*, const void*, void*, cudaStream_t);
+int d2_dense_launch(const int32_t*, const void*, int, int64_t, int32_t, int32_t, const double*, const double*,
+                    const double*, double*, cudaStream_t);
 int d2_point_launch(const int32_t*, const void*, int, int64_t, int32_t, int32_t, int64_t, const double*, double*,
                     double*, cudaStream_t);
 
@@ -405,6 +407,15 @@ int skc_kmeans_d2_to_point(const int32_t* idx, const void* val, int32_t val_dtyp
   if ((rc = check_dtype(val_dtype))) return rc;
   if (c < 0 || c >= n) return fail(SKC_EPARAM, "point index out of range");
   return d2_point_launch(idx, val, val_dtype == SKC_F64, n, m, p_pad, c, colsq, dense, out, S(stream));
+}
+
+int skc_kmeans_d2_to_dense(const int32_t* idx, const void* val, int32_t val_dtype, int64_t n, int32_t m,
+                           int32_t p_pad, const double* dense, const double* dense_sq, const double* colsq, double* out,
+                           void* stream) {
+  int rc;
+  if ((rc = check_dtype(val_dtype))) return rc;
+  if (n < 0 || m < 1 || p_pad < 1) return fail(SKC_EDIM, "need n >= 0, m >= 1 and p_pad >= 1");
+  return d2_dense_launch(idx, val, val_dtype == SKC_F64, n, m, p_pad, dense, dense_sq, colsq, out, S(stream));
 }
 
 int skc_sketch_pack_records(const int32_t* idx, const void* val, int32_t val_dtype, int64_t n, int32_t m,

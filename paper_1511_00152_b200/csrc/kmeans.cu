@@ -1673,13 +1673,13 @@ __global__ void dense_point_kernel(const int32_t* __restrict__ idx, const void* 
 
 template <typename V>
 __global__ void d2_point_kernel(const int32_t* __restrict__ idx, const void* __restrict__ val, int64_t n, int m,
-                                int64_t c, const double* __restrict__ colsq, const double* __restrict__ dense,
-                                double scale, double* __restrict__ out) {
+                                const double* __restrict__ csq, const double* __restrict__ colsq,
+                                const double* __restrict__ dense, double scale, double* __restrict__ out) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   double cross = 0.0;
   for (int t = 0; t < m; ++t) cross = dadd(cross, dmul(ldd<V>(val, i * m + t), __ldg(dense + __ldg(idx + i * m + t))));
-  const double d2 = dsub(dadd(colsq[i], colsq[c]), dmul(2.0, cross));
+  const double d2 = dsub(dadd(colsq[i], *csq), dmul(2.0, cross));
   out[i] = dmul(scale, d2 > 0.0 ? d2 : 0.0);
 }
 
@@ -1695,6 +1695,9 @@ int row_sqnorms_launch(const void* val, int val_f64, int64_t n, int32_t m, doubl
   return check_launch("row_sqnorm_kernel");
 }
 
+int d2_dense_launch(const int32_t*, const void*, int, int64_t, int32_t, int32_t, const double*, const double*,
+                    const double*, double*, cudaStream_t);
+
 int d2_point_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, int32_t p_pad, int64_t c,
                     const double* colsq, double* dense, double* out, cudaStream_t st) {
   const double scale = (double)p_pad / (double)m;
@@ -1702,9 +1705,18 @@ int d2_point_launch(const int32_t* idx, const void* val, int val_f64, int64_t n,
   else dense_point_kernel<float><<<1, 256, 0, st>>>(idx, val, m, p_pad, c, dense);
   int rc = check_launch("dense_point_kernel");
   if (rc) return rc;
+  return d2_dense_launch(idx, val, val_f64, n, m, p_pad, dense, colsq + c, colsq, out, st);
+}
+
+// d2 of every point to a point given as its densified row and squared norm (a point of another
+// shard: sharded K-means++ seeding, cluster.py:169-173 with W[:, c] supplied).
+int d2_dense_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, int32_t p_pad,
+                    const double* dense, const double* csq, const double* colsq, double* out, cudaStream_t st) {
+  if (n == 0) return SKC_OK;
+  const double scale = (double)p_pad / (double)m;
   const unsigned blocks = (unsigned)((n + 255) / 256);
-  if (val_f64) d2_point_kernel<double><<<blocks, 256, 0, st>>>(idx, val, n, m, c, colsq, dense, scale, out);
-  else d2_point_kernel<float><<<blocks, 256, 0, st>>>(idx, val, n, m, c, colsq, dense, scale, out);
+  if (val_f64) d2_point_kernel<double><<<blocks, 256, 0, st>>>(idx, val, n, m, csq, colsq, dense, scale, out);
+  else d2_point_kernel<float><<<blocks, 256, 0, st>>>(idx, val, n, m, csq, colsq, dense, scale, out);
   return check_launch("d2_point_kernel");
 }
 

@@ -5,9 +5,11 @@ Each rank sketches the global columns [c0, c1) = shard_bounds(n, rank, world) wi
 (_hash.py:46-56), so a sharded sketch is byte-identical to the 1-GPU sketch. The
 exchange steps are the reductions the reference spec allows:
   * estimators: ONE allreduce per pass of [mean acc (p), stats, packed triangle];
-  * K-means: per Lloyd iteration, an allreduce of [changed, objective, d2max], a
-    MIN-allreduce for the global first argmax, an allreduce of the K x p sums and
-    counts, and a broadcast of the reseed row when a cluster empties.
+  * K-means: per Lloyd iteration ONE allreduce of the packed exchange [sums | counts |
+    sizes | changed | objective | per-rank (max d2min, argmax row)] (cluster.py
+    _lloyd_loop_sharded), plus one of the reseed row when a cluster empties;
+  * K-means++ seeding: per chosen point, one allreduce of its densified row and norm and
+    one all-gather of the D^2 shards, so every rank draws from the global D^2 vector.
 All helpers reduce to no-ops when torch.distributed is not initialised or world == 1.
 """
 
@@ -143,3 +145,64 @@ def shard_ranges(col0: int, n: int, device, group=None) -> list:
     t[rank(group), 1] = int(n)
     allreduce_(t, group=group)
     return [(int(a), int(b)) for a, b in t.cpu().tolist()]
+
+
+def collective_device():
+    """Device for small host-logic collectives: the current CUDA device under NCCL, else CPU."""
+    if world() > 1 and dist.get_backend() == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def shard_offset(n_local: int, group=None) -> tuple[int, int]:
+    """(col0, n_total) of this rank when shards are concatenated in rank order."""
+    w = world(group)
+    if w == 1:
+        return 0, int(n_local)
+    t = torch.zeros(w, dtype=torch.int64, device=collective_device())
+    t[rank(group)] = int(n_local)
+    allreduce_(t, group=group)
+    sizes = t.cpu().tolist()
+    return int(sum(sizes[: rank(group)])), int(sum(sizes))
+
+
+def gather_ranges(local: torch.Tensor, ranges: list, group=None):
+    """Concatenate every rank's 1-D shard ``local`` into the global host (numpy) vector.
+
+    ``ranges`` is shard_ranges' [(col0, n)] per rank; together they must tile [0, total).
+    One all-gather of max(n)-padded buffers."""
+    import numpy as np
+
+    total = sum(n for _, n in ranges)
+    if world(group) == 1:
+        return local.cpu().numpy()
+    nmax = max(max(n for _, n in ranges), 1)
+    on = torch.device("cpu") if dist.get_backend(group) == "gloo" else local.device
+    buf = torch.zeros(nmax, dtype=local.dtype, device=on)
+    buf[: local.numel()] = local
+    parts = [torch.empty_like(buf) for _ in ranges]
+    dist.all_gather(parts, buf, group=group)
+    out = np.empty(total, dtype=buf.cpu().numpy().dtype)
+    covered = 0
+    for (c0, n), part in zip(ranges, parts):
+        if c0 < 0 or c0 + n > total:
+            raise ValueError("shard ranges do not tile [0, total)")
+        out[c0:c0 + n] = part[:n].cpu().numpy()
+        covered += n
+    if covered != total:
+        raise ValueError("shard ranges do not tile [0, total)")
+    return out
+
+
+def ordered_sum(values: list, group=None) -> float:
+    """Sum every rank's list of floats in (rank, position) order, as one process would."""
+    if world(group) == 1:
+        allv = [values]
+    else:
+        allv = [None] * world(group)
+        dist.all_gather_object(allv, [float(v) for v in values], group=group)
+    tot = 0.0
+    for vs in allv:
+        for v in vs:
+            tot += float(v)
+    return tot

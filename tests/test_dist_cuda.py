@@ -56,9 +56,16 @@ def _run(skc, X, col0, n_total):
     mu0 = dist.init_centers_global(ops, CHOSEN)
     labels, mu, traj, iters, _ = ops.lloyd(mu0, 30)
     counts = dist.allreduce_(ops.partials(labels, K)[1])  # per-(coordinate, cluster) sampling counts
+    # the public API on the shard: K-means++ restarts (sharded D^2 draws), then the two-pass variant
+    Xd = torch.as_tensor(X, device=dev)
+    res = skc.sparsified_kmeans(skc.RowSource(Xd), K, M / P, max_iter=30, n_init=2, seed=5)
+    res2 = skc.sparsified_kmeans_two_pass(skc.RowSource(Xd, chunk_cols=4096), K, M / P, max_iter=30, n_init=1,
+                                          seed=5)
     return dict(idx=sk.host_indices(), val=sk.host_values(), acc=mom.acc.cpu().numpy(), tri=mom.tri.cpu().numpy(),
                 labels=labels.cpu().numpy(), mu=mu.cpu().numpy(), traj=np.array(traj), iters=iters,
-                counts=counts.cpu().numpy())
+                counts=counts.cpu().numpy(), api_labels=res.assignments.labels, api_obj=res.objective,
+                api_centers=res.centers.centers, api_curve=np.array(res.diagnostics["objective_curve"]),
+                tp_labels=res2.assignments.labels, tp_obj=res2.objective, tp_centers=res2.centers.centers)
 
 
 def _worker(rank, world, port, outdir):
@@ -116,6 +123,51 @@ def test_sharded_lloyd_matches_unsharded(runs):
         assert np.abs(s["mu"] - full["mu"]).max() <= 1e-12 * np.abs(full["mu"]).max()
         assert np.allclose(s["traj"], full["traj"], rtol=1e-12)
     assert np.array_equal(shards[0]["mu"], shards[1]["mu"])
+
+
+def test_sharded_public_kmeans_matches_unsharded(runs):
+    """sparsified_kmeans on shards (col0 from rank order, K-means++ restarts drawn from the
+    global D^2 vector) equals the one-process run: same seeds, same labels and trajectory."""
+    shards, full = runs
+    assert np.array_equal(np.concatenate([s["api_labels"] for s in shards]), full["api_labels"])
+    for s in shards:
+        assert len(s["api_curve"]) == len(full["api_curve"])
+        assert np.allclose(s["api_curve"], full["api_curve"], rtol=1e-12)
+        assert np.abs(s["api_centers"] - full["api_centers"]).max() <= 1e-12 * np.abs(full["api_centers"]).max()
+    assert np.array_equal(shards[0]["api_centers"], shards[1]["api_centers"])
+
+
+def test_sharded_two_pass_matches_unsharded(runs):
+    shards, full = runs
+    assert np.array_equal(np.concatenate([s["tp_labels"] for s in shards]), full["tp_labels"])
+    for s in shards:
+        assert np.isclose(float(s["tp_obj"]), float(full["tp_obj"]), rtol=1e-12)
+        assert np.abs(s["tp_centers"] - full["tp_centers"]).max() <= 1e-12 * np.abs(full["tp_centers"]).max()
+
+
+def test_d2_to_dense_equals_d2_to_point():
+    """skc_kmeans_d2_to_dense with the point's own densified row == skc_kmeans_d2_to_point."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1511_00152_b200 as skc
+    from paper_1511_00152_b200 import _lib
+    from paper_1511_00152_b200.kmeanspp import _D2
+
+    dev = torch.device("cuda", 0)
+    X = _data()[:5000]
+    spec = skc.PreconditionSpec.create("hadamard", P, sign_seed=SS)
+    sk = skc.sketch_stream(skc.RowSource(torch.as_tensor(X, device=dev)), spec, skc.SamplingPlan(MS, P, M))
+    ops = skc.SketchKMeans(sk)
+    d2 = _D2(ops)
+    for c in (0, 1234, 4999):
+        want = d2(c)
+        row = torch.zeros(P + 1, dtype=torch.float64, device=dev)
+        row[:P] = ops.init_centers(np.array([c]))[:, 0]
+        row[P] = d2.colsq[c]
+        out = torch.empty(ops.n, dtype=torch.float64, device=dev)
+        _lib.call("skc_kmeans_d2_to_dense", ops.idx.data_ptr(), ops.val.data_ptr(), ops.vcode, ops.n, ops.m, P,
+                  row.data_ptr(), row[P:].data_ptr(), d2.colsq.data_ptr(), out.data_ptr(), _lib.stream_ptr(dev))
+        assert np.array_equal(out.cpu().numpy(), want)
 
 
 def test_nccl_entry_points_single_rank():

@@ -135,10 +135,33 @@ def _worker(rank, world, port, outdir):
     labels, mu, traj, iters, _ = lloyd_loop(ops, mu0, 30, None)
     loop_calls = list(calls)
     dist.allreduce_ = real_allreduce
+    # --- sharded K-means++ host logic (kmeanspp._D2Sharded with the D^2 kernel in numpy):
+    # owner's densified row + norm by one allreduce, D^2 shards by one all-gather ---
+    from paper_1511_00152_b200.kmeanspp import pp_select, restart_rng
+
+    sh_col0, sh_total = dist.shard_offset(u1 - u0)
+    ranges = dist.shard_ranges(u0, u1 - u0, torch.device("cpu"))
+    gathered = dist.gather_ranges(torch.arange(u0, u1, dtype=torch.float64), ranges)
+    osum = dist.ordered_sum([0.1 * (rank + 1), 0.2 * (rank + 1)])
+    li, lv = idx_full[u0:u1], val_full[u0:u1]
+    colsq = (lv * lv).sum(axis=1)
+
+    def d2_sharded(c):
+        row = torch.zeros(p_pad + 1, dtype=torch.float64)
+        if u0 <= c < u1:
+            row[li[c - u0]] = torch.from_numpy(lv[c - u0])
+            row[p_pad] = float(colsq[c - u0])
+        dist.allreduce_(row)
+        dense, csq = row[:p_pad].numpy(), float(row[p_pad])
+        d2 = colsq + csq - 2.0 * (lv * dense[li]).sum(axis=1)
+        return dist.gather_ranges(torch.from_numpy((p_pad / m) * np.clip(d2, 0.0, None)), ranges)
+
+    pp = pp_select(sh_total, 6, restart_rng(3, 1), d2_sharded)
     np.savez(os.path.join(outdir, f"r{rank}.npz"), idx=idx, val=val, acc=acc.numpy(), stats=stats.numpy(),
              tri=tri.numpy(), n_tot=n_tot, labels=labels.numpy(), mu=mu.numpy(), traj=np.array(traj), iters=iters,
              packed=mom.packed.numpy(), n_packed=n_packed, pass_calls=np.array(pass_calls),
-             loop_calls=np.array(loop_calls), shard=np.array([u0, u1]))
+             loop_calls=np.array(loop_calls), shard=np.array([u0, u1]), sh=np.array([sh_col0, sh_total]),
+             gathered=gathered, osum=osum, pp=np.array(pp))
     tdist.barrier()
     tdist.destroy_process_group()
 
@@ -217,3 +240,31 @@ def test_uneven_shards_lloyd_matches_single_process(sharded):
     assert [tuple(r["shard"]) for r in sharded] == [(0, 1000), (1000, 3001)]
     assert np.array_equal(labels, lo) and int(sharded[0]["iters"]) == io
     assert np.allclose(sharded[0]["mu"], muo, rtol=1e-12, atol=1e-12)
+
+
+def test_shard_offsets_gather_and_ordered_sum(sharded):
+    n = _data().shape[1]
+    assert [tuple(r["sh"]) for r in sharded] == [(0, n), (1000, n)]
+    for r in sharded:
+        assert np.array_equal(r["gathered"], np.arange(n, dtype=np.float64))
+        assert float(r["osum"]) == ((0.0 + 0.1) + 0.2) + 0.2 + 0.4  # rank order, then list order
+
+
+def test_sharded_kmeanspp_chooses_the_unsharded_points(sharded):
+    """cluster.py:74-93 on a sharded sketch: every rank draws from the global D^2 vector."""
+    from oracle import oracle as O
+    from paper_1511_00152_b200.kmeanspp import pp_select, restart_rng
+
+    X = _data()
+    idx, val = O.sketch(X.T.copy(), 64, O.HADAMARD, 11, 12, 12)
+    colsq = (val * val).sum(axis=1)
+
+    def d2_full(c):
+        dense = np.zeros(64)
+        dense[idx[c]] = val[c]
+        d2 = colsq + colsq[c] - 2.0 * (val * dense[idx]).sum(axis=1)
+        return (64 / 12) * np.clip(d2, 0.0, None)
+
+    want = pp_select(X.shape[1], 6, restart_rng(3, 1), d2_full)
+    for r in sharded:
+        assert list(r["pp"]) == want
