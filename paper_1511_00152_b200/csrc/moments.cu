@@ -2,6 +2,7 @@
 // K4 covariance finalize, K7 adjoint transform (mean / PCs / centres).
 // Reference: estimators.py:30-66, transform.py:92-200.
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -187,7 +188,7 @@ int moments_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, 
 #define SKC_COV_UNROLL 1  // unroll of the flat pair loop (experiments)
 #endif
 #ifndef SKC_COV_SMEM_KB
-#define SKC_COV_SMEM_KB 220
+#define SKC_COV_SMEM_KB 226
 #endif
 #ifndef SKC_COV_WARPS
 #define SKC_COV_WARPS 32
@@ -200,16 +201,24 @@ constexpr int kMaxBands = 511;
 __host__ __device__ inline int64_t tri_off(int64_t a, int64_t p) { return a * p - a * (a - 1) / 2; }
 
 // visit pair table (m <= 64): bytes t[f], u[f] of the f-th pair (t <= u) in t-major order,
-// so the pairs of rows t in [nlo, nhi) are the contiguous range [tri_off(nlo), tri_off(nhi))
+// so the pairs of rows t in [nlo, nhi) are the contiguous range [tri_off(nlo), tri_off(nhi)),
+// followed by the u16 table F(t) = tri_off(t) for t = 0..m (the flat kernel's loop bounds)
 static size_t pair_table_bytes(int32_t m) {
-  return m <= 64 ? ((size_t)m * (m + 1) + 7) & ~(size_t)7 : 0;
+  return m <= 64 ? (((size_t)m * (m + 1) / 2 + 1) & ~(size_t)1) * 4 + (((size_t)m + 4) & ~(size_t)3) * 2 : 0;
+}
+// band kernel for m <= 64: 'f' flat pair table (default) or 'b' the round-1 band kernel
+// (SKC_COV_KERNEL=band, A/B runs); m > 64: 'b'.
+static char band_kind(int32_t m) {
+  if (m > 64) return 'b';
+  const char* k = getenv("SKC_COV_KERNEL");
+  return (k && k[0] == 'b') ? 'b' : 'f';
 }
 static int band_capacity(int32_t m, int32_t p_pad) {
   // int32 entries left after the per-warp row staging, the row table and the pair table
   return (int)(((size_t)kSmemBudget - (size_t)kCovWarps * m * 16 - 4 * (size_t)p_pad - pair_table_bytes(m)) / 4);
 }
 // greedy row bands of <= cap entries; returns the count, fills out[0..count] if given
-static int make_bands(int32_t p_pad, int cap, int* out) {
+static int greedy_bands(int32_t p_pad, int64_t cap, int* out) {
   int nb = 0, a = 0;
   while (a < p_pad) {
     int64_t e = 0;
@@ -225,6 +234,16 @@ static int make_bands(int32_t p_pad, int cap, int* out) {
   }
   if (out && nb <= kMaxBands) out[nb] = p_pad;
   return nb;
+}
+// as few bands as the capacity allows, balanced: the smallest per-band bound that keeps the
+// greedy count (equal entries = equal expected pairs per band)
+static int make_bands(int32_t p_pad, int cap, int* out) {
+  const int nb = greedy_bands(p_pad, cap, nullptr);
+  const int64_t total = tri_off(p_pad, p_pad);
+  int64_t t = (total + nb - 1) / nb;
+  while (t < cap && greedy_bands(p_pad, t, nullptr) > nb) t += (t >> 6) + 1;
+  if (t > cap) t = cap;
+  return greedy_bands(p_pad, t, out);
 }
 
 struct CovParams {
@@ -451,6 +470,140 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
   }
 }
 
+// K3 flat kernel (m <= 64, the configs' shapes): the same fixed-point band accumulation as
+// cov_band_kernel, with the per-visit work cut to what the pair loop needs.
+//  * rowaddr[a - r0] holds the shared byte address of entry (a, 0), so a staged T entry is
+//    the address itself; F(t) comes from a u16 table instead of multiplies.
+//  * Rows are walked with 32-bit counters and pointer bumps; band membership of a lane's
+//    element is one unsigned compare (indices are sorted, so in-band lanes are [nlo, nhi)).
+//  * The pair loop's induction variable is the pair-table pointer.
+// Rows holding a value above tau (or a wide-range scale) take the exact fp64 path.
+template <typename V>
+__global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __grid_constant__ CovParams P) {
+  extern __shared__ int smem_i[];
+  const int m = P.m;
+  const int band = blockIdx.x % P.nbands, group = blockIdx.x / P.nbands;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = P.band_rows[band], r1 = P.band_rows[band + 1];
+  const int64_t e0 = tri_off(r0, P.p_pad), e1 = tri_off(r1, P.p_pad);
+  const int ne = (int)(e1 - e0);
+  uint32_t* lo = reinterpret_cast<uint32_t*>(smem_i);
+  uint32_t* rowaddr = lo + ((ne + 1) & ~1);  // [r1 - r0]
+  const int npair = m * (m + 1) / 2;
+  // pair f: byte offsets of T[t] and U[u] in the warp's staging, 8 t | 8 (m + u) << 16
+  uint32_t* ptab = rowaddr + ((r1 - r0 + 1) & ~1);
+  uint16_t* ptoff = reinterpret_cast<uint16_t*>(ptab + ((npair + 1) & ~1));  // [m + 1]
+  int2* S = reinterpret_cast<int2*>(ptoff + ((m + 4) & ~3)) + (size_t)warp * 2 * m;  // T[m] then U[m]
+  unsigned long long* part = P.part + (size_t)group * tri_off(P.p_pad, P.p_pad) + e0;
+  const uint32_t lo_sh = (uint32_t)__cvta_generic_to_shared(lo);
+
+  double tau;
+  const int S_ = cov_scale(P.stats, m, &tau);
+  const bool wide = cov_wide(S_);
+  const float sh = wide ? 1.0f : (float)ldexp(1.0, S_ / 2);  // 2^(S/2) on each factor
+  const double full_s = ldexp(1.0, S_);
+  const float ftau = wide ? -1.0f : (float)tau;  // wide: every row takes the exact path
+  double* tri_b = P.tri + e0;
+
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) lo[e] = kBias;
+  for (int a = r0 + threadIdx.x; a < r1; a += blockDim.x)
+    rowaddr[a - r0] = lo_sh + 4u * (uint32_t)((tri_off(a, P.p_pad) - e0) - a);
+  if (threadIdx.x <= m) ptoff[threadIdx.x] = (uint16_t)(threadIdx.x * m - ((threadIdx.x * (threadIdx.x - 1)) >> 1));
+  if (threadIdx.x < m) {
+    const int t = threadIdx.x, f0 = t * m - ((t * (t - 1)) >> 1);
+    for (int u = t; u < m; ++u) ptab[f0 + u - t] = (uint32_t)(8 * t) | ((uint32_t)(8 * (m + u)) << 16);
+  }
+  __syncthreads();
+
+  const int64_t g0 = P.n * group / P.groups, g1 = P.n * (group + 1) / P.groups;
+  const int nrows = (int)(g1 - g0);
+  const V* val = reinterpret_cast<const V*>(P.val);
+  // lane's element pointers for row i of the group: gi + i * m (the prefetch of row i + 32
+  // is clamped to the last row instead of branched around)
+  const int32_t* const gi = P.idx + g0 * (int64_t)m + lane;
+  const V* const gv = val + g0 * (int64_t)m + lane;
+  const bool has0 = lane < m, has1 = lane + 32 < m;
+  const uint32_t bw = (uint32_t)(r1 - r0);
+  const uint32_t S_sh = (uint32_t)__cvta_generic_to_shared(S);
+  int aj0 = 0x7FFFFFFF, aj1 = 0x7FFFFFFF;
+  V av0 = 0, av1 = 0;
+  if (warp < nrows) {
+    const int32_t* ip = gi + (int64_t)warp * m;
+    const V* vp = gv + (int64_t)warp * m;
+    if (has0) aj0 = __ldg(ip), av0 = __ldg(vp);
+    if (has1) aj1 = __ldg(ip + 32), av1 = __ldg(vp + 32);
+  }
+  for (int i = warp; i < nrows; i += kCovWarps) {
+    const int j0 = aj0, j1 = aj1;
+    const float v0 = (float)av0, v1 = (float)av1;
+    {
+      const uint32_t off = (uint32_t)min(i + kCovWarps, nrows - 1) * (uint32_t)m;  // < 2^31 per launch
+      const int32_t* ip = gi + off;
+      const V* vp = gv + off;
+      if (has0) aj0 = __ldg(ip), av0 = __ldg(vp);
+      if (has1) aj1 = __ldg(ip + 32), av1 = __ldg(vp + 32);
+    }
+    const int nlo = __popc(__ballot_sync(kFullMask, j0 < r0)) + __popc(__ballot_sync(kFullMask, j1 < r0));
+    const int nhi = __popc(__ballot_sync(kFullMask, j0 < r1)) + __popc(__ballot_sync(kFullMask, j1 < r1));
+    if (nlo == nhi) continue;  // none of this row's indices fall in the band
+    const bool big = !(fabsf(v0) <= ftau) || !(fabsf(v1) <= ftau);  // lanes past m hold 0; NaN is big
+    if (__any_sync(kFullMask, big)) {
+      // exact fp64 products for this row's band pairs
+      const int64_t r = g0 + i;
+      const int32_t* ir = P.idx + r * m;
+      const V* vr = val + r * m;
+      for (int t = nlo; t < nhi; ++t) {
+        const double va = (double)__ldg(vr + t);
+        const int base = (int)(rowaddr[__ldg(ir + t) - r0] - lo_sh) >> 2;  // signed: entry (a, 0) may precede e0
+        for (int u = t + lane; u < m; u += 32) {
+          const int e = base + __ldg(ir + u);
+#ifdef SKC_COV_DEBUG
+          if (e < 0 || e >= ne) {
+            printf("cov_flat big: bad e %d ne %d band %d row %d t %d u %d\n", e, ne, band, i, t, u);
+            __trap();
+          }
+#endif
+          cov_add_exact(va, (double)__ldg(vr + u), full_s, wide, part + e, tri_b + e);
+        }
+      }
+      continue;
+    }
+    const float s0 = v0 * sh, s1 = v1 * sh;  // exact power-of-two scalings
+    if (has0) S[m + lane] = make_int2(j0 << 2, __float_as_int(s0));
+    if (has1) S[m + 32 + lane] = make_int2(j1 << 2, __float_as_int(s1));
+    if ((uint32_t)(j0 - r0) < bw) S[lane] = make_int2((int)rowaddr[j0 - r0], __float_as_int(s0));
+    if ((uint32_t)(j1 - r0) < bw) S[lane + 32] = make_int2((int)rowaddr[j1 - r0], __float_as_int(s1));
+    __syncwarp();
+    const uint32_t* tp = ptab + ptoff[nlo] + lane;
+    const uint32_t* const te = ptab + ptoff[nhi];
+    for (; tp < te; tp += 32) {
+      const uint32_t pe = *tp;
+      int tx, ty, ux, uy;
+      asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(tx), "=r"(ty) : "r"(S_sh + (pe & 0xFFFFu)));
+      asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(ux), "=r"(uy) : "r"(S_sh + (pe >> 16)));
+      const uint32_t addr = (uint32_t)(tx + ux);
+#ifdef SKC_COV_DEBUG
+      if (addr < lo_sh || addr >= lo_sh + 4u * (uint32_t)ne || (addr & 3)) {
+        printf("cov_flat: bad addr %u (lo %u ne %d) band %d row %d t %d u %d nlo %d nhi %d\n", addr, lo_sh, ne, band,
+               i, (int)(pe & 0xFFFF) / 8, (int)(pe >> 16) / 8 - m, nlo, nhi);
+        __trap();
+      }
+#endif
+      const int q = __float2int_rn(__int_as_float(ty) * __int_as_float(uy));
+      uint32_t old;
+      asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"((uint32_t)q) : "memory");
+      if ((old + (uint32_t)q < old) != (q < 0))  // carry (q >= 0) / borrow (q < 0): rare
+        atomicAdd(part + ((addr - lo_sh) >> 2), (unsigned long long)((long long)(q < 0 ? -1 : 1) << 32));
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+    const long long q = (long long)lo[e] - (long long)kBias;
+    if (q != 0) atomicAdd(part + e, (unsigned long long)q);
+  }
+}
+
 __global__ void cov_reduce_kernel(const unsigned long long* __restrict__ part, int groups, int64_t total, int m,
                                   const double* __restrict__ stats, double* __restrict__ tri) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -643,8 +796,9 @@ static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int
   }
   const size_t smem = (size_t)((maxe + 1) & ~1) * 4 + (size_t)((maxr + 1) & ~1) * 4 + pair_table_bytes(m) +
                       (size_t)kCovWarps * m * 16;
-  auto k = val_f64 ? (m > 64 ? cov_band_kernel<double, true> : cov_band_kernel<double, false>)
-                   : (m > 64 ? cov_band_kernel<float, true> : cov_band_kernel<float, false>);
+  const bool flat = band_kind(m) == 'f';
+  auto k = val_f64 ? (m > 64 ? cov_band_kernel<double, true> : flat ? cov_flat_kernel<double> : cov_band_kernel<double, false>)
+                   : (m > 64 ? cov_band_kernel<float, true> : flat ? cov_flat_kernel<float> : cov_band_kernel<float, false>);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<H.nbands * H.groups, kCovWarps * 32, smem, st>>>(H);
   int rc = check_launch("cov_band_kernel");

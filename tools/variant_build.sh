@@ -13,6 +13,6 @@ for s in $SRCS; do
   $NVCC $FL -c $SRC/paper_1511_00152_b200/csrc/$s.cu -o $OUT/$s.o &
 done
 wait
-$NVCC -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/libsketchcu.so $OUT/*.o -lcudart
+$NVCC -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/libsketchcu.so $OUT/*.o -lcudart -ldl -lcusolver
 rm -f $OUT/*.o
 echo $OUT/libsketchcu.so
