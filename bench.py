@@ -435,11 +435,11 @@ def shard(cfg, ctx, scaling):
     return c1 - c0, c0, cfg["n"]
 
 
-def profiled_traffic(workload, n, stage, compute):
+def profiled_kernel(workload, n, stage, compute):
     """dram read+write bytes per launch of the stage's kernel from the committed ncu capture
     (profiles/<wl>_ncu_full.json, tools/ncu_summary.py) when it was taken at this size and
     compute type, else None."""
-    names = {"indices": "indices_kernel", "gather": "gtma::gather_tma_kernel", "covariance": "cov_band_kernel",
+    names = {"indices": "indices_kernel", "gather": "gtma::gather_tma_kernel", "covariance": "cov_flat_kernel",
              "moments": "moments_kernel"}
     path = os.path.join(ROOT, "profiles", f"{workload}_ncu_full.json")
     try:
@@ -449,10 +449,15 @@ def profiled_traffic(workload, n, stage, compute):
             return None
         for k, v in d["kernels"].items():
             if k.startswith(names.get(stage, "?")):
-                return v.get("traffic_bytes")
+                return v
     except Exception:
         return None
     return None
+
+
+def profiled_traffic(workload, n, stage, compute):
+    v = profiled_kernel(workload, n, stage, compute)
+    return v.get("traffic_bytes") if v else None
 
 
 def cov_line(ctx, wl, args, steps, warmup, compute, sampler="oracle", clocks=True):
@@ -540,6 +545,11 @@ def cov_line(ctx, wl, args, steps, warmup, compute, sampler="oracle", clocks=Tru
     upd = n * m * (m + 1) / 2 / (stage_ms["covariance"] * 1e-3)
     per_stage["covariance"]["pair_updates_per_s"] = upd
     per_stage["covariance"]["frac_of_measured_smem_atomic_peak"] = upd / 1.355e12  # tools/microbench/mb_dsmem
+    # K3's binding resource is the shared-memory pipe (profiles/round2/notes.md): its busy fraction
+    # from the committed ncu capture of this shape, when there is one
+    kc = profiled_kernel(wl, n, "covariance", compute)
+    if kc and "l1tex_busy_pct" in kc:
+        per_stage["covariance"]["smem_pipe_busy_frac_ncu"] = kc["l1tex_busy_pct"] / 100.0
     roofline["stages"] = per_stage
     roofline["pass_frac_hbm"] = (4 * p + (4 + vsz) * m) * (n / (ms_step * 1e-3)) / 1e9 / ctx.hbm_peak
     out = {"metric": metric_name(cfg), "value": n_glob / (ms_step * 1e-3), "unit": "samples/s",

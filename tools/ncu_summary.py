@@ -24,6 +24,11 @@ keys = {
     "warps_active_pct": ("sm__warps_active.avg.pct_of_peak_sustained_active", 1.0),
     "registers": ("launch__registers_per_thread", 1.0),
     "shared_atomics": ("smsp__inst_executed_op_shared_atom.sum", 1.0),
+    # the shared-memory / L1 pipe: K3's binding resource (wavefronts; ATOMS ~2 LDS-equivalents)
+    "l1tex_busy_pct": ("l1tex__throughput.avg.pct_of_peak_sustained_active", 1.0),
+    "smem_wavefronts": ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", 1.0),
+    "smem_atom_wavefronts": ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum", 1.0),
+    "smem_ld_wavefronts": ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", 1.0),
 }
 units_row = rows[1]
 out = []
