@@ -447,6 +447,128 @@ __global__ void __launch_bounds__(kSmallThreads, 2) km_assign_small_kernel(
   }
 }
 
+// K5c: small K with the padded tables in shared memory. H = KC/2 lanes cooperate on a point,
+// lane h owning centres 2h and 2h+1 (one 16-byte table read per coordinate), G = 32/H points per
+// warp step, the step's rows staged in shared memory with coalesced loads. Every (point, centre)
+// sum runs in the reference's order (cluster.py:183: values then ones, ascending t), so labels
+// and d2min equal K5s / K5 bit for bit; the argmin is the sequential lowest-index scan.
+constexpr int kCoopWarps = 8;
+__device__ __forceinline__ double colsq_pairwise_row(const double* __restrict__ rv, int m) {
+  // numpy's pairwise-8 sum of squares, the order colsq_pairwise uses
+  if (m < 8) {
+    double c = 0.0;
+    for (int t = 0; t < m; ++t) c = dadd(c, dmul(rv[t], rv[t]));
+    return c;
+  }
+  double r[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r[k] = dmul(rv[k], rv[k]);
+  int t = 8;
+  for (; t < m - (m % 8); t += 8)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = dadd(r[k], dmul(rv[t + k], rv[t + k]));
+  double c = dadd(dadd(dadd(r[0], r[1]), dadd(r[2], r[3])), dadd(dadd(r[4], r[5]), dadd(r[6], r[7])));
+  for (; t < m; ++t) c = dadd(c, dmul(rv[t], rv[t]));
+  return c;
+}
+
+template <typename V, int H>
+__global__ void __launch_bounds__(kCoopWarps * 32, 2) km_assign_coop_kernel(
+    const int32_t* __restrict__ idx, const void* __restrict__ val, int64_t n, int m, const double* __restrict__ tx2,
+    const double* __restrict__ ty2, int K, int p_pad, const int32_t* __restrict__ prev, int32_t* __restrict__ labels,
+    double* __restrict__ d2min, int64_t* __restrict__ blk_changed, double* __restrict__ blk_max,
+    int64_t* __restrict__ blk_arg) {
+  constexpr int G = 32 / H;  // points per warp step
+  extern __shared__ __align__(16) unsigned char csm[];
+  double2* tabx = reinterpret_cast<double2*>(csm);  // [p_pad][H]: (-2 mu) pairs
+  double2* taby = tabx + (size_t)p_pad * H;          // [p_pad][H]: mu^2 pairs
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* sval = reinterpret_cast<double*>(taby + (size_t)p_pad * H) + (size_t)warp * G * m;
+  int* sidx = reinterpret_cast<int*>(reinterpret_cast<double*>(taby + (size_t)p_pad * H) + (size_t)kCoopWarps * G * m) +
+              (size_t)warp * G * m;
+  {
+    const double2* gx = reinterpret_cast<const double2*>(tx2);
+    const double2* gy = reinterpret_cast<const double2*>(ty2);
+    for (int e = threadIdx.x; e < p_pad * H; e += blockDim.x) tabx[e] = __ldg(gx + e), taby[e] = __ldg(gy + e);
+  }
+  __syncthreads();
+  const int g = lane / H, h = lane - g * H;
+  int64_t changed = 0;
+  double bmax = -1.0;
+  int64_t barg = -1;
+  const int64_t step = (int64_t)gridDim.x * kCoopWarps * G;
+  for (int64_t b0 = ((int64_t)blockIdx.x * kCoopWarps + warp) * G; b0 < n; b0 += step) {
+    const int np = (int)min((int64_t)G, n - b0);
+    const int ne = np * m;
+    const int32_t* gi = idx + b0 * m;
+    const V* gv = reinterpret_cast<const V*>(val) + b0 * m;
+    for (int e = lane; e < ne; e += 32) sidx[e] = __ldg(gi + e), sval[e] = (double)__ldg(gv + e);
+    __syncwarp();
+    const bool valid = lane < G * H && g < np;
+    const int* ri = sidx + (valid ? g : 0) * m;
+    const double* rv = sval + (valid ? g : 0) * m;
+    double a0 = 0.0, a1 = 0.0;
+    for (int t = 0; t < m; ++t) {
+      const double v = rv[t];
+      const double2 a = tabx[ri[t] * H + h];
+      a0 = dadd(a0, dmul(v, a.x));
+      a1 = dadd(a1, dmul(v, a.y));
+    }
+    for (int t = 0; t < m; ++t) {
+      const double2 b = taby[ri[t] * H + h];
+      a0 = dadd(a0, b.x);
+      a1 = dadd(a1, b.y);
+    }
+    const double cs = colsq_pairwise_row(rv, m);
+    const double d0 = dadd(a0, cs), d1 = dadd(a1, cs);
+    double best = 0.0;
+    int bk = 0;
+#pragma unroll
+    for (int q = 0; q < H; ++q) {
+      const int src = (g * H + q) & 31;
+      const double x = __shfl_sync(kFM, d0, src), y = __shfl_sync(kFM, d1, src);
+      if (q == 0) best = x;
+      else if (2 * q < K && x < best) best = x, bk = 2 * q;
+      if (2 * q + 1 < K && y < best) best = y, bk = 2 * q + 1;
+    }
+    if (valid && h == 0) {
+      const int64_t i = b0 + g;
+      const double dm = best > 0.0 ? best : 0.0;  // np.clip(.., 0, None)
+      labels[i] = bk;
+      d2min[i] = dm;
+      if (prev != nullptr) changed += prev[i] != bk;
+      if (dm > bmax) bmax = dm, barg = i;  // ascending i per lane: keeps the first max
+    }
+    __syncwarp();  // the staging is reused by the next step
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t oc = __shfl_xor_sync(kFM, changed, o), oa = __shfl_xor_sync(kFM, barg, o);
+    const double om = __shfl_xor_sync(kFM, bmax, o);
+    changed += oc;
+    if (oa >= 0 && (om > bmax || (om == bmax && (barg < 0 || oa < barg)))) bmax = om, barg = oa;
+  }
+  __shared__ int64_t s_ch[kCoopWarps], s_arg[kCoopWarps];
+  __shared__ double s_mx[kCoopWarps];
+  if (lane == 0) s_ch[warp] = changed, s_mx[warp] = bmax, s_arg[warp] = barg;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t c = 0, a = -1;
+    double mx = -1.0;
+    for (int w = 0; w < kCoopWarps; ++w) {
+      c += s_ch[w];
+      if (s_arg[w] >= 0 && (s_mx[w] > mx || (s_mx[w] == mx && (a < 0 || s_arg[w] < a)))) mx = s_mx[w], a = s_arg[w];
+    }
+    blk_changed[blockIdx.x] = c;
+    blk_max[blockIdx.x] = mx;
+    blk_arg[blockIdx.x] = a;
+  }
+}
+static size_t coop_smem(int32_t p_pad, int KC, int m) {
+  const int H = KC / 2, G = 32 / H;
+  return (size_t)p_pad * KC * 16 + (size_t)kCoopWarps * G * m * 12;
+}
+
 __global__ void km_assign_reduce_kernel(const int64_t* __restrict__ blk_changed, const double* __restrict__ blk_max,
                                         const int64_t* __restrict__ blk_arg, int nb, int64_t* out, double* d2max) {
   int64_t c = 0, a = -1;
@@ -816,6 +938,45 @@ int assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, i
     km_tables_pad_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(mu, p_pad, K, KC, tx2, ty2);
     int rc = check_launch("km_tables_pad_kernel");
     if (rc) return rc;
+    // K5c when the padded tables fit shared memory next to the row staging (SKC_ASSIGN_COOP=0: K5s)
+    static const bool coop_on = [] {
+      const char* e = getenv("SKC_ASSIGN_COOP");
+      return !(e && e[0] == '0');
+    }();
+    const size_t csm = coop_smem(p_pad, KC, m);
+    if (coop_on && m <= 64 && csm <= 110 * 1024) {
+      const int H = KC / 2, Gp = 32 / H;
+      int64_t Gc = (n + (int64_t)kCoopWarps * Gp - 1) / ((int64_t)kCoopWarps * Gp);
+      const int64_t cap = 2 * (int64_t)sm_count();
+      if (Gc > cap) Gc = cap;
+      if (Gc > G) Gc = G;  // the per-block arrays hold G entries
+      auto goc = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+        kern<<<(unsigned)Gc, kCoopWarps * 32, csm, st>>>(idx, val, n, m, tx2, ty2, K, p_pad, prev, labels, d2min, bch,
+                                                          reinterpret_cast<double*>(bch + G),
+                                                          reinterpret_cast<int64_t*>(bch + 2 * G));
+      };
+#define SKC_COOP_CASE(HH)                                              \
+  case HH:                                                             \
+    if (val_f64) goc(km_assign_coop_kernel<double, HH>);               \
+    else goc(km_assign_coop_kernel<float, HH>);                        \
+    break;
+      switch (H) {
+        SKC_COOP_CASE(1)
+        SKC_COOP_CASE(2)
+        SKC_COOP_CASE(3)
+        SKC_COOP_CASE(4)
+        SKC_COOP_CASE(5)
+        SKC_COOP_CASE(6)
+        SKC_COOP_CASE(7)
+        SKC_COOP_CASE(8)
+      }
+#undef SKC_COOP_CASE
+      if ((rc = check_launch("km_assign_coop_kernel"))) return rc;
+      km_assign_reduce_kernel<<<1, 1024, 0, st>>>(bch, reinterpret_cast<double*>(bch + G),
+                                                  reinterpret_cast<int64_t*>(bch + 2 * G), (int)Gc, out, d2max);
+      return check_launch("km_assign_reduce_kernel");
+    }
     int64_t Gs = (n + kSmallThreads - 1) / kSmallThreads;
     if (Gs > G) Gs = G;  // the per-block arrays hold G entries
     auto go = [&](auto kern) {
