@@ -256,7 +256,6 @@ struct CovParams {
   unsigned long long* part;  // [groups][tri_total] int64 fixed-point partials
   int nbands, groups;
   int aligned;               // idx/val 16-byte aligned: tiles may use bulk copies
-  unsigned* progress;        // [groups][nbands] chunks done (flat kernel's drift window), or null
   int band_rows[kMaxBands + 1];
 };
 
@@ -479,14 +478,6 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
 //    element is one unsigned compare (indices are sorted, so in-band lanes are [nlo, nhi)).
 //  * The pair loop's induction variable is the pair-table pointer.
 // Rows holding a value above tau (or a wide-range scale) take the exact fp64 path.
-#ifndef SKC_COV_CHUNK
-#define SKC_COV_CHUNK 64  // steps of 32 rows per progress chunk (2048 rows)
-#endif
-#ifndef SKC_COV_WINDOW
-#define SKC_COV_WINDOW 4  // chunks a band may run ahead of its group's slowest band
-#endif
-constexpr int kCovChunk = SKC_COV_CHUNK, kCovWindow = SKC_COV_WINDOW;
-constexpr int kCovSpinNs = 200000;  // give up waiting after ~200 us
 template <typename V>
 __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __grid_constant__ CovParams P) {
   extern __shared__ int smem_i[];
@@ -542,35 +533,7 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __gri
     if (has0) aj0 = __ldg(ip), av0 = __ldg(vp);
     if (has1) aj1 = __ldg(ip + 32), av1 = __ldg(vp + 32);
   }
-  // Drift window: the band CTAs of a group read the same rows; left alone they drift apart by
-  // more than L2 holds and re-read rows from DRAM (8x the algorithmic bytes at C3). Every
-  // kCovChunk rows of its own, a warp records its progress in shared memory, publishes the CTA's
-  // minimum (atomicMax keeps the global counter monotonic), and waits, polling with a bounded
-  // spin, while its group's slowest band is more than kCovWindow chunks behind. No CTA barriers
-  // (a barrier per chunk stalls 32 warps on the slowest); the spin gives up after ~kCovSpinNs,
-  // so CTAs that are not co-resident cannot deadlock it.
-  __shared__ unsigned wprog[kCovWarps];
-  if (lane == 0) wprog[warp] = 0;
-  __syncthreads();
-  const int steps = (nrows - warp + kCovWarps - 1) / kCovWarps;  // this warp's rows
-  unsigned* prog = P.progress != nullptr ? P.progress + (size_t)group * P.nbands : nullptr;
-  for (int q = 0; q < steps; ++q) {
-    if (prog != nullptr && q > 0 && q % kCovChunk == 0) {
-      const unsigned c = (unsigned)(q / kCovChunk);
-      if (lane == 0) *reinterpret_cast<volatile unsigned*>(&wprog[warp]) = c;
-      __syncwarp();
-      const unsigned cmin = __reduce_min_sync(kFullMask, *reinterpret_cast<volatile unsigned*>(&wprog[lane]));
-      if (lane == 0) atomicMax(prog + band, cmin);
-      if (c > (unsigned)kCovWindow) {
-        for (int spin = 0; spin < kCovSpinNs / 256; ++spin) {
-          unsigned v = 0xFFFFFFFFu;
-          if (lane < P.nbands) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(prog + lane) : "memory");
-          if (__reduce_min_sync(kFullMask, v) + (unsigned)kCovWindow >= c) break;
-          __nanosleep(256);
-        }
-      }
-    }
-    const int i = warp + q * kCovWarps;  // < nrows
+  for (int i = warp; i < nrows; i += kCovWarps) {
     const int j0 = aj0, j1 = aj1;
     const float v0 = (float)av0, v1 = (float)av1;
     {
@@ -633,12 +596,6 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __gri
         atomicAdd(part + ((addr - lo_sh) >> 2), (unsigned long long)((long long)(q < 0 ? -1 : 1) << 32));
     }
     __syncwarp();
-  }
-  if (prog != nullptr) {  // done: this warp no longer holds back the CTA's published progress
-    if (lane == 0) *reinterpret_cast<volatile unsigned*>(&wprog[warp]) = 0xFFFFFFFFu;
-    __syncwarp();
-    const unsigned cmin = __reduce_min_sync(kFullMask, *reinterpret_cast<volatile unsigned*>(&wprog[lane]));
-    if (lane == 0) atomicMax(prog + band, cmin);
   }
   __syncthreads();
   for (int e = threadIdx.x; e < ne; e += blockDim.x) {
@@ -811,7 +768,7 @@ size_t cov_ws(int64_t n, int32_t m, int32_t p_pad) {
   if (path == 'g') return (size_t)tri_off(p_pad, p_pad) * sizeof(unsigned long long);
   const int nb = make_bands(p_pad, band_capacity(m, p_pad), nullptr);
   const int g = cov_groups(nb, n);
-  return (size_t)g * tri_off(p_pad, p_pad) * sizeof(unsigned long long) + (size_t)g * nb * sizeof(unsigned);
+  return (size_t)g * tri_off(p_pad, p_pad) * sizeof(unsigned long long);
 }
 
 static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, int32_t p_pad,
@@ -830,11 +787,7 @@ static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int
   H.part = reinterpret_cast<unsigned long long*>(ws);
   H.aligned = (reinterpret_cast<uintptr_t>(idx) % 16 == 0) && (reinterpret_cast<uintptr_t>(val) % 16 == 0);
   const int64_t total = tri_off(p_pad, p_pad);
-  // progress counters of the flat kernel's drift window follow the partials (SKC_COV_WINDOW_OFF=1: off)
-  static const bool window_off = getenv("SKC_COV_WINDOW_OFF") != nullptr;
-  H.progress = window_off ? nullptr
-                          : reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ws) + (size_t)H.groups * total * 8);
-  cudaMemsetAsync(ws, 0, (size_t)H.groups * total * 8 + (size_t)H.groups * H.nbands * sizeof(unsigned), st);
+  cudaMemsetAsync(ws, 0, (size_t)H.groups * total * 8, st);
   int maxe = 0, maxr = 0;
   for (int b = 0; b < H.nbands; ++b) {
     const int e = (int)(tri_off(H.band_rows[b + 1], p_pad) - tri_off(H.band_rows[b], p_pad));

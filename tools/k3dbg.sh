@@ -1,9 +1,13 @@
 mkdir -p gpurun_out
-for e in on off on off; do
-  if [ $e = off ]; then export SKC_COV_WINDOW_OFF=1; else unset SKC_COV_WINDOW_OFF; fi
-  echo "== window $e: $(K3AB_SHAPES=1 timeout 300 python tools/k3_ab.py 24 3 2>&1 | tail -1)"
-done > gpurun_out/k3w_ab.log 2>&1
-cat gpurun_out/k3w_ab.log
-unset SKC_COV_WINDOW_OFF
-K3AB_SHAPES=1 timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,l1tex__throughput.avg.pct_of_peak_sustained_active --clock-control none -k regex:cov_flat_kernel -c 1 python tools/k3_ab.py 24 1 > gpurun_out/k3w_ncu.log 2>&1; grep -E "dram__|gpu__time|l1tex" gpurun_out/k3w_ncu.log
-timeout 900 python -m pytest tests -x -q -m gpu -k "cov or covariance or full_configs" > gpurun_out/k3w_tests.log 2>&1; tail -2 gpurun_out/k3w_tests.log
+run() { python bench.py --no-configs --no-secondary --no-e2e --no-cpu --no-python-ref --steps 5 --warmup 3 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step'],2), {k: round(x,2) for k,x in d['stages_ms'].items()})"; }
+for rep in 1 2; do
+for v in default off r2x; do
+  unset SKC_LIB SKC_COV_WINDOW_OFF
+  case $v in default) ;; off) export SKC_COV_WINDOW_OFF=1 ;; *) export SKC_LIB=$PWD/build/variants/$v/libsketchcu.so ;; esac
+  echo "== $v: $(run)"
+done
+done > gpurun_out/k3r2x_bench2.log 2>&1
+cat gpurun_out/k3r2x_bench2.log
+unset SKC_LIB SKC_COV_WINDOW_OFF
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:cov_flat -c 1 python bench.py --no-configs --no-secondary --no-e2e --no-cpu --no-python-ref --steps 1 --warmup 0 > gpurun_out/k3win_ncu.log 2>&1; grep -E "dram__|gpu__time" gpurun_out/k3win_ncu.log
+timeout 900 python -m pytest tests -x -q -m gpu -k "cov or covariance" > gpurun_out/k3win_tests.log 2>&1; tail -1 gpurun_out/k3win_tests.log
