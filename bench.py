@@ -460,6 +460,17 @@ def profiled_traffic(workload, n, stage, compute):
     return v.get("traffic_bytes") if v else None
 
 
+def lloyd_traffic(workload, n):
+    """DRAM read+write bytes per Lloyd iteration (the K-means roofline's 'launch') from the committed
+    ncu launch list (profiles/<wl>_ncu_lloyd.json, tools/ncu_iter_traffic.py) taken at this n, else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"{workload}_ncu_lloyd.json")) as f:
+            d = json.load(f)
+        return d["dram_bytes_per_iteration"] if int(d["points"]) == int(n) else None
+    except Exception:
+        return None
+
+
 def cov_line(ctx, wl, args, steps, warmup, compute, sampler="oracle", clocks=True):
     """HBM-resident covariance pass (K1a..K4), stage-timed with CUDA events on the stream."""
     torch, skc, lib = ctx.torch, ctx.skc, ctx.lib
@@ -671,7 +682,7 @@ def kmeans_line(ctx, wl, args, steps, warmup, clocks=True):
            "rows_per_gpu": n, "global_rows": n_glob,
            "roofline": {"bound": "hbm", "kernel": "lloyd iteration (assign + partials + centres)",
                         "achieved": gbs, "peak": ctx.hbm_peak, "unit": "GB/s", "frac": gbs / ctx.hbm_peak,
-                        "traffic": None, "peak_source": ctx.peak_src, "bytes_per_point_iter": ub}}
+                        "traffic": lloyd_traffic(wl, n), "peak_source": ctx.peak_src, "bytes_per_point_iter": ub}}
     if clk:
         out["clocks"] = clk.summary()
     del sk, ops
