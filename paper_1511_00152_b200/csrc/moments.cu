@@ -183,6 +183,10 @@ int moments_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, 
 // point and independent of order (deterministic). At the end the CTA adds its low words
 // into the same int64 partial. A reduce kernel sums the groups in int64 and scales to fp64.
 // tau = 8 * rms(values), from K2's statistics. Quantum 2^-S ~ 6e-8 * tau^2.
+// Two kernels share this scheme: cov_flat_kernel (m <= 64, the default; lean per-visit work and
+// a packed pair table) and cov_band_kernel (m > 64, or SKC_COV_KERNEL=band). Both are bound by
+// the shared-memory pipe: an ATOMS wavefront costs about two load wavefronts, and random 32-lane
+// atomics average 3.3 wavefronts of bank conflicts (profiles/round2/notes.md).
 // ======================================================================================
 #ifndef SKC_COV_UNROLL
 #define SKC_COV_UNROLL 1  // unroll of the flat pair loop (experiments)
