@@ -939,10 +939,8 @@ int assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, i
     int rc = check_launch("km_tables_pad_kernel");
     if (rc) return rc;
     // K5c when the padded tables fit shared memory next to the row staging (SKC_ASSIGN_COOP=0: K5s)
-    static const bool coop_on = [] {
-      const char* e = getenv("SKC_ASSIGN_COOP");
-      return !(e && e[0] == '0');
-    }();
+    const char* coop_env = getenv("SKC_ASSIGN_COOP");  // read per call: tests compare both kernels
+    const bool coop_on = !(coop_env && coop_env[0] == '0');
     const size_t csm = coop_smem(p_pad, KC, m);
     if (coop_on && m <= 64 && csm <= 110 * 1024) {
       const int H = KC / 2, Gp = 32 / H;
