@@ -476,8 +476,8 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
 
 // K3 flat kernel (m <= 64, the configs' shapes): the same fixed-point band accumulation as
 // cov_band_kernel, with the per-visit work cut to what the pair loop needs.
-//  * rowaddr[a - r0] holds the shared byte address of entry (a, 0), so a staged T entry is
-//    the address itself; F(t) comes from a u16 table instead of multiplies.
+//  * A staged T entry is the shared byte address of entry (a, 0) itself, computed in registers
+//    like F(t) (no table loads).
 //  * Rows are walked with 32-bit counters and pointer bumps; band membership of a lane's
 //    element is one unsigned compare (indices are sorted, so in-band lanes are [nlo, nhi)).
 //  * The pair loop's induction variable is the pair-table pointer.
@@ -510,9 +510,10 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __gri
   double* tri_b = P.tri + e0;
 
   for (int e = threadIdx.x; e < ne; e += blockDim.x) lo[e] = kBias;
-  for (int a = r0 + threadIdx.x; a < r1; a += blockDim.x)
-    rowaddr[a - r0] = lo_sh + 4u * (uint32_t)((tri_off(a, P.p_pad) - e0) - a);
-  if (threadIdx.x <= m) ptoff[threadIdx.x] = (uint16_t)(threadIdx.x * m - ((threadIdx.x * (threadIdx.x - 1)) >> 1));
+  // row addresses and the pair-list offsets F(t) are computed in registers (two fewer shared
+  // loads per visit, ~7% of the kernel's shared-memory wavefronts); their layout slots stay unused
+  const uint32_t rb = lo_sh - 4u * (uint32_t)e0;  // entry (a, 0) at rb + 4 (a (p - 1) - a (a - 1) / 2)
+  const uint32_t pm1 = (uint32_t)P.p_pad - 1u;
   if (threadIdx.x < m) {
     const int t = threadIdx.x, f0 = t * m - ((t * (t - 1)) >> 1);
     for (int u = t; u < m; ++u) ptab[f0 + u - t] = (uint32_t)(8 * t) | ((uint32_t)(8 * (m + u)) << 16);
@@ -558,7 +559,8 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __gri
       const V* vr = val + r * m;
       for (int t = nlo; t < nhi; ++t) {
         const double va = (double)__ldg(vr + t);
-        const int base = (int)(rowaddr[__ldg(ir + t) - r0] - lo_sh) >> 2;  // signed: entry (a, 0) may precede e0
+        const uint32_t a = (uint32_t)__ldg(ir + t);
+        const int base = (int)(a * pm1 - ((a * (a - 1u)) >> 1)) - (int)e0;  // signed: entry (a, 0) may precede e0
         for (int u = t + lane; u < m; u += 32) {
           const int e = base + __ldg(ir + u);
 #ifdef SKC_COV_DEBUG
@@ -575,11 +577,18 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __gri
     const float s0 = v0 * sh, s1 = v1 * sh;  // exact power-of-two scalings
     if (has0) S[m + lane] = make_int2(j0 << 2, __float_as_int(s0));
     if (has1) S[m + 32 + lane] = make_int2(j1 << 2, __float_as_int(s1));
-    if ((uint32_t)(j0 - r0) < bw) S[lane] = make_int2((int)rowaddr[j0 - r0], __float_as_int(s0));
-    if ((uint32_t)(j1 - r0) < bw) S[lane + 32] = make_int2((int)rowaddr[j1 - r0], __float_as_int(s1));
+    // shared address of entry (a, 0), in registers: lo + 4 (a (p - 1) - a (a - 1) / 2 - e0)
+    if ((uint32_t)(j0 - r0) < bw) {
+      const uint32_t a = (uint32_t)j0;
+      S[lane] = make_int2((int)(rb + 4u * (a * pm1 - ((a * (a - 1u)) >> 1))), __float_as_int(s0));
+    }
+    if ((uint32_t)(j1 - r0) < bw) {
+      const uint32_t a = (uint32_t)j1;
+      S[lane + 32] = make_int2((int)(rb + 4u * (a * pm1 - ((a * (a - 1u)) >> 1))), __float_as_int(s1));
+    }
     __syncwarp();
-    const uint32_t* tp = ptab + ptoff[nlo] + lane;
-    const uint32_t* const te = ptab + ptoff[nhi];
+    const uint32_t* tp = ptab + (nlo * m - ((nlo * (nlo - 1)) >> 1)) + lane;  // F(t) in registers
+    const uint32_t* const te = ptab + (nhi * m - ((nhi * (nhi - 1)) >> 1));
     for (; tp < te; tp += 32) {
       const uint32_t pe = *tp;
       int tx, ty, ux, uy;
