@@ -217,7 +217,10 @@ static char band_kind(int32_t m) {
   const char* k = getenv("SKC_COV_KERNEL");
   return (k && k[0] == 'b') ? 'b' : 'f';
 }
+static size_t flat_ptab_bytes(int32_t m) { return (((size_t)m * (m + 1) / 2 + 1) & ~(size_t)1) * 4; }
 static int band_capacity(int32_t m, int32_t p_pad) {
+  if (band_kind(m) == 'f')  // lo words + the pair table + per-warp U staging
+    return (int)(((size_t)kSmemBudget - (size_t)kCovWarps * m * 8 - flat_ptab_bytes(m)) / 4);
   // int32 entries left after the per-warp row staging, the row table and the pair table
   return (int)(((size_t)kSmemBudget - (size_t)kCovWarps * m * 16 - 4 * (size_t)p_pad - pair_table_bytes(m)) / 4);
 }
@@ -476,8 +479,10 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
 
 // K3 flat kernel (m <= 64, the configs' shapes): the same fixed-point band accumulation as
 // cov_band_kernel, with the per-visit work cut to what the pair loop needs.
-//  * A staged T entry is the shared byte address of entry (a, 0) itself, computed in registers
-//    like F(t) (no table loads).
+//  * A warp stages only U[u] = (4 j_u, w_u 2^(S/2)) per row; pair (t, u) reads U[t] and U[u]
+//    and forms the shared address of band row j_t in registers (a (p - 1) - a (a - 1) / 2), as it
+//    does F(t): no row-address or offset tables, half the staging, so the band holds more entries
+//    (10 bands at C3 instead of 11, one row visit fewer).
 //  * Rows are walked with 32-bit counters and pointer bumps; band membership of a lane's
 //    element is one unsigned compare (indices are sorted, so in-band lanes are [nlo, nhi)).
 //  * The pair loop's induction variable is the pair-table pointer.
@@ -492,12 +497,10 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __gri
   const int64_t e0 = tri_off(r0, P.p_pad), e1 = tri_off(r1, P.p_pad);
   const int ne = (int)(e1 - e0);
   uint32_t* lo = reinterpret_cast<uint32_t*>(smem_i);
-  uint32_t* rowaddr = lo + ((ne + 1) & ~1);  // [r1 - r0]
   const int npair = m * (m + 1) / 2;
-  // pair f: byte offsets of T[t] and U[u] in the warp's staging, 8 t | 8 (m + u) << 16
-  uint32_t* ptab = rowaddr + ((r1 - r0 + 1) & ~1);
-  uint16_t* ptoff = reinterpret_cast<uint16_t*>(ptab + ((npair + 1) & ~1));  // [m + 1]
-  int2* S = reinterpret_cast<int2*>(ptoff + ((m + 4) & ~3)) + (size_t)warp * 2 * m;  // T[m] then U[m]
+  // pair f: byte offsets of U[t] and U[u] in the warp's staging, 8 t | 8 u << 16
+  uint32_t* ptab = lo + ((ne + 1) & ~1);
+  int2* S = reinterpret_cast<int2*>(ptab + ((npair + 1) & ~1)) + (size_t)warp * m;  // U[m]
   unsigned long long* part = P.part + (size_t)group * tri_off(P.p_pad, P.p_pad) + e0;
   const uint32_t lo_sh = (uint32_t)__cvta_generic_to_shared(lo);
 
@@ -510,13 +513,13 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __gri
   double* tri_b = P.tri + e0;
 
   for (int e = threadIdx.x; e < ne; e += blockDim.x) lo[e] = kBias;
-  // row addresses and the pair-list offsets F(t) are computed in registers (two fewer shared
-  // loads per visit, ~7% of the kernel's shared-memory wavefronts); their layout slots stay unused
+  // band-row addresses and the pair-list offsets F(t) are computed in registers (fewer shared
+  // loads per visit: ~7% of the kernel's shared-memory wavefronts)
   const uint32_t rb = lo_sh - 4u * (uint32_t)e0;  // entry (a, 0) at rb + 4 (a (p - 1) - a (a - 1) / 2)
   const uint32_t pm1 = (uint32_t)P.p_pad - 1u;
   if (threadIdx.x < m) {
     const int t = threadIdx.x, f0 = t * m - ((t * (t - 1)) >> 1);
-    for (int u = t; u < m; ++u) ptab[f0 + u - t] = (uint32_t)(8 * t) | ((uint32_t)(8 * (m + u)) << 16);
+    for (int u = t; u < m; ++u) ptab[f0 + u - t] = (uint32_t)(8 * t) | ((uint32_t)(8 * u) << 16);
   }
   __syncthreads();
 
@@ -575,17 +578,8 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __gri
       continue;
     }
     const float s0 = v0 * sh, s1 = v1 * sh;  // exact power-of-two scalings
-    if (has0) S[m + lane] = make_int2(j0 << 2, __float_as_int(s0));
-    if (has1) S[m + 32 + lane] = make_int2(j1 << 2, __float_as_int(s1));
-    // shared address of entry (a, 0), in registers: lo + 4 (a (p - 1) - a (a - 1) / 2 - e0)
-    if ((uint32_t)(j0 - r0) < bw) {
-      const uint32_t a = (uint32_t)j0;
-      S[lane] = make_int2((int)(rb + 4u * (a * pm1 - ((a * (a - 1u)) >> 1))), __float_as_int(s0));
-    }
-    if ((uint32_t)(j1 - r0) < bw) {
-      const uint32_t a = (uint32_t)j1;
-      S[lane + 32] = make_int2((int)(rb + 4u * (a * pm1 - ((a * (a - 1u)) >> 1))), __float_as_int(s1));
-    }
+    if (has0) S[lane] = make_int2(j0 << 2, __float_as_int(s0));
+    if (has1) S[lane + 32] = make_int2(j1 << 2, __float_as_int(s1));
     __syncwarp();
     const uint32_t* tp = ptab + (nlo * m - ((nlo * (nlo - 1)) >> 1)) + lane;  // F(t) in registers
     const uint32_t* const te = ptab + (nhi * m - ((nhi * (nhi - 1)) >> 1));
@@ -594,7 +588,8 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __gri
       int tx, ty, ux, uy;
       asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(tx), "=r"(ty) : "r"(S_sh + (pe & 0xFFFFu)));
       asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(ux), "=r"(uy) : "r"(S_sh + (pe >> 16)));
-      const uint32_t addr = (uint32_t)(tx + ux);
+      const uint32_t ta = (uint32_t)tx >> 2;  // j_t: the band row's address in registers
+      const uint32_t addr = rb + 4u * (ta * pm1 - ((ta * (ta - 1u)) >> 1)) + (uint32_t)ux;
 #ifdef SKC_COV_DEBUG
       if (addr < lo_sh || addr >= lo_sh + 4u * (uint32_t)ne || (addr & 3)) {
         printf("cov_flat: bad addr %u (lo %u ne %d) band %d row %d t %d u %d nlo %d nhi %d\n", addr, lo_sh, ne, band,
@@ -807,9 +802,10 @@ static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int
     if (e > maxe) maxe = e;
     if (H.band_rows[b + 1] - H.band_rows[b] > maxr) maxr = H.band_rows[b + 1] - H.band_rows[b];
   }
-  const size_t smem = (size_t)((maxe + 1) & ~1) * 4 + (size_t)((maxr + 1) & ~1) * 4 + pair_table_bytes(m) +
-                      (size_t)kCovWarps * m * 16;
   const bool flat = band_kind(m) == 'f';
+  const size_t smem = flat ? (size_t)((maxe + 1) & ~1) * 4 + flat_ptab_bytes(m) + (size_t)kCovWarps * m * 8
+                           : (size_t)((maxe + 1) & ~1) * 4 + (size_t)((maxr + 1) & ~1) * 4 + pair_table_bytes(m) +
+                                 (size_t)kCovWarps * m * 16;
   auto k = val_f64 ? (m > 64 ? cov_band_kernel<double, true> : flat ? cov_flat_kernel<double> : cov_band_kernel<double, false>)
                    : (m > 64 ? cov_band_kernel<float, true> : flat ? cov_flat_kernel<float> : cov_band_kernel<float, false>);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
