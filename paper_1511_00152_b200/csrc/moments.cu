@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
 //    element is one unsigned compare (indices are sorted, so in-band lanes are [nlo, nhi)).
 //  * The pair loop's induction variable is the pair-table pointer.
 // Rows holding a value above tau (or a wide-range scale) take the exact fp64 path.
-template <typename V>
+template <typename V, bool PK>  // PK (p_pad <= 2048): U.x packs (row offset of j) << 11 | j
 __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __grid_constant__ CovParams P) {
   extern __shared__ int smem_i[];
   const int m = P.m;
@@ -578,8 +578,17 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __gri
       continue;
     }
     const float s0 = v0 * sh, s1 = v1 * sh;  // exact power-of-two scalings
-    if (has0) S[lane] = make_int2(j0 << 2, __float_as_int(s0));
-    if (has1) S[lane + 32] = make_int2(j1 << 2, __float_as_int(s1));
+    if constexpr (PK) {
+      // U.x = rowoff(j) << 11 | j, rowoff(a) = a (p - 1) - a (a - 1) / 2 < 2^21 for p <= 2048:
+      // a pair's entry is then rb + 4 (rowoff(j_t) + j_u), four instructions per pair
+      const uint32_t a0 = (uint32_t)j0, a1 = (uint32_t)j1;
+      if (has0) S[lane] = make_int2((int)(((a0 * pm1 - ((a0 * (a0 - 1u)) >> 1)) << 11) | a0), __float_as_int(s0));
+      if (has1)
+        S[lane + 32] = make_int2((int)(((a1 * pm1 - ((a1 * (a1 - 1u)) >> 1)) << 11) | a1), __float_as_int(s1));
+    } else {
+      if (has0) S[lane] = make_int2(j0 << 2, __float_as_int(s0));
+      if (has1) S[lane + 32] = make_int2(j1 << 2, __float_as_int(s1));
+    }
     __syncwarp();
     const uint32_t* tp = ptab + (nlo * m - ((nlo * (nlo - 1)) >> 1)) + lane;  // F(t) in registers
     const uint32_t* const te = ptab + (nhi * m - ((nhi * (nhi - 1)) >> 1));
@@ -588,8 +597,13 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __gri
       int tx, ty, ux, uy;
       asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(tx), "=r"(ty) : "r"(S_sh + (pe & 0xFFFFu)));
       asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(ux), "=r"(uy) : "r"(S_sh + (pe >> 16)));
-      const uint32_t ta = (uint32_t)tx >> 2;  // j_t: the band row's address in registers
-      const uint32_t addr = rb + 4u * (ta * pm1 - ((ta * (ta - 1u)) >> 1)) + (uint32_t)ux;
+      uint32_t addr;
+      if constexpr (PK) {
+        addr = rb + 4u * (((uint32_t)tx >> 11) + ((uint32_t)ux & 0x7FFu));
+      } else {
+        const uint32_t ta = (uint32_t)tx >> 2;  // j_t: the band row's address in registers
+        addr = rb + 4u * (ta * pm1 - ((ta * (ta - 1u)) >> 1)) + (uint32_t)ux;
+      }
 #ifdef SKC_COV_DEBUG
       if (addr < lo_sh || addr >= lo_sh + 4u * (uint32_t)ne || (addr & 3)) {
         printf("cov_flat: bad addr %u (lo %u ne %d) band %d row %d t %d u %d nlo %d nhi %d\n", addr, lo_sh, ne, band,
@@ -806,8 +820,13 @@ static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int
   const size_t smem = flat ? (size_t)((maxe + 1) & ~1) * 4 + flat_ptab_bytes(m) + (size_t)kCovWarps * m * 8
                            : (size_t)((maxe + 1) & ~1) * 4 + (size_t)((maxr + 1) & ~1) * 4 + pair_table_bytes(m) +
                                  (size_t)kCovWarps * m * 16;
-  auto k = val_f64 ? (m > 64 ? cov_band_kernel<double, true> : flat ? cov_flat_kernel<double> : cov_band_kernel<double, false>)
-                   : (m > 64 ? cov_band_kernel<float, true> : flat ? cov_flat_kernel<float> : cov_band_kernel<float, false>);
+  const bool pk = p_pad <= 2048;  // the packed U.x of the flat kernel
+  auto k = val_f64 ? (m > 64 ? cov_band_kernel<double, true>
+                             : flat ? (pk ? cov_flat_kernel<double, true> : cov_flat_kernel<double, false>)
+                                    : cov_band_kernel<double, false>)
+                   : (m > 64 ? cov_band_kernel<float, true>
+                             : flat ? (pk ? cov_flat_kernel<float, true> : cov_flat_kernel<float, false>)
+                                    : cov_band_kernel<float, false>);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<H.nbands * H.groups, kCovWarps * 32, smem, st>>>(H);
   int rc = check_launch("cov_band_kernel");
