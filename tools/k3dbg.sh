@@ -1,1 +1,6 @@
-timeout 600 python bench.py --workload c2 --no-cpu --no-configs --no-secondary --no-python-ref --steps 5 --warmup 3 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e'])"
+for r in 1 2; do
+timeout 300 python tools/idx_probe.py 1024 51 16777216 5 2>&1 | tail -1
+timeout 300 python tools/idx_probe.py 4096 82 2097152 5 2>&1 | tail -1
+timeout 300 python tools/idx_probe.py 512 26 200000 20 2>&1 | tail -1
+done
+timeout 600 python -m pytest tests -x -q -m gpu -k "indices or sketch or golden or philox or scale or full_configs and c1" > gpurun_out/idxf_tests.log 2>&1; tail -1 gpurun_out/idxf_tests.log
