@@ -126,6 +126,19 @@ __global__ void __launch_bounds__(1024) pairwise_combine_kernel(const double* __
 
 size_t pairwise_ws() { return ((size_t)1 << kPwDeep) * (sizeof(double) + 1); }
 
+// the leaves alone (the Lloyd graph combines them in its objective-and-check kernel): subtree
+// sums in ws as [2^kPwDeep] doubles then [2^kPwDeep] depth bytes, *D_out the split depth
+int pairwise_leaves_launch(const double* x, int64_t n, void* ws, int* D_out, cudaStream_t st) {
+  double* res = reinterpret_cast<double*>(ws);
+  uint8_t* ld = reinterpret_cast<uint8_t*>(res + (1 << kPwDeep));
+  int D = 0;
+  while (D < kPwDeep && ((int64_t)128 << D) < n) ++D;
+  const int threads = 8 << D;
+  pairwise_leaves_kernel<<<(threads + 255) / 256, 256, 0, st>>>(x, n, D, res, ld);
+  *D_out = D;
+  return check_launch("pairwise_leaves_kernel");
+}
+
 int pairwise_launch(const double* x, int64_t n, double* out, void* ws, cudaStream_t st) {
   double* res = reinterpret_cast<double*>(ws);
   uint8_t* ld = reinterpret_cast<uint8_t*>(res + (1 << kPwDeep));
@@ -569,6 +582,152 @@ static size_t coop_smem(int32_t p_pad, int KC, int m) {
   return (size_t)p_pad * KC * 16 + (size_t)kCoopWarps * G * m * 12;
 }
 
+// K5r: K5c with one table pass. The shared table holds mu itself ([p_pad + 1][H] pairs, half of
+// K5c's two planes, loaded straight from the centres: no table kernel; row p_pad is zero); a lane
+// keeps the mu values of its point's coordinates in registers for the second half of the chain.
+// The terms are the reference's bit for bit: fl((-2 v) mu) = fl(v (-2 mu)) (both round the same
+// real number, the factors of -2 are exact) and fl(mu mu) is the table's square. Rows are staged
+// padded to MT entries with (coordinate p_pad, value 0): a padded term is (-0)(0) = -0 or
+// (0)(0) = +0, and adding a zero leaves the accumulator as it is (it starts at +0 and so is
+// never -0), so the unrolled loops need no predicates and the loads batch ahead of the chain.
+// Same chain order as K5c / K5s: labels and d2min are bit-identical. m <= MT <= 32 (registers).
+#ifndef SKC_REG_WARPS
+#define SKC_REG_WARPS 8
+#endif
+constexpr int kRegWarps = SKC_REG_WARPS;
+template <typename V, int H, int MT>
+__global__ void __launch_bounds__(kRegWarps * 32, 1) km_assign_reg_kernel(
+    const int32_t* __restrict__ idx, const void* __restrict__ val, int64_t n, int m, const double* __restrict__ mu,
+    int K, int p_pad, const int32_t* __restrict__ prev, int32_t* __restrict__ labels, double* __restrict__ d2min,
+    int64_t* __restrict__ blk_changed, double* __restrict__ blk_max, int64_t* __restrict__ blk_arg) {
+  constexpr int G = 32 / H;                 // points per warp step
+  constexpr int NE = G * MT;                // staged entries per warp step
+  constexpr int RS = MT | 1;                // staged row stride (odd: the G rows start in distinct banks)
+  constexpr int PF = (NE + 31) / 32;        // per lane
+  constexpr bool kPrefetch = PF <= 8;       // next step's rows in registers during this step's chains
+  extern __shared__ __align__(16) unsigned char csm[];
+  double2* tab = reinterpret_cast<double2*>(csm);  // [p_pad + 1][H]: (mu[j][2h], mu[j][2h+1])
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* sval = reinterpret_cast<double*>(tab + (size_t)(p_pad + 1) * H) + (size_t)warp * G * RS;
+  int* sidx = reinterpret_cast<int*>(reinterpret_cast<double*>(tab + (size_t)(p_pad + 1) * H) + (size_t)kRegWarps * G * RS) +
+              (size_t)warp * G * RS;
+  for (int e = threadIdx.x; e < (p_pad + 1) * H; e += blockDim.x) {
+    const int j = e / H, c = 2 * (e - j * H);
+    const double* r = mu + (size_t)j * K;
+    const bool row = j < p_pad;
+    tab[e] = make_double2(row && c < K ? __ldg(r + c) : 0.0, row && c + 1 < K ? __ldg(r + c + 1) : 0.0);
+  }
+  __syncthreads();
+  const int g = lane / H, h = lane - g * H;
+  const V* const vals = reinterpret_cast<const V*>(val);
+  int64_t changed = 0;
+  double bmax = -1.0;
+  int64_t barg = -1;
+  const int64_t step = (int64_t)gridDim.x * kRegWarps * G;
+  int pi[PF];
+  V pv[PF];
+  // entry e of a step: point e / MT, slot e % MT; slots past m are the zero row
+  auto fetch = [&](int64_t b0) {
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int e = lane + 32 * q, gp = e / MT, t = e - gp * MT;
+      const bool ok = e < NE && t < m && b0 + gp < n;
+      const int64_t at = (b0 + gp) * m + t;
+      pi[q] = ok ? __ldg(idx + at) : p_pad;
+      pv[q] = ok ? __ldg(vals + at) : (V)0;
+    }
+  };
+  int64_t b0 = ((int64_t)blockIdx.x * kRegWarps + warp) * G;
+  if (kPrefetch && b0 < n) fetch(b0);
+  for (; b0 < n; b0 += step) {
+    if (!kPrefetch) fetch(b0);
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int e = lane + 32 * q, gp = e / MT;
+      if (e < NE) sidx[e + gp * (RS - MT)] = pi[q], sval[e + gp * (RS - MT)] = (double)pv[q];
+    }
+    __syncwarp();
+    if (kPrefetch && b0 + step < n) fetch(b0 + step);
+    const int np = (int)min((int64_t)G, n - b0);
+    const bool valid = lane < G * H && g < np;
+    const int* ri = sidx + (lane < G * H ? g : 0) * RS;
+    const double* rv = sval + (lane < G * H ? g : 0) * RS;
+    double m0[MT], m1[MT];
+    double a0 = 0.0, a1 = 0.0;
+    // colsq in numpy's pairwise order from the same value reads: eight running sums over the
+    // full groups of eight (t < m8), the tail added in order after their combine
+    const int m8 = m < 8 ? 0 : m - (m & 7);
+    double r8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int t = 0; t < MT; ++t) {
+      const double v = rv[t];
+      if (t < 8) r8[t] = dmul(v, v);  // slots >= m8 are not used below
+      else if (t < m8) r8[t & 7] = dadd(r8[t & 7], dmul(v, v));
+      const double v2 = dmul(-2.0, v);
+      const double2 u = tab[ri[t] * H + h];
+      m0[t] = u.x;
+      m1[t] = u.y;
+      a0 = dadd(a0, dmul(v2, u.x));
+      a1 = dadd(a1, dmul(v2, u.y));
+    }
+#pragma unroll
+    for (int t = 0; t < MT; ++t) {
+      a0 = dadd(a0, dmul(m0[t], m0[t]));
+      a1 = dadd(a1, dmul(m1[t], m1[t]));
+    }
+    double cs = 0.0;
+    if (m8) cs = dadd(dadd(dadd(r8[0], r8[1]), dadd(r8[2], r8[3])), dadd(dadd(r8[4], r8[5]), dadd(r8[6], r8[7])));
+    for (int t = m8; t < m; ++t) cs = dadd(cs, dmul(rv[t], rv[t]));
+    const double d0 = dadd(a0, cs), d1 = dadd(a1, cs);
+    double best = 0.0;
+    int bk = 0;
+#pragma unroll
+    for (int q = 0; q < H; ++q) {
+      const int src = (g * H + q) & 31;
+      const double x = __shfl_sync(kFM, d0, src), y = __shfl_sync(kFM, d1, src);
+      if (q == 0) best = x;
+      else if (2 * q < K && x < best) best = x, bk = 2 * q;
+      if (2 * q + 1 < K && y < best) best = y, bk = 2 * q + 1;
+    }
+    if (valid && h == 0) {
+      const int64_t i = b0 + g;
+      const double dm = best > 0.0 ? best : 0.0;  // np.clip(.., 0, None)
+      labels[i] = bk;
+      d2min[i] = dm;
+      if (prev != nullptr) changed += prev[i] != bk;
+      if (dm > bmax) bmax = dm, barg = i;  // ascending i per lane: keeps the first max
+    }
+    __syncwarp();  // the staging is reused by the next step
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t oc = __shfl_xor_sync(kFM, changed, o), oa = __shfl_xor_sync(kFM, barg, o);
+    const double om = __shfl_xor_sync(kFM, bmax, o);
+    changed += oc;
+    if (oa >= 0 && (om > bmax || (om == bmax && (barg < 0 || oa < barg)))) bmax = om, barg = oa;
+  }
+  __shared__ int64_t s_ch[kRegWarps], s_arg[kRegWarps];
+  __shared__ double s_mx[kRegWarps];
+  if (lane == 0) s_ch[warp] = changed, s_mx[warp] = bmax, s_arg[warp] = barg;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t c = 0, a = -1;
+    double mx = -1.0;
+    for (int w = 0; w < kRegWarps; ++w) {
+      c += s_ch[w];
+      if (s_arg[w] >= 0 && (s_mx[w] > mx || (s_mx[w] == mx && (a < 0 || s_arg[w] < a)))) mx = s_mx[w], a = s_arg[w];
+    }
+    blk_changed[blockIdx.x] = c;
+    blk_max[blockIdx.x] = mx;
+    blk_arg[blockIdx.x] = a;
+  }
+}
+static int reg_mt(int m) { return m <= 8 ? 8 : m <= 16 ? 16 : m <= 24 ? 24 : m <= 28 ? 28 : 32; }
+static size_t reg_smem(int32_t p_pad, int KC, int m) {
+  const int H = KC / 2, G = 32 / H;
+  return (size_t)(p_pad + 1) * KC * 8 + (size_t)kRegWarps * G * (reg_mt(m) | 1) * 12;
+}
+
 __global__ void km_assign_reduce_kernel(const int64_t* __restrict__ blk_changed, const double* __restrict__ blk_max,
                                         const int64_t* __restrict__ blk_arg, int nb, int64_t* out, double* d2max) {
   int64_t c = 0, a = -1;
@@ -932,6 +1091,53 @@ int assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, i
   }();
   if (n > 0 && small_on && K <= 16 && m <= 128 && !use_filter(p_pad, K)) {
     const int KC = (K + 1) & ~1;
+    // K5r when m fits the register copy of the row's centres (SKC_ASSIGN_REG=0: K5c / K5s)
+    const char* reg_env = getenv("SKC_ASSIGN_REG");  // read per call: tests compare the kernels
+    const bool reg_on = !(reg_env && reg_env[0] == '0');
+    const size_t rsm = reg_smem(p_pad, KC, m);
+    if (reg_on && m <= 32 && rsm <= 200 * 1024) {
+      const int H = KC / 2, Gp = 32 / H;
+      int64_t Gc = (n + (int64_t)kRegWarps * Gp - 1) / ((int64_t)kRegWarps * Gp);
+      const int64_t cap = (int64_t)sm_count();  // one CTA per SM (registers)
+      if (Gc > cap) Gc = cap;
+      if (Gc > G) Gc = G;  // the per-block arrays hold G entries
+      auto gor = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
+        kern<<<(unsigned)Gc, kRegWarps * 32, rsm, st>>>(idx, val, n, m, mu, K, p_pad, prev, labels, d2min, bch,
+                                                         reinterpret_cast<double*>(bch + G),
+                                                         reinterpret_cast<int64_t*>(bch + 2 * G));
+      };
+#define SKC_REG_MT(HH, MM)                                                        \
+  if (val_f64) gor(km_assign_reg_kernel<double, HH, MM>);                         \
+  else gor(km_assign_reg_kernel<float, HH, MM>);
+#define SKC_REG_CASE(HH)                                                          \
+  case HH:                                                                        \
+    switch (reg_mt(m)) {                                                          \
+      case 8: SKC_REG_MT(HH, 8) break;                                            \
+      case 16: SKC_REG_MT(HH, 16) break;                                          \
+      case 24: SKC_REG_MT(HH, 24) break;                                          \
+      case 28: SKC_REG_MT(HH, 28) break;                                          \
+      default: SKC_REG_MT(HH, 32) break;                                          \
+    }                                                                             \
+    break;
+      switch (H) {
+        SKC_REG_CASE(1)
+        SKC_REG_CASE(2)
+        SKC_REG_CASE(3)
+        SKC_REG_CASE(4)
+        SKC_REG_CASE(5)
+        SKC_REG_CASE(6)
+        SKC_REG_CASE(7)
+        SKC_REG_CASE(8)
+      }
+#undef SKC_REG_CASE
+#undef SKC_REG_MT
+      int rcr = check_launch("km_assign_reg_kernel");
+      if (rcr) return rcr;
+      km_assign_reduce_kernel<<<1, 1024, 0, st>>>(bch, reinterpret_cast<double*>(bch + G),
+                                                  reinterpret_cast<int64_t*>(bch + 2 * G), (int)Gc, out, d2max);
+      return check_launch("km_assign_reduce_kernel");
+    }
     double* tx2 = tx;
     double* ty2 = tx + (size_t)p_pad * KC;
     const int64_t tot = (int64_t)p_pad * KC;
@@ -1638,6 +1844,7 @@ int csc_build_launch(const int32_t* idx, const void* val, int val_f64, int64_t n
 }
 
 static int sizes_launch(const int32_t* labels, int64_t n, int32_t K, int64_t* sizes, cudaStream_t st) {
+  if (sizes == nullptr) return SKC_OK;  // the caller derives them from the counts (sum_j counts[j][k] = m n_k)
   cudaMemsetAsync(sizes, 0, (size_t)K * 8, st);
   if (n > 0) {
     int64_t blocks = (n + 255) / 256;

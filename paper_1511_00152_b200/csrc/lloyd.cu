@@ -28,6 +28,7 @@ namespace skc {
 size_t assign_ws(int64_t, int32_t, int32_t);
 size_t kmtc_assign_ws(int64_t, int32_t, int32_t);
 size_t pairwise_ws();
+int pairwise_leaves_launch(const double* x, int64_t n, void* ws, int* D_out, cudaStream_t st);
 size_t seg_ws(int64_t, int32_t, int32_t, int32_t, int);
 void note_launches(int64_t delta);
 
@@ -50,6 +51,85 @@ __global__ void lloyd_commit_kernel(const int32_t* __restrict__ state, const dou
   if (state[1]) return;  // converged: the centres of the final assignment stay
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pk; i += stride) mu[i] = mu_next[i];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) prev[i] = cur[i];
+}
+
+// Fused tail of an iteration (SKC_LLOYD_FUSED=0 keeps the kernel-per-step sequence above).
+// objcheck: the objective's subtree sums combined level by level (pairwise_combine_kernel's
+// order), then the convergence check. One block.
+constexpr int kPwDeepL = 14;  // = kPwDeep of the pairwise sum
+__global__ void __launch_bounds__(1024) lloyd_objcheck_kernel(const double* __restrict__ gres,
+                                                              const uint8_t* __restrict__ gld, int D,
+                                                              const int64_t* __restrict__ out,
+                                                              double* __restrict__ obj, double* __restrict__ traj,
+                                                              int32_t* __restrict__ state, int max_iter, int first,
+                                                              cudaGraphConditionalHandle cond) {
+  extern __shared__ double lres[];
+  uint8_t* ld = reinterpret_cast<uint8_t*>(lres + (1 << D));
+  for (int t = threadIdx.x; t < (1 << D); t += blockDim.x) lres[t] = gres[t], ld[t] = gld[t];
+  __syncthreads();
+  for (int d = D - 1; d >= 0; --d) {
+    const int sh = D - d;
+    for (int t = threadIdx.x; t < (1 << d); t += blockDim.x)
+      if (ld[t << sh] > d) lres[t << sh] = dadd(lres[(2 * t) << (sh - 1)], lres[(2 * t + 1) << (sh - 1)]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const int it = state[0] + 1;  // iterations executed, this assignment included
+    obj[0] = lres[0];
+    traj[it - 1] = lres[0];
+    const int conv = (!first && out[0] == 0) ? 1 : 0;
+    state[0] = it;
+    state[1] = conv;
+    cudaGraphSetConditional(cond, (!conv && it < max_iter) ? 1u : 0u);
+  }
+}
+
+// finish: centres, reseed and commit in one kernel (cluster.py:207-215, :238-241). Block (k, s)
+// takes column k's coordinates [p s / S, p (s + 1) / S). The cluster's size is sum_j counts[j][k] / m
+// (every point holds m coordinates), so only "empty or not" is needed: the sum is
+// zero. A non-empty cluster's centre is sums / counts where counts > 0, else the previous value
+// (left in place); an empty cluster takes the farthest point's column (zero elsewhere), the
+// same point for every empty cluster. Nothing is written once the iteration converged (the
+// update is speculative, the reference breaks before it); the labels become the previous labels.
+template <typename V>
+__global__ void __launch_bounds__(256) lloyd_finish_kernel(const int32_t* __restrict__ state,
+                                                           const double* __restrict__ sums,
+                                                           const int64_t* __restrict__ counts, int m, int p_pad, int K,
+                                                           int S, const int32_t* __restrict__ idx,
+                                                           const V* __restrict__ val, const int64_t* __restrict__ row,
+                                                           double* __restrict__ mu, const int32_t* __restrict__ cur,
+                                                           int32_t* __restrict__ prev, int64_t n) {
+  if (state[1]) return;
+  const int k = blockIdx.x % K, s = blockIdx.x / K;
+  __shared__ long long red[8];
+  long long c = 0;
+  for (int j = threadIdx.x; j < p_pad; j += blockDim.x) c += counts[(int64_t)j * K + k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  long long tot = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+  const int j0 = (int)((int64_t)p_pad * s / S), j1 = (int)((int64_t)p_pad * (s + 1) / S);
+  if (tot != 0) {
+    for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+      const int64_t e = (int64_t)j * K + k;
+      const int64_t cn = counts[e];
+      if (cn != 0) mu[e] = __ddiv_rn(sums[e], (double)cn);
+    }
+  } else {
+    const int64_t r = *row > 0 ? *row : 0;
+    const int32_t* ir = idx + r * m;
+    const V* vr = val + r * m;
+    for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+      double v = 0.0;
+      for (int t = 0; t < m; ++t)
+        if (__ldg(ir + t) == j) v = (double)__ldg(vr + t);
+      mu[(int64_t)j * K + k] = v;
+    }
+  }
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) prev[i] = cur[i];
 }
 
@@ -143,8 +223,30 @@ struct Args {
   int32_t* iters;
 };
 
+// side stream and fork / join events of one captured iteration (the fused tail runs the
+// objective branch beside the partial sums)
+struct Side {
+  cudaStream_t st = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  bool make() {
+    return cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess;
+  }
+  ~Side() {
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    if (st) cudaStreamDestroy(st);
+  }
+};
+
+static bool fused_on() {
+  const char* e = getenv("SKC_LLOYD_FUSED");
+  return !(e && e[0] == '0');
+}
+
 // one iteration's launches on stream s; returns SKC_OK or the first error
-int iteration(const Args& A, const Bufs& B, bool first, cudaGraphConditionalHandle cond, cudaStream_t s) {
+int iteration(const Args& A, const Bufs& B, bool first, cudaGraphConditionalHandle cond, cudaStream_t s, Side& sd) {
   int rc;
   const int32_t* prev = first ? nullptr : B.prev;
   if (!first && A.prep != nullptr)
@@ -154,6 +256,36 @@ int iteration(const Args& A, const Bufs& B, bool first, cudaGraphConditionalHand
     rc = skc_kmeans_assign(A.idx, A.val, A.vdt, A.n, A.m, A.mu, A.p_pad, A.K, prev, A.labels, B.d2min, B.out,
                            B.d2max, B.aws, B.aws_bytes, s);
   if (rc) return rc;
+  if (fused_on()) {
+    // assign -> { objective leaves -> combine + check } || { partial sums } -> finish
+    if (cudaEventRecord(sd.fork, s) != cudaSuccess || cudaStreamWaitEvent(sd.st, sd.fork, 0) != cudaSuccess)
+      return check_launch("lloyd fork");
+    if ((rc = skc_kmeans_partials_csc(A.csc, A.vdt, A.n, A.m, A.p_pad, A.labels, A.K, B.sums, B.counts, nullptr,
+                                      B.sws, B.sws_bytes, sd.st)))
+      return rc;
+    int D = 0;
+    if ((rc = pairwise_leaves_launch(B.d2min, A.n, B.pws, &D, s))) return rc;
+    const size_t osm = ((size_t)1 << D) * 9 + 16;
+    cudaFuncSetAttribute(lloyd_objcheck_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
+    lloyd_objcheck_kernel<<<1, 1024, osm, s>>>(reinterpret_cast<const double*>(B.pws),
+                                               reinterpret_cast<const uint8_t*>(B.pws) + ((size_t)8 << kPwDeepL), D,
+                                               B.out, B.obj, A.traj, B.state, A.max_iter, first ? 1 : 0, cond);
+    if ((rc = check_launch("lloyd_objcheck_kernel"))) return rc;
+    if (cudaEventRecord(sd.join, sd.st) != cudaSuccess || cudaStreamWaitEvent(s, sd.join, 0) != cudaSuccess)
+      return check_launch("lloyd join");
+    int S = (2 * sm_count() + A.K - 1) / A.K;
+    if (S < 1) S = 1;
+    if (S > A.p_pad) S = A.p_pad;
+    if (A.vdt == SKC_F64)
+      lloyd_finish_kernel<double><<<(unsigned)(A.K * S), 256, 0, s>>>(
+          B.state, B.sums, B.counts, A.m, A.p_pad, A.K, S, A.idx, static_cast<const double*>(A.val), B.out + 1, A.mu,
+          A.labels, B.prev, A.n);
+    else
+      lloyd_finish_kernel<float><<<(unsigned)(A.K * S), 256, 0, s>>>(
+          B.state, B.sums, B.counts, A.m, A.p_pad, A.K, S, A.idx, static_cast<const float*>(A.val), B.out + 1, A.mu,
+          A.labels, B.prev, A.n);
+    return check_launch("lloyd_finish_kernel");
+  }
   if ((rc = skc_pairwise_sum(B.d2min, A.n, B.obj, B.pws, B.pws_bytes, s))) return rc;
   lloyd_check_kernel<<<1, 1, 0, s>>>(B.out, B.obj, A.traj, B.state, A.max_iter, first ? 1 : 0, cond);
   if ((rc = check_launch("lloyd_check_kernel"))) return rc;
@@ -184,18 +316,20 @@ int build(const Args& A, const Bufs& B, Entry& E) {
   cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking);
   cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
   int rc = SKC_OK;
+  Side sd1, sd2;  // prologue / body
   auto done = [&](int code) {
     cudaStreamDestroy(s1);
     cudaStreamDestroy(s2);
     if (code != SKC_OK) cudaGraphDestroy(g);
     return code;
   };
+  if (!sd1.make() || !sd2.make()) return done(check_launch("lloyd side streams"));
   if (cudaStreamBeginCaptureToGraph(s1, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) != cudaSuccess)
     return done(check_launch("begin capture"));
   cudaMemcpyAsync(A.mu, A.mu0, sizeof(double) * A.p_pad * A.K, cudaMemcpyDeviceToDevice, s1);
   cudaMemsetAsync(B.state, 0, 2 * sizeof(int32_t), s1);
   const uint64_t l0 = skc_launch_count();
-  rc = iteration(A, B, true, cond, s1);
+  rc = iteration(A, B, true, cond, s1, sd1);
   const uint64_t l1 = skc_launch_count();
   cudaStreamCaptureStatus status;
   const cudaGraphNode_t* deps = nullptr;
@@ -223,7 +357,7 @@ int build(const Args& A, const Bufs& B, Entry& E) {
       rc = check_launch("begin body capture");
     } else {
       l2 = skc_launch_count();
-      rc = iteration(A, B, false, cond, s2);
+      rc = iteration(A, B, false, cond, s2, sd2);
       l3 = skc_launch_count();
       cudaGraph_t bo = nullptr;
       if (cudaStreamEndCapture(s2, &bo) != cudaSuccess && rc == SKC_OK) rc = check_launch("end body capture");
@@ -314,7 +448,7 @@ int skc_kmeans_lloyd(const int32_t* idx, const void* val, int32_t val_dtype, int
                 [] {
                   int d = 0;
                   cudaGetDevice(&d);
-                  return d;
+                  return 2 * d + (fused_on() ? 1 : 0);  // SKC_LLOYD_FUSED is read per call (tests compare both)
                 }()};
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_cache.find(key);
