@@ -124,7 +124,9 @@ def test_tc_filter_equals_exact(skc, monkeypatch, p, m, K, n, spread, compute, i
 
 
 @pytest.mark.parametrize("p,m,K,n", [(2048, 102, 100, 30000), (1024, 51, 7, 20001), (512, 26, 10, 90000),
-                                     (256, 25, 256, 50000)])
+                                     (256, 25, 256, 50000), (256, 30, 32, 40000), (128, 3, 1, 5000),
+                                     (256, 25, 2, 70001), (256, 25, 20, 30000), (128, 16, 13, 33333),
+                                     (128, 9, 5, 100000)])
 def test_partials_paths_agree(skc, monkeypatch, p, m, K, n):
     """K6's exact paths (tiled counting sort, warp-per-coordinate walk, segmented label sort) agree bit for bit."""
     rng = np.random.default_rng(p * 7 + K)
