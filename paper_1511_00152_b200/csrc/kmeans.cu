@@ -595,7 +595,32 @@ static size_t coop_smem(int32_t p_pad, int KC, int m) {
 #define SKC_REG_WARPS 8
 #endif
 constexpr int kRegWarps = SKC_REG_WARPS;
-template <typename V, int H, int MT>
+// H (pairs of centres per point) as a sum of powers of two, widest first: component c has width
+// w(c) and starts at pair o(c) (the spread table layout of K5r)
+template <int H>
+struct RegDecomp {
+  static constexpr int n = ((H >> 3) & 1) + ((H >> 2) & 1) + ((H >> 1) & 1) + (H & 1);
+  static constexpr int w(int c) {
+    int seen = 0;
+    for (int b = 8; b >= 1; b >>= 1)
+      if (H & b) {
+        if (seen == c) return b;
+        ++seen;
+      }
+    return 1;
+  }
+  static constexpr int o(int c) {
+    int sum = 0;
+    for (int i = 0; i < c; ++i) sum += w(i);
+    return sum;
+  }
+  static constexpr int comp(int h) {
+    int c = 0;
+    while (c + 1 < n && h >= o(c + 1)) ++c;
+    return c;
+  }
+};
+template <typename V, int H, int MT, bool SPREAD>
 __global__ void __launch_bounds__(kRegWarps * 32, 1) km_assign_reg_kernel(
     const int32_t* __restrict__ idx, const void* __restrict__ val, int64_t n, int m, const double* __restrict__ mu,
     int K, int p_pad, const int32_t* __restrict__ prev, int32_t* __restrict__ labels, double* __restrict__ d2min,
@@ -606,19 +631,55 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) km_assign_reg_kernel(
   constexpr int PF = (NE + 31) / 32;        // per lane
   constexpr bool kPrefetch = PF <= 8;       // next step's rows in registers during this step's chains
   extern __shared__ __align__(16) unsigned char csm[];
-  double2* tab = reinterpret_cast<double2*>(csm);  // [p_pad + 1][H]: (mu[j][2h], mu[j][2h+1])
+  // Table layouts. Compact: [p_pad + 1][H] pairs (mu[j][2h], mu[j][2h+1]); the 16 H-byte rows of
+  // the two or three points inside a quarter-warp overlap banks (~7.5 wavefronts per 16-byte read
+  // at H = 5). Spread (when it fits): H splits into its powers of two, widest first; component c
+  // (width w, first pair o) has its own table of 128-byte rows holding 8 / w replicas of the
+  // row's w pairs, its lanes form one region (point g at lanes G o + g w ...), and a lane reads
+  // the replica that puts it at bank 4 (lane mod 8): every quarter-warp covers the 32 banks
+  // once, whatever rows its points read (4 wavefronts per read).
+  using RD = RegDecomp<H>;
+  constexpr int NC = SPREAD ? RD::n : 1;
+  constexpr int kRowBytes = SPREAD ? 128 : 16 * H;
+  const size_t tab_bytes = (size_t)NC * (p_pad + 1) * kRowBytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* sval = reinterpret_cast<double*>(tab + (size_t)(p_pad + 1) * H) + (size_t)warp * G * RS;
-  int* sidx = reinterpret_cast<int*>(reinterpret_cast<double*>(tab + (size_t)(p_pad + 1) * H) + (size_t)kRegWarps * G * RS) +
+  double* sval = reinterpret_cast<double*>(csm + tab_bytes) + (size_t)warp * G * RS;
+  int* sidx = reinterpret_cast<int*>(reinterpret_cast<double*>(csm + tab_bytes) + (size_t)kRegWarps * G * RS) +
               (size_t)warp * G * RS;
-  for (int e = threadIdx.x; e < (p_pad + 1) * H; e += blockDim.x) {
-    const int j = e / H, c = 2 * (e - j * H);
-    const double* r = mu + (size_t)j * K;
-    const bool row = j < p_pad;
-    tab[e] = make_double2(row && c < K ? __ldg(r + c) : 0.0, row && c + 1 < K ? __ldg(r + c + 1) : 0.0);
+  if constexpr (SPREAD) {
+    double2* tab = reinterpret_cast<double2*>(csm);
+    for (int e = threadIdx.x; e < NC * (p_pad + 1) * 8; e += blockDim.x) {
+      const int q = e & 7, j = (e >> 3) % (p_pad + 1), c = (e >> 3) / (p_pad + 1);
+      const int hh = RD::o(c) + q % RD::w(c), c2 = 2 * hh;
+      const double* r = mu + (size_t)j * K;
+      const bool row = j < p_pad;
+      tab[e] = make_double2(row && c2 < K ? __ldg(r + c2) : 0.0, row && c2 + 1 < K ? __ldg(r + c2 + 1) : 0.0);
+    }
+  } else {
+    double2* tab = reinterpret_cast<double2*>(csm);
+    for (int e = threadIdx.x; e < (p_pad + 1) * H; e += blockDim.x) {
+      const int j = e / H, c = 2 * (e - j * H);
+      const double* r = mu + (size_t)j * K;
+      const bool row = j < p_pad;
+      tab[e] = make_double2(row && c < K ? __ldg(r + c) : 0.0, row && c + 1 < K ? __ldg(r + c + 1) : 0.0);
+    }
   }
   __syncthreads();
-  const int g = lane / H, h = lane - g * H;
+  // lane -> (point slot g, pair h) and the lane's byte offset inside a table row
+  int g = lane / H, h = lane - g * H;
+  const unsigned char* tlane = csm + 16 * h;
+  if constexpr (SPREAD) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int lo = G * RD::o(c), hi = lo + G * RD::w(c);
+      if (lane >= lo && lane < hi) {
+        const int r = lane - lo;
+        g = r / RD::w(c);
+        h = RD::o(c) + r % RD::w(c);
+        tlane = csm + (size_t)c * (p_pad + 1) * 128 + 16 * (lane & 7);
+      }
+    }
+  }
   const V* const vals = reinterpret_cast<const V*>(val);
   int64_t changed = 0;
   double bmax = -1.0;
@@ -664,7 +725,7 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) km_assign_reg_kernel(
       if (t < 8) r8[t] = dmul(v, v);  // slots >= m8 are not used below
       else if (t < m8) r8[t & 7] = dadd(r8[t & 7], dmul(v, v));
       const double v2 = dmul(-2.0, v);
-      const double2 u = tab[ri[t] * H + h];
+      const double2 u = *reinterpret_cast<const double2*>(tlane + (size_t)ri[t] * kRowBytes);
       m0[t] = u.x;
       m1[t] = u.y;
       a0 = dadd(a0, dmul(v2, u.x));
@@ -683,7 +744,7 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) km_assign_reg_kernel(
     int bk = 0;
 #pragma unroll
     for (int q = 0; q < H; ++q) {
-      const int src = (g * H + q) & 31;
+      const int src = (SPREAD ? G * RD::o(RD::comp(q)) + g * RD::w(RD::comp(q)) + q - RD::o(RD::comp(q)) : g * H + q) & 31;
       const double x = __shfl_sync(kFM, d0, src), y = __shfl_sync(kFM, d1, src);
       if (q == 0) best = x;
       else if (2 * q < K && x < best) best = x, bk = 2 * q;
@@ -723,9 +784,11 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) km_assign_reg_kernel(
   }
 }
 static int reg_mt(int m) { return m <= 8 ? 8 : m <= 16 ? 16 : m <= 24 ? 24 : m <= 28 ? 28 : 32; }
-static size_t reg_smem(int32_t p_pad, int KC, int m) {
+static size_t reg_smem(int32_t p_pad, int KC, int m, bool spread) {
   const int H = KC / 2, G = 32 / H;
-  return (size_t)(p_pad + 1) * KC * 8 + (size_t)kRegWarps * G * (reg_mt(m) | 1) * 12;
+  const int nc = ((H >> 3) & 1) + ((H >> 2) & 1) + ((H >> 1) & 1) + (H & 1);
+  const size_t tab = spread ? (size_t)nc * (p_pad + 1) * 128 : (size_t)(p_pad + 1) * KC * 8;
+  return tab + (size_t)kRegWarps * G * (reg_mt(m) | 1) * 12;
 }
 
 __global__ void km_assign_reduce_kernel(const int64_t* __restrict__ blk_changed, const double* __restrict__ blk_max,
@@ -1094,7 +1157,11 @@ int assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, i
     // K5r when m fits the register copy of the row's centres (SKC_ASSIGN_REG=0: K5c / K5s)
     const char* reg_env = getenv("SKC_ASSIGN_REG");  // read per call: tests compare the kernels
     const bool reg_on = !(reg_env && reg_env[0] == '0');
-    const size_t rsm = reg_smem(p_pad, KC, m);
+    // the spread (conflict-free) table when it fits beside the staging (SKC_ASSIGN_SPREAD=0: compact)
+    const char* spr_env = getenv("SKC_ASSIGN_SPREAD");
+    const bool spread = !(spr_env && spr_env[0] == '0') && reg_smem(p_pad, KC, m, true) <= 200 * 1024 &&
+                        KC / 2 != 8;  // H = 8: a quarter-warp reads one 128-byte row as it is
+    const size_t rsm = reg_smem(p_pad, KC, m, spread);
     if (reg_on && m <= 32 && rsm <= 200 * 1024) {
       const int H = KC / 2, Gp = 32 / H;
       int64_t Gc = (n + (int64_t)kRegWarps * Gp - 1) / ((int64_t)kRegWarps * Gp);
@@ -1108,8 +1175,13 @@ int assign_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, i
                                                          reinterpret_cast<int64_t*>(bch + 2 * G));
       };
 #define SKC_REG_MT(HH, MM)                                                        \
-  if (val_f64) gor(km_assign_reg_kernel<double, HH, MM>);                         \
-  else gor(km_assign_reg_kernel<float, HH, MM>);
+  if (spread) {                                                                   \
+    if (val_f64) gor(km_assign_reg_kernel<double, HH, MM, true>);                 \
+    else gor(km_assign_reg_kernel<float, HH, MM, true>);                          \
+  } else {                                                                        \
+    if (val_f64) gor(km_assign_reg_kernel<double, HH, MM, false>);                \
+    else gor(km_assign_reg_kernel<float, HH, MM, false>);                         \
+  }
 #define SKC_REG_CASE(HH)                                                          \
   case HH:                                                                        \
     switch (reg_mt(m)) {                                                          \

@@ -114,7 +114,10 @@ def test_k5c_equals_k5s(skc, monkeypatch, p, m, K, n, spread, compute):
     (128, 12, 13, 777, 1.0, "f64"),     # H = 7
     (256, 16, 16, 6000, 1.0, "f64"),    # H = 8 (largest K of the small path), m = MT = 16
     (256, 20, 11, 2500, 1.0, "f64"),    # H = 6
-    (2048, 30, 9, 3000, 1.0, "f64"),    # a table above 100 KB
+    (2048, 30, 9, 3000, 1.0, "f64"),    # a table above 100 KB (compact layout only)
+    (256, 9, 14, 2222, 1.0, "f64"),     # H = 7: three components (4 + 2 + 1)
+    (128, 5, 3, 1500, 1.0, "f32"),      # H = 2
+    (256, 28, 8, 3333, 0.7, "f64"),     # H = 4, m = MT = 28
 ])
 def test_k5r_equals_k5s(skc, monkeypatch, p, m, K, n, spread, compute):
     """K5r (mu in registers between the two halves of the chain, one table pass, products formed
@@ -135,11 +138,13 @@ def test_k5r_equals_k5s(skc, monkeypatch, p, m, K, n, spread, compute):
     mu_h[2::11] *= 1e-160  # products and squares in the subnormal range
     mu = torch.as_tensor(mu_h, device=dev)
     prev = torch.as_tensor(rng.integers(0, K, n).astype(np.int32), device=dev)
-    a = _assign(skc, sk, mu, prev, False, monkeypatch, reg=True)
     b = _assign(skc, sk, mu, prev, False, monkeypatch)
-    assert np.array_equal(a[0], b[0]), "labels"
-    assert np.array_equal(a[1], b[1]), "d2min"
-    assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3]), "changed / farthest point"
+    for spread in ("1", "0"):  # the replicated conflict-free table (when it fits), and the compact one
+        monkeypatch.setenv("SKC_ASSIGN_SPREAD", spread)
+        a = _assign(skc, sk, mu, prev, False, monkeypatch, reg=True)
+        assert np.array_equal(a[0], b[0]), "labels"
+        assert np.array_equal(a[1], b[1]), "d2min"
+        assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3]), "changed / farthest point"
 
 
 @pytest.mark.parametrize("p,m,K,n,spread", [(512, 26, 10, 20000, 2.0), (256, 20, 12, 3000, 0.3), (2048, 40, 30, 4000, 1.0)])
