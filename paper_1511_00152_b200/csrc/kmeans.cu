@@ -1408,7 +1408,17 @@ int partials_check(int32_t p_pad, int32_t K) {
 // Lanes with equal labels (match_any) are folded by their lowest lane, in lane order
 // (= point order), into warp-private acc[k]. Every (j, k) sum is the reference's chain,
 // bit for bit, and the counts come with it.
-constexpr int kCscRange = 2048;
+constexpr int kCscRange = 2048;  // points per warp range, at most
+// Points per range: as small as keeps the [p_pad][R] offset table at <= 8M cells (64 MB), between
+// 64 and kCscRange. A warp walks its range point by point, so the range count is the transpose's
+// parallelism: C2 (200K points, p = 512) gets 3125 ranges of 64 instead of 98 of 2048; C5 (10M
+// points, p = 2048) stays at 2048 (its scatter is bound by the scattered 4- and 8-byte stores).
+static int csc_range(int64_t n, int32_t p_pad) {
+  if (const char* e = getenv("SKC_CSC_RANGE")) return atoi(e) > 0 ? atoi(e) : kCscRange;  // A/B runs
+  int64_t r = (n * (int64_t)p_pad + (8 << 20) - 1) / (8 << 20);
+  r = (r + 63) / 64 * 64;
+  return (int)(r < 64 ? 64 : r > kCscRange ? kCscRange : r);
+}
 
 struct CscLayout {
   int64_t R, nnz;
@@ -1419,7 +1429,8 @@ struct CscLayout {
 
 static CscLayout csc_layout(int64_t n, int32_t m, int32_t p_pad, int val_f64) {
   CscLayout L{};
-  L.R = (n + kCscRange - 1) / kCscRange;
+  const int range = csc_range(n, p_pad);
+  L.R = (n + range - 1) / range;
   if (L.R < 1) L.R = 1;
   L.nnz = n * (int64_t)m;
   const int64_t cells = (int64_t)p_pad * L.R + 1;
@@ -1470,7 +1481,7 @@ static SegLayout seg_layout(int64_t n, int32_t m, int32_t p_pad, int32_t K, int 
 
 // counts of range r at coordinate j -> off[j * R + r] (int64, scanned in place afterwards)
 __global__ void km_csc_count_kernel(const int32_t* __restrict__ idx, int64_t n, int m, int32_t p_pad, int64_t R,
-                                    int64_t* __restrict__ off) {
+                                    int range, int64_t* __restrict__ off) {
   extern __shared__ int ccnt[];  // [warps][p_pad]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   int* c = ccnt + (size_t)warp * p_pad;
@@ -1478,8 +1489,8 @@ __global__ void km_csc_count_kernel(const int32_t* __restrict__ idx, int64_t n, 
   for (int j = lane; j < p_pad; j += 32) c[j] = 0;
   __syncwarp();
   if (r < R) {
-    const int64_t i1 = min(n, (r + 1) * (int64_t)kCscRange);
-    for (int64_t i = r * (int64_t)kCscRange; i < i1; ++i)
+    const int64_t i1 = min(n, (r + 1) * (int64_t)range);
+    for (int64_t i = r * (int64_t)range; i < i1; ++i)
       for (int t = lane; t < m; t += 32) atomicAdd(&c[__ldg(idx + i * m + t)], 1);
     __syncwarp();
     for (int j = lane; j < p_pad; j += 32) off[(int64_t)j * R + r] = c[j];
@@ -1489,7 +1500,7 @@ __global__ void km_csc_count_kernel(const int32_t* __restrict__ idx, int64_t n, 
 // stable scatter: range r's entries of coordinate j go to off[j * R + r] ... in point order
 template <typename V>
 __global__ void km_csc_scatter_kernel(const int32_t* __restrict__ idx, const V* __restrict__ val, int64_t n, int m,
-                                      int32_t p_pad, int64_t R, const int64_t* __restrict__ off,
+                                      int32_t p_pad, int64_t R, int range, const int64_t* __restrict__ off,
                                       int32_t* __restrict__ rows, V* __restrict__ vals) {
   extern __shared__ int64_t cpos[];  // [warps][p_pad]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -1498,8 +1509,8 @@ __global__ void km_csc_scatter_kernel(const int32_t* __restrict__ idx, const V* 
   if (r >= R) return;
   for (int j = lane; j < p_pad; j += 32) q[j] = off[(int64_t)j * R + r];
   __syncwarp();
-  const int64_t i1 = min(n, (r + 1) * (int64_t)kCscRange);
-  for (int64_t i = r * (int64_t)kCscRange; i < i1; ++i) {
+  const int64_t i1 = min(n, (r + 1) * (int64_t)range);
+  for (int64_t i = r * (int64_t)range; i < i1; ++i) {
     for (int t = lane; t < m; t += 32) {
       const int j = __ldg(idx + i * m + t);
       const int64_t pos = q[j]++;
@@ -1889,7 +1900,8 @@ int csc_build_launch(const int32_t* idx, const void* val, int val_f64, int64_t n
     const int wc = csc_warps_for(p_pad, 4);
     const size_t smc = (size_t)wc * p_pad * 4;
     cudaFuncSetAttribute(km_csc_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
-    km_csc_count_kernel<<<(unsigned)((L.R + wc - 1) / wc), wc * 32, smc, st>>>(idx, n, m, p_pad, L.R, off);
+    km_csc_count_kernel<<<(unsigned)((L.R + wc - 1) / wc), wc * 32, smc, st>>>(idx, n, m, p_pad, L.R,
+                                                                                csc_range(n, p_pad), off);
     if ((rc = check_launch("km_csc_count_kernel"))) return rc;
   }
   size_t tb = L.temp_bytes;
@@ -1901,12 +1913,14 @@ int csc_build_launch(const int32_t* idx, const void* val, int val_f64, int64_t n
     const unsigned grid = (unsigned)((L.R + ws_ - 1) / ws_);
     if (val_f64) {
       cudaFuncSetAttribute(km_csc_scatter_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms);
-      km_csc_scatter_kernel<double><<<grid, ws_ * 32, sms, st>>>(idx, (const double*)val, n, m, p_pad, L.R, off,
+      km_csc_scatter_kernel<double><<<grid, ws_ * 32, sms, st>>>(idx, (const double*)val, n, m, p_pad, L.R,
+                                                                  csc_range(n, p_pad), off,
                                                                   reinterpret_cast<int32_t*>(w + L.off_rows),
                                                                   reinterpret_cast<double*>(w + L.off_vals));
     } else {
       cudaFuncSetAttribute(km_csc_scatter_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms);
-      km_csc_scatter_kernel<float><<<grid, ws_ * 32, sms, st>>>(idx, (const float*)val, n, m, p_pad, L.R, off,
+      km_csc_scatter_kernel<float><<<grid, ws_ * 32, sms, st>>>(idx, (const float*)val, n, m, p_pad, L.R,
+                                                                csc_range(n, p_pad), off,
                                                                 reinterpret_cast<int32_t*>(w + L.off_rows),
                                                                 reinterpret_cast<float*>(w + L.off_vals));
     }
