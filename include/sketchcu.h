@@ -187,7 +187,9 @@ size_t skc_kmeans_csc_workspace(int64_t n, int32_t m, int32_t p_pad, int32_t val
 int skc_kmeans_build_csc(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m, int32_t p_pad,
                          void *csc, size_t csc_bytes, void *stream);
 /* seg: skc_kmeans_seg_workspace bytes of per-iteration scratch (labels per entry, the
- * values in chain order, segment offsets). K <= 256. */
+ * values in chain order, segment offsets). K <= 256. sizes may be NULL when the caller does not
+ * need the cluster sizes (they follow from the counts: sum_j counts[j][k] = m * n_k, SPEC.md:297;
+ * skc_kmeans_lloyd's finish kernel uses that). */
 size_t skc_kmeans_seg_workspace(int64_t n, int32_t m, int32_t p_pad, int32_t K, int32_t val_dtype);
 int skc_kmeans_partials_csc(const void *csc, int32_t val_dtype, int64_t n, int32_t m, int32_t p_pad,
                             const int32_t *labels, int32_t K, double *sums, int64_t *counts, int64_t *sizes, void *seg,
@@ -202,8 +204,11 @@ int skc_kmeans_reseed_at(const int32_t *idx, const void *val, int32_t val_dtype,
 /* The whole Lloyd loop of _lloyd_iterate (cluster.py:230-241) from centres mu0, device-resident:
  * ONE CUDA graph with a conditional WHILE node runs the iterations (assign, numpy-order objective,
  * convergence test on the device, partial sums through csc, centres, reseed) with no host round
- * trip; it is built once per argument set and relaunched. The kernels are those of the
- * host-driven loop, so labels, mu and the objective trajectory are bit-identical to it.
+ * trip; it is built once per argument set and relaunched. The assignment, objective-leaf and
+ * partial-sum kernels are those of the host-driven loop; the objective's combine + check and the
+ * centres + reseed + commit step are each one kernel (the latter takes "cluster empty" from the
+ * counts), with the same arithmetic, so labels, mu and the objective trajectory are bit-identical
+ * to the host-driven loop.
  * csc: from skc_kmeans_build_csc (required). tc_prep: from skc_kmeans_tc_prepare, or NULL (then
  * every assignment uses skc_kmeans_assign; otherwise iterations 2.. use the tensor-core filter).
  * ws: skc_kmeans_lloyd_workspace bytes. Outputs (device, =): labels (n) int32 of the last
