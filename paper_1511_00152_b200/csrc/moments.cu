@@ -5,6 +5,10 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "common.cuh"
 
 namespace skc {
@@ -183,6 +187,8 @@ int moments_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, 
 // point and independent of order (deterministic). At the end the CTA adds its low words
 // into the same int64 partial. A reduce kernel sums the groups in int64 and scales to fp64.
 // tau = 8 * rms(values), from K2's statistics. Quantum 2^-S ~ 6e-8 * tau^2.
+// Band boundaries of the flat kernel adapt to measured per-band time (band_plan below); the
+// sums do not depend on them.
 // Two kernels share this scheme: cov_flat_kernel (m <= 64, the default; lean per-visit work and
 // a packed pair table) and cov_band_kernel (m > 64, or SKC_COV_KERNEL=band). Both are bound by
 // the shared-memory pipe: an ATOMS wavefront costs about two load wavefronts, and random 32-lane
@@ -263,6 +269,7 @@ struct CovParams {
   unsigned long long* part;  // [groups][tri_total] int64 fixed-point partials
   int nbands, groups;
   int aligned;               // idx/val 16-byte aligned: tiles may use bulk copies
+  unsigned long long* cyc;   // [groups][nbands] elapsed cycles per band CTA (flat kernel; may be null)
   int band_rows[kMaxBands + 1];
 };
 
@@ -504,6 +511,7 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __gri
   unsigned long long* part = P.part + (size_t)group * tri_off(P.p_pad, P.p_pad) + e0;
   const uint32_t lo_sh = (uint32_t)__cvta_generic_to_shared(lo);
 
+  const long long tc0 = clock64();  // per-band time for the adaptive band plan (band_plan)
   double tau;
   const int S_ = cov_scale(P.stats, m, &tau);
   const bool wide = cov_wide(S_);
@@ -620,6 +628,7 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __gri
     __syncwarp();
   }
   __syncthreads();
+  if (threadIdx.x == 0 && P.cyc != nullptr) P.cyc[blockIdx.x] = (unsigned long long)(clock64() - tc0);
   for (int e = threadIdx.x; e < ne; e += blockDim.x) {
     const long long q = (long long)lo[e] - (long long)kBias;
     if (q != 0) atomicAdd(part + e, (unsigned long long)q);
@@ -756,6 +765,103 @@ static int tc_min_m(int32_t p_pad) {
   return l < 8 ? 1 << 30 : t[l > 13 ? 5 : l - 8];
 }
 
+// Band count of the banded path. The flat kernel takes one band more than the capacity needs
+// when the entry-balanced bands would sit within 5% of it: the adaptive plan below then has room
+// to move boundaries (SKC_COV_ADAPT=0: the minimum count, entry-balanced, no adaptation).
+static bool cov_adapt_on() {
+  const char* e = getenv("SKC_COV_ADAPT");
+  return !(e && e[0] == '0');
+}
+static int band_count(int32_t p_pad, int32_t m) {
+  const int cap = band_capacity(m, p_pad);
+  int nb = make_bands(p_pad, cap, nullptr);
+  if (band_kind(m) == 'f' && cov_adapt_on() && nb >= 4 && nb < kMaxBands &&
+      (double)nb * cap < 1.05 * (double)tri_off(p_pad, p_pad))
+    ++nb;
+  return nb;
+}
+// nb bands balanced by entries (the starting plan); nb is at least the capacity's minimum count
+static void bands_by_entries(int32_t p_pad, int nb, int cap, int* out) {
+  const int64_t total = tri_off(p_pad, p_pad);
+  int64_t t = (total + nb - 1) / nb;
+  while (t < cap && greedy_bands(p_pad, t, nullptr) > nb) t += (t >> 8) + 1;
+  if (t > cap) t = cap;
+  int tmp[kMaxBands + 1];
+  const int got = greedy_bands(p_pad, t, tmp);
+  for (int b = 0; b <= nb; ++b) out[b] = b <= got ? tmp[b] : p_pad;  // fewer bands than asked (tiny p): empty tail
+}
+
+// Adaptive band plan (flat kernel). Equal entries are equal expected pairs, but a band CTA also
+// pays per in-band element of a row, so bands of many short rows run slower (3.9% between the
+// fastest and slowest of C3's ten bands). The slowest band sets the kernel time, and bands of a
+// group that drift apart re-read its rows from DRAM once their distance exceeds what L2 holds.
+// Every flat-kernel CTA records its elapsed cycles; the next launch of the same shape moves the
+// band boundaries so that the measured time per band evens out (time taken as uniform per entry
+// inside a band), a few times, then keeps the plan. Results do not depend on the boundaries (the
+// fixed-point sums are exact), only the time and the DRAM traffic do.
+struct BandPlan {
+  int nb = 0, updates = 0, groups = 0;
+  int rows[kMaxBands + 1];
+  int best_rows[kMaxBands + 1];  // the measured plan with the fastest slowest band
+  double best_max = 0.0;         // its slowest band, cycles per row of the launch
+  int64_t n_meas = 1;            // rows of the measured launch
+  unsigned long long* h_cyc = nullptr;  // pinned
+  cudaEvent_t ev = nullptr;
+  bool pending = false;
+};
+constexpr int kPlanUpdates = 2;  // proposals; every one is measured, the best measured plan stays (at C3 the
+                                 // second is the best: later ones, and damped steps, measured worse)
+constexpr int kPlanMaxCtas = 1024;
+static std::mutex g_plan_mu;
+static std::map<std::tuple<int, int, int, int>, BandPlan> g_plans;
+
+static void plan_update(BandPlan& B, int32_t p_pad, int cap) {
+  // mean cycles per band over the groups of the measured launch
+  double T[kMaxBands], tot = 0.0, mx = 0.0;
+  for (int b = 0; b < B.nb; ++b) {
+    double sum = 0.0;
+    for (int g = 0; g < B.groups; ++g) sum += (double)B.h_cyc[(size_t)g * B.nb + b];
+    T[b] = sum / B.groups;
+    if (!(T[b] > 0.0)) return;  // no measurement
+    tot += T[b];
+    if (T[b] > mx) mx = T[b];
+  }
+  mx /= (double)B.n_meas;
+  if (B.best_max == 0.0 || mx < B.best_max) {
+    B.best_max = mx;
+    for (int b = 0; b <= B.nb; ++b) B.best_rows[b] = B.rows[b];
+  }
+  if (B.updates >= kPlanUpdates) {  // the last proposal has been measured: keep the best plan
+    for (int b = 0; b <= B.nb; ++b) B.rows[b] = B.best_rows[b];
+    return;
+  }
+  const double target = tot / B.nb;
+  int out[kMaxBands + 1];
+  int nbo = 0, a = 0, src = 0;
+  out[0] = 0;
+  while (a < p_pad && nbo < B.nb) {
+    double w = 0.0;
+    int64_t e = 0;
+    int r = a;
+    const bool last = nbo == B.nb - 1;
+    while (r < p_pad) {
+      while (src + 1 < B.nb && r >= B.rows[src + 1]) ++src;
+      const double eb = (double)(tri_off(B.rows[src + 1], p_pad) - tri_off(B.rows[src], p_pad));
+      const double wr = T[src] / eb * (double)(p_pad - r);
+      if (e + (p_pad - r) > cap) break;
+      if (!last && w + 0.5 * wr > target) break;
+      w += wr;
+      e += p_pad - r;
+      ++r;
+    }
+    if (r == a) ++r;
+    out[++nbo] = r;
+    a = r;
+  }
+  if (a < p_pad || nbo != B.nb) return;  // the capacity could not take the remainder: keep the plan
+  for (int b = 0; b <= B.nb; ++b) B.rows[b] = out[b];
+}
+
 // 'b' banded scatter (K3), 'g' global L2 scatter (K3g), 't' tensor cores (K3t).
 // SKC_COV_PATH=b|g|t forces a path where it applies.
 constexpr int64_t kCovSmallRows = (int64_t)1 << 18;  // below: the band partials' reduce dominates (C1: 0.29 vs 0.05 ms)
@@ -770,7 +876,7 @@ static char cov_path(int32_t m, int32_t p_pad, int64_t n) {
   if (tc && (m >= tc_min_m(p_pad) || cap < p_pad)) return 't';
   if (cap < p_pad) return 'g';
   if (n < kCovSmallRows && (size_t)kCovGWarps * 2 * m * sizeof(int2) <= 200 * 1024) return 'g';
-  return make_bands(p_pad, cap, nullptr) > kCovGlobalBands ? 'g' : 'b';
+  return band_count(p_pad, m) > kCovGlobalBands ? 'g' : 'b';
 }
 
 int cov_check(int32_t p_pad, int32_t m) {
@@ -779,8 +885,7 @@ int cov_check(int32_t p_pad, int32_t m) {
   if (path == 'g') return (size_t)kCovGWarps * 2 * m * sizeof(int2) <= 200 * 1024
                               ? SKC_OK
                               : fail(SKC_EPARAM, "m too large for the covariance kernels");
-  if (make_bands(p_pad, band_capacity(m, p_pad), nullptr) > kMaxBands)
-    return fail(SKC_EPARAM, "too many covariance bands for p_pad");
+  if (band_count(p_pad, m) > kMaxBands) return fail(SKC_EPARAM, "too many covariance bands for p_pad");
   return SKC_OK;
 }
 
@@ -788,17 +893,52 @@ size_t cov_ws(int64_t n, int32_t m, int32_t p_pad) {
   const char path = cov_path(m, p_pad, n);
   if (path == 't') return covtc_ws(n, m, p_pad);
   if (path == 'g') return (size_t)tri_off(p_pad, p_pad) * sizeof(unsigned long long);
-  const int nb = make_bands(p_pad, band_capacity(m, p_pad), nullptr);
+  const int nb = band_count(p_pad, m);
   const int g = cov_groups(nb, n);
-  return (size_t)g * tri_off(p_pad, p_pad) * sizeof(unsigned long long);
+  return (size_t)g * tri_off(p_pad, p_pad) * sizeof(unsigned long long) + (size_t)kPlanMaxCtas * 8;
 }
 
 static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, int32_t p_pad,
                            const double* stats, double* tri, void* ws, cudaStream_t st) {
   CovParams H;
   const int cap = band_capacity(m, p_pad);
-  H.nbands = make_bands(p_pad, cap, H.band_rows);
+  const bool flat = band_kind(m) == 'f';
+  H.nbands = band_count(p_pad, m);
   H.groups = cov_groups(H.nbands, n);
+  H.cyc = nullptr;
+  bool measure = false;
+  BandPlan* plan = nullptr;
+  if (flat && cov_adapt_on() && H.nbands * H.groups <= kPlanMaxCtas) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    BandPlan& B = g_plans[std::make_tuple(dev, (int)p_pad, (int)m, val_f64)];
+    if (B.nb != H.nbands) {  // first use (or the count changed with the environment)
+      B.nb = H.nbands;
+      B.updates = 0;
+      B.best_max = 0.0;
+      B.pending = false;
+      bands_by_entries(p_pad, B.nb, cap, B.rows);
+      if (B.h_cyc == nullptr && cudaMallocHost(&B.h_cyc, (size_t)kPlanMaxCtas * 8) != cudaSuccess) B.h_cyc = nullptr;
+      if (B.ev == nullptr && cudaEventCreateWithFlags(&B.ev, cudaEventDisableTiming) != cudaSuccess) B.ev = nullptr;
+      cudaGetLastError();
+    }
+    if (B.pending && cudaEventQuery(B.ev) == cudaSuccess) {
+      B.pending = false;
+      plan_update(B, p_pad, cap);
+      ++B.updates;
+    }
+    cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not an error
+    for (int b = 0; b <= B.nb; ++b) H.band_rows[b] = B.rows[b];
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    measure = B.h_cyc && B.ev && !B.pending && B.updates <= kPlanUpdates && cs == cudaStreamCaptureStatusNone &&
+              n >= ((int64_t)1 << 20);  // short launches measure start-up, not the bands
+    plan = &B;
+  } else {
+    H.nbands = make_bands(p_pad, cap, H.band_rows);
+    H.groups = cov_groups(H.nbands, n);
+  }
   H.idx = idx;
   H.val = val;
   H.n = n;
@@ -807,6 +947,7 @@ static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int
   H.stats = stats;
   H.tri = tri;
   H.part = reinterpret_cast<unsigned long long*>(ws);
+  if (measure) H.cyc = H.part + (size_t)H.groups * tri_off(p_pad, p_pad);
   H.aligned = (reinterpret_cast<uintptr_t>(idx) % 16 == 0) && (reinterpret_cast<uintptr_t>(val) % 16 == 0);
   const int64_t total = tri_off(p_pad, p_pad);
   cudaMemsetAsync(ws, 0, (size_t)H.groups * total * 8, st);
@@ -816,7 +957,6 @@ static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int
     if (e > maxe) maxe = e;
     if (H.band_rows[b + 1] - H.band_rows[b] > maxr) maxr = H.band_rows[b + 1] - H.band_rows[b];
   }
-  const bool flat = band_kind(m) == 'f';
   const size_t smem = flat ? (size_t)((maxe + 1) & ~1) * 4 + flat_ptab_bytes(m) + (size_t)kCovWarps * m * 8
                            : (size_t)((maxe + 1) & ~1) * 4 + (size_t)((maxr + 1) & ~1) * 4 + pair_table_bytes(m) +
                                  (size_t)kCovWarps * m * 16;
@@ -831,6 +971,15 @@ static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int
   k<<<H.nbands * H.groups, kCovWarps * 32, smem, st>>>(H);
   int rc = check_launch("cov_band_kernel");
   if (rc) return rc;
+  if (measure) {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    plan->groups = H.groups;
+    plan->n_meas = n;
+    if (cudaMemcpyAsync(plan->h_cyc, H.cyc, (size_t)H.nbands * H.groups * 8, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+        cudaEventRecord(plan->ev, st) == cudaSuccess)
+      plan->pending = true;
+    cudaGetLastError();
+  }
   cov_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(H.part, H.groups, total, m, stats, tri);
   return check_launch("cov_reduce_kernel");
 }
@@ -843,7 +992,7 @@ int cov_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int3
   if (path == 't') return covtc_launch(idx, val, val_f64, n, m, p_pad, stats, tri, ws, st);
   if (path == 'g') return cov_launch_global(idx, val, val_f64, n, m, p_pad, stats, tri, ws, st);
   // the kernel addresses a group's rows with 32-bit element offsets: split huge inputs
-  const int groups = cov_groups(make_bands(p_pad, band_capacity(m, p_pad), nullptr), n);
+  const int groups = cov_groups(band_count(p_pad, m), n);
   int64_t max_rows = (int64_t)groups * ((((int64_t)1 << 31) / m) - kCovWarps);
   if (const char* e = getenv("SKC_COV_SPLIT_ROWS")) max_rows = atoll(e) > 0 ? atoll(e) : max_rows;  // tests
   const size_t vsz = val_f64 ? 8 : 4;

@@ -11,7 +11,8 @@ timeout 1500 python bench.py > $out/${tag}_bench.json 2> $out/${tag}_bench.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > $out/${tag}_ref.json 2> $out/${tag}_ref.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/${tag}_c3_launches.csv \
   python bench.py --no-cpu --no-configs --no-secondary --no-e2e --no-python-ref --steps 2 --warmup 3 > $out/${tag}_ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'indices_kernel|gather_tma|cov_flat|cov_band|moments_kernel' -c 4 \
-  -o $out/${tag}_c3_full python bench.py --no-cpu --no-configs --no-secondary --no-e2e --no-python-ref --steps 1 --warmup 0 \
+# the fourth pass of the bench (after three warm-up passes: K3's adaptive band plan has settled)
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'indices_kernel|gather_tma|cov_flat|cov_band|moments_kernel' -s 12 -c 4 \
+  -o $out/${tag}_c3_full python bench.py --no-cpu --no-configs --no-secondary --no-e2e --no-python-ref --steps 1 --warmup 3 \
   > $out/${tag}_ncu_full.log 2>&1
 tail -c 300 $out/${tag}_bench.json
