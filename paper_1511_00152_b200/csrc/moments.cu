@@ -766,16 +766,18 @@ static int tc_min_m(int32_t p_pad) {
 }
 
 // Band count of the banded path. The flat kernel takes one band more than the capacity needs
-// when the entry-balanced bands would sit within 5% of it: the adaptive plan below then has room
-// to move boundaries (SKC_COV_ADAPT=0: the minimum count, entry-balanced, no adaptation).
+// when the entry-balanced bands would sit within 5% of it and the launch is long enough to be
+// measured: the adaptive plan below then has room to move boundaries (SKC_COV_ADAPT=0, or a launch
+// under 2^20 rows: the minimum count, entry-balanced, as before).
 static bool cov_adapt_on() {
   const char* e = getenv("SKC_COV_ADAPT");
   return !(e && e[0] == '0');
 }
-static int band_count(int32_t p_pad, int32_t m) {
+constexpr int64_t kPlanMinRows = (int64_t)1 << 20;  // shorter launches measure start-up, not the bands
+static int band_count(int32_t p_pad, int32_t m, int64_t n) {
   const int cap = band_capacity(m, p_pad);
   int nb = make_bands(p_pad, cap, nullptr);
-  if (band_kind(m) == 'f' && cov_adapt_on() && nb >= 4 && nb < kMaxBands &&
+  if (band_kind(m) == 'f' && cov_adapt_on() && n >= kPlanMinRows && nb >= 4 && nb < kMaxBands &&
       (double)nb * cap < 1.05 * (double)tri_off(p_pad, p_pad))
     ++nb;
   return nb;
@@ -813,7 +815,7 @@ constexpr int kPlanUpdates = 2;  // proposals; every one is measured, the best m
                                  // second is the best: later ones, and damped steps, measured worse)
 constexpr int kPlanMaxCtas = 1024;
 static std::mutex g_plan_mu;
-static std::map<std::tuple<int, int, int, int>, BandPlan> g_plans;
+static std::map<std::tuple<int, int, int, int, int>, BandPlan> g_plans;
 
 static void plan_update(BandPlan& B, int32_t p_pad, int cap) {
   // mean cycles per band over the groups of the measured launch
@@ -876,7 +878,7 @@ static char cov_path(int32_t m, int32_t p_pad, int64_t n) {
   if (tc && (m >= tc_min_m(p_pad) || cap < p_pad)) return 't';
   if (cap < p_pad) return 'g';
   if (n < kCovSmallRows && (size_t)kCovGWarps * 2 * m * sizeof(int2) <= 200 * 1024) return 'g';
-  return band_count(p_pad, m) > kCovGlobalBands ? 'g' : 'b';
+  return make_bands(p_pad, cap, nullptr) > kCovGlobalBands ? 'g' : 'b';
 }
 
 int cov_check(int32_t p_pad, int32_t m) {
@@ -885,7 +887,7 @@ int cov_check(int32_t p_pad, int32_t m) {
   if (path == 'g') return (size_t)kCovGWarps * 2 * m * sizeof(int2) <= 200 * 1024
                               ? SKC_OK
                               : fail(SKC_EPARAM, "m too large for the covariance kernels");
-  if (band_count(p_pad, m) > kMaxBands) return fail(SKC_EPARAM, "too many covariance bands for p_pad");
+  if (band_count(p_pad, m, kPlanMinRows) > kMaxBands) return fail(SKC_EPARAM, "too many covariance bands for p_pad");
   return SKC_OK;
 }
 
@@ -893,9 +895,9 @@ size_t cov_ws(int64_t n, int32_t m, int32_t p_pad) {
   const char path = cov_path(m, p_pad, n);
   if (path == 't') return covtc_ws(n, m, p_pad);
   if (path == 'g') return (size_t)tri_off(p_pad, p_pad) * sizeof(unsigned long long);
-  const int nb = band_count(p_pad, m);
-  const int g = cov_groups(nb, n);
-  return (size_t)g * tri_off(p_pad, p_pad) * sizeof(unsigned long long) + (size_t)kPlanMaxCtas * 8;
+  // a split launch's tail part may fall under kPlanMinRows and take the smaller band count
+  const int ga = cov_groups(band_count(p_pad, m, n), n), gb = cov_groups(band_count(p_pad, m, 0), n);
+  return (size_t)(ga > gb ? ga : gb) * tri_off(p_pad, p_pad) * sizeof(unsigned long long) + (size_t)kPlanMaxCtas * 8;
 }
 
 static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, int32_t p_pad,
@@ -903,16 +905,16 @@ static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int
   CovParams H;
   const int cap = band_capacity(m, p_pad);
   const bool flat = band_kind(m) == 'f';
-  H.nbands = band_count(p_pad, m);
+  H.nbands = band_count(p_pad, m, n);
   H.groups = cov_groups(H.nbands, n);
   H.cyc = nullptr;
   bool measure = false;
   BandPlan* plan = nullptr;
-  if (flat && cov_adapt_on() && H.nbands * H.groups <= kPlanMaxCtas) {
+  if (flat && cov_adapt_on() && n >= kPlanMinRows && H.nbands * H.groups <= kPlanMaxCtas) {
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_plan_mu);
-    BandPlan& B = g_plans[std::make_tuple(dev, (int)p_pad, (int)m, val_f64)];
+    BandPlan& B = g_plans[std::make_tuple(dev, (int)p_pad, (int)m, val_f64, H.nbands)];
     if (B.nb != H.nbands) {  // first use (or the count changed with the environment)
       B.nb = H.nbands;
       B.updates = 0;
@@ -933,7 +935,7 @@ static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(st, &cs);
     measure = B.h_cyc && B.ev && !B.pending && B.updates <= kPlanUpdates && cs == cudaStreamCaptureStatusNone &&
-              n >= ((int64_t)1 << 20);  // short launches measure start-up, not the bands
+              n >= kPlanMinRows;
     plan = &B;
   } else {
     H.nbands = make_bands(p_pad, cap, H.band_rows);
@@ -992,7 +994,8 @@ int cov_launch(const int32_t* idx, const void* val, int val_f64, int64_t n, int3
   if (path == 't') return covtc_launch(idx, val, val_f64, n, m, p_pad, stats, tri, ws, st);
   if (path == 'g') return cov_launch_global(idx, val, val_f64, n, m, p_pad, stats, tri, ws, st);
   // the kernel addresses a group's rows with 32-bit element offsets: split huge inputs
-  const int groups = cov_groups(band_count(p_pad, m), n);
+  const int ga = cov_groups(band_count(p_pad, m, n), n), gb = cov_groups(band_count(p_pad, m, 0), n);
+  const int groups = ga < gb ? ga : gb;
   int64_t max_rows = (int64_t)groups * ((((int64_t)1 << 31) / m) - kCovWarps);
   if (const char* e = getenv("SKC_COV_SPLIT_ROWS")) max_rows = atoll(e) > 0 ? atoll(e) : max_rows;  // tests
   const size_t vsz = val_f64 ? 8 : 4;
