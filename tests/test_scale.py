@@ -4,7 +4,8 @@ At this size the oracle cannot run the whole job, so the checks are:
 * every row's indices are strictly increasing and in range;
 * 2000 random rows match the oracle bit for bit (indices and fp64 values);
 * covariance additivity: the sums of the two halves equal the sum of the whole, exactly,
-  because the fixed-point accumulator is integer for one shared scale;
+  because the fixed-point accumulator is integer for one shared scale; the same triangle under
+  every band plan of the adaptive K3;
 * the Philox sampler keeps every coordinate with frequency m/p.
 """
 
@@ -67,6 +68,31 @@ def test_covariance_additive_over_halves(big):
         _lib.call("skc_cov_accumulate", h.indices.data_ptr(), h.values.data_ptr(), _lib.F64, h.n, m, p,
                   whole.stats.data_ptr(), tri.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(X.device))
     assert torch.equal(tri, whole.tri)
+
+
+def test_covariance_independent_of_the_band_plan(big, monkeypatch):
+    """K3's band boundaries adapt to measured per-band time over the first launches of a shape
+    (one spare band, two proposals, the best measured plan stays). The fixed-point sums are exact,
+    so every plan -- and the static ten-band plan of SKC_COV_ADAPT=0 -- gives the same triangle."""
+    skc, X, spec, plan, sk = big
+    from paper_1511_00152_b200 import _lib
+
+    n, m, p = sk.n, sk.m, sk.p
+    whole = skc.accumulate_moments(sk)
+    L = _lib.lib()
+
+    def run():
+        tri = torch.zeros_like(whole.tri)
+        ws = _lib.workspace(L.skc_cov_workspace(n, m, p), X.device)
+        _lib.call("skc_cov_accumulate", sk.indices.data_ptr(), sk.values.data_ptr(), _lib.F64, n, m, p,
+                  whole.stats.data_ptr(), tri.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(X.device))
+        torch.cuda.synchronize()
+        return tri
+
+    for _ in range(5):  # entry-balanced, two proposals, the kept plan (twice)
+        assert torch.equal(run(), whole.tri)
+    monkeypatch.setenv("SKC_COV_ADAPT", "0")
+    assert torch.equal(run(), whole.tri)
 
 
 def test_philox_inclusion_uniform_at_scale(big):
