@@ -107,7 +107,11 @@ int skc_mean_finalize(const double *acc, int32_t p, int32_t p_pad, int32_t m, in
  * scale outside the float range, take exact fp64 products. Integer sums make the result
  * deterministic and order-independent. Measured relative Frobenius error against the
  * reference's fp64: 2.5e-9 (C3, n=2^24) to 1.2e-7 (C4, n=2^21), tests/test_full_configs.py;
- * the north_star bound is 1e-5. */
+ * the north_star bound is 1e-5.
+ * For launches of 2^20 rows or more the shared-memory kernel keeps a small per-process table of
+ * band boundaries per (device, p_pad, m, val_dtype) and tunes it over the first three launches from
+ * per-band cycle counts read back asynchronously (pinned memory, no synchronisation); the result
+ * does not depend on it. SKC_COV_ADAPT=0 disables the tuning. */
 size_t skc_cov_workspace(int64_t n, int32_t m, int32_t p_pad);
 int skc_cov_accumulate(const int32_t *idx, const void *val, int32_t val_dtype, int64_t n, int32_t m,
                        int32_t p_pad, const double *stats, double *tri, void *workspace, size_t ws_bytes,
