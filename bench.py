@@ -519,6 +519,10 @@ def cov_line(ctx, wl, args, steps, warmup, compute, sampler="oracle", clocks=Tru
 
     for _ in range(warmup):
         step(mk())
+        # warm-up passes end with a synchronise, as a chunked pipeline's passes do: K3 tunes its band
+        # plan from the previous launch's per-band cycle counts (read back without blocking), so
+        # the previous launch has to have finished when the next one is enqueued
+        torch.cuda.synchronize()
     ctx.barrier()
     evs = [mk() for _ in range(steps)]
     launches0 = L.skc_launch_count()
