@@ -269,8 +269,8 @@ struct CovParams {
   unsigned long long* part;  // [groups][tri_total] int64 fixed-point partials
   int nbands, groups;
   int aligned;               // idx/val 16-byte aligned: tiles may use bulk copies
-  unsigned long long* cyc;   // [groups][nbands] elapsed cycles per band CTA (flat kernel; may be null)
   int band_rows[kMaxBands + 1];
+  unsigned long long* cyc;   // [groups][nbands] end stamps per band CTA + the start stamp, ns (measuring launches)
 };
 
 template <typename V>
@@ -494,7 +494,17 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_band_kernel(const __gri
 //    element is one unsigned compare (indices are sorted, so in-band lanes are [nlo, nhi)).
 //  * The pair loop's induction variable is the pair-table pointer.
 // Rows holding a value above tau (or a wide-range scale) take the exact fp64 path.
-template <typename V, bool PK>  // PK (p_pad <= 2048): U.x packs (row offset of j) << 11 | j
+__device__ __forceinline__ unsigned long long global_timer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// MEASURE: the launch stamps every block's end time for the adaptive band plan (BandPlan). A
+// separate instantiation, because even this one store after all the work moves the kernel's code
+// enough to cost ~2% (8.75 -> 8.90 ms at p = 512, 6.44 -> 6.58 ms at p = 256); the steady-state
+// launches run the kernel without it.
+template <typename V, bool PK, bool MEASURE>  // PK (p_pad <= 2048): U.x packs (row offset of j) << 11 | j
 __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __grid_constant__ CovParams P) {
   extern __shared__ int smem_i[];
   const int m = P.m;
@@ -511,7 +521,6 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __gri
   unsigned long long* part = P.part + (size_t)group * tri_off(P.p_pad, P.p_pad) + e0;
   const uint32_t lo_sh = (uint32_t)__cvta_generic_to_shared(lo);
 
-  const long long tc0 = clock64();  // per-band time for the adaptive band plan (band_plan)
   double tau;
   const int S_ = cov_scale(P.stats, m, &tau);
   const bool wide = cov_wide(S_);
@@ -628,12 +637,17 @@ __global__ void __launch_bounds__(kCovWarps * 32, 1) cov_flat_kernel(const __gri
     __syncwarp();
   }
   __syncthreads();
-  if (threadIdx.x == 0 && P.cyc != nullptr) P.cyc[blockIdx.x] = (unsigned long long)(clock64() - tc0);
   for (int e = threadIdx.x; e < ne; e += blockDim.x) {
     const long long q = (long long)lo[e] - (long long)kBias;
     if (q != 0) atomicAdd(part + e, (unsigned long long)q);
   }
+  // every block stamps its end (%globaltimer); the start stamp comes from cov_stamp_kernel,
+  // launched just before
+  if constexpr (MEASURE) {
+    if (threadIdx.x == 0) P.cyc[blockIdx.x] = global_timer_ns();
+  }
 }
+__global__ void cov_stamp_kernel(unsigned long long* out) { *out = global_timer_ns(); }
 
 __global__ void cov_reduce_kernel(const unsigned long long* __restrict__ part, int groups, int64_t total, int m,
                                   const double* __restrict__ stats, double* __restrict__ tri) {
@@ -782,14 +796,41 @@ static int band_count(int32_t p_pad, int32_t m, int64_t n) {
     ++nb;
   return nb;
 }
-// nb bands balanced by entries (the starting plan); nb is at least the capacity's minimum count
-static void bands_by_entries(int32_t p_pad, int nb, int cap, int* out) {
-  const int64_t total = tri_off(p_pad, p_pad);
-  int64_t t = (total + nb - 1) / nb;
-  while (t < cap && greedy_bands(p_pad, t, nullptr) > nb) t += (t >> 8) + 1;
-  if (t > cap) t = cap;
+// The starting plan: nb bands (at least the capacity's minimum count) balanced on the weight
+// (p - a) + kappa p / m per row a -- its entries plus a fixed cost per row, which is what the
+// measured per-band times at C3 fit (kappa ~ 1; the converged C3 plan gives its last band 8.5%
+// fewer entries than its first). kappa = 0: balanced by entries. The measurements correct it.
+static void bands_by_entries(int32_t p_pad, int nb, int cap, int32_t m, int* out) {
+  double kappa = 1.0;
+  if (const char* e = getenv("SKC_COV_KAPPA")) kappa = atof(e);
+  const double c = kappa > 0.0 ? kappa * (double)p_pad / (double)m : 0.0;
+  auto pack = [&](double W, int* o) {
+    int count = 0, a = 0;
+    while (a < p_pad) {
+      int64_t e = 0;
+      double w = 0.0;
+      int r = a;
+      while (r < p_pad && e + (p_pad - r) <= cap && w + (p_pad - r) + c <= W) {
+        e += p_pad - r;
+        w += (p_pad - r) + c;
+        ++r;
+      }
+      if (r == a) r = a + 1;
+      if (o && count < nb) o[count] = a;
+      ++count;
+      a = r;
+    }
+    if (o && count <= nb) o[count] = p_pad;
+    return count;
+  };
+  double lo = 0.0, hi = (double)tri_off(p_pad, p_pad) + c * p_pad + 1.0;
+  for (int it = 0; it < 60; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (pack(mid, nullptr) <= nb) hi = mid;
+    else lo = mid;
+  }
   int tmp[kMaxBands + 1];
-  const int got = greedy_bands(p_pad, t, tmp);
+  const int got = pack(hi, tmp);
   for (int b = 0; b <= nb; ++b) out[b] = b <= got ? tmp[b] : p_pad;  // fewer bands than asked (tiny p): empty tail
 }
 
@@ -813,7 +854,7 @@ struct BandPlan {
 };
 constexpr int kPlanUpdates = 2;  // proposals; every one is measured, the best measured plan stays (at C3 the
                                  // second is the best: later ones, and damped steps, measured worse)
-constexpr int kPlanMaxCtas = 1024;
+constexpr int kPlanMaxCtas = 1023;  // + the start stamp
 static std::mutex g_plan_mu;
 static std::map<std::tuple<int, int, int, int, int>, BandPlan> g_plans;
 
@@ -821,9 +862,10 @@ static void plan_update(BandPlan& B, int32_t p_pad, int cap) {
   // mean cycles per band over the groups of the measured launch
   double T[kMaxBands], tot = 0.0, mx = 0.0;
   for (int b = 0; b < B.nb; ++b) {
-    double sum = 0.0;
-    for (int g = 0; g < B.groups; ++g) sum += (double)B.h_cyc[(size_t)g * B.nb + b];
-    T[b] = sum / B.groups;
+    double sum = 0.0;  // mean end stamp of the band's CTAs, from the launch's start stamp (ns)
+    const unsigned long long t0 = B.h_cyc[(size_t)B.groups * B.nb];
+    for (int g = 0; g < B.groups; ++g) sum += (double)(B.h_cyc[(size_t)g * B.nb + b] - t0);
+    T[b] = t0 ? sum / B.groups : 0.0;
     if (!(T[b] > 0.0)) return;  // no measurement
     tot += T[b];
     if (T[b] > mx) mx = T[b];
@@ -834,7 +876,7 @@ static void plan_update(BandPlan& B, int32_t p_pad, int cap) {
     for (int b = 0; b <= B.nb; ++b) B.best_rows[b] = B.rows[b];
   }
   if (getenv("SKC_COV_PLAN_LOG")) {
-    fprintf(stderr, "band plan update %d: slowest %.0f cycles, spread %.2f%%, rows", B.updates, mx * (double)B.n_meas,
+    fprintf(stderr, "band plan update %d: slowest %.0f ns, spread %.2f%%, rows", B.updates, mx * (double)B.n_meas,
             100.0 * (mx * (double)B.n_meas * B.nb / tot - 1.0));
     for (int b = 0; b <= B.nb; ++b) fprintf(stderr, " %d", B.rows[b]);
     fprintf(stderr, "\n");
@@ -912,7 +954,7 @@ size_t cov_ws(int64_t n, int32_t m, int32_t p_pad) {
   if (path == 'g') return (size_t)tri_off(p_pad, p_pad) * sizeof(unsigned long long);
   // a split launch's tail part may fall under kPlanMinRows and take the smaller band count
   const int ga = cov_groups(band_count(p_pad, m, n), n), gb = cov_groups(band_count(p_pad, m, 0), n);
-  return (size_t)(ga > gb ? ga : gb) * tri_off(p_pad, p_pad) * sizeof(unsigned long long) + (size_t)kPlanMaxCtas * 8;
+  return (size_t)(ga > gb ? ga : gb) * tri_off(p_pad, p_pad) * sizeof(unsigned long long) + (size_t)(kPlanMaxCtas + 1) * 8;
 }
 
 static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int64_t n, int32_t m, int32_t p_pad,
@@ -935,8 +977,8 @@ static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int
       B.updates = 0;
       B.best_max = 0.0;
       B.pending = false;
-      bands_by_entries(p_pad, B.nb, cap, B.rows);
-      if (B.h_cyc == nullptr && cudaMallocHost(&B.h_cyc, (size_t)kPlanMaxCtas * 8) != cudaSuccess) B.h_cyc = nullptr;
+      bands_by_entries(p_pad, B.nb, cap, m, B.rows);
+      if (B.h_cyc == nullptr && cudaMallocHost(&B.h_cyc, (size_t)(kPlanMaxCtas + 1) * 8) != cudaSuccess) B.h_cyc = nullptr;
       if (B.ev == nullptr && cudaEventCreateWithFlags(&B.ev, cudaEventDisableTiming) != cudaSuccess) B.ev = nullptr;
       cudaGetLastError();
     }
@@ -978,13 +1020,15 @@ static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int
                            : (size_t)((maxe + 1) & ~1) * 4 + (size_t)((maxr + 1) & ~1) * 4 + pair_table_bytes(m) +
                                  (size_t)kCovWarps * m * 16;
   const bool pk = p_pad <= 2048;  // the packed U.x of the flat kernel
-  auto k = val_f64 ? (m > 64 ? cov_band_kernel<double, true>
-                             : flat ? (pk ? cov_flat_kernel<double, true> : cov_flat_kernel<double, false>)
-                                    : cov_band_kernel<double, false>)
-                   : (m > 64 ? cov_band_kernel<float, true>
-                             : flat ? (pk ? cov_flat_kernel<float, true> : cov_flat_kernel<float, false>)
-                                    : cov_band_kernel<float, false>);
+  auto flat_kernel = [&](auto v) {
+    using V = decltype(v);
+    return pk ? (measure ? cov_flat_kernel<V, true, true> : cov_flat_kernel<V, true, false>)
+              : (measure ? cov_flat_kernel<V, false, true> : cov_flat_kernel<V, false, false>);
+  };
+  auto k = val_f64 ? (m > 64 ? cov_band_kernel<double, true> : flat ? flat_kernel(double()) : cov_band_kernel<double, false>)
+                   : (m > 64 ? cov_band_kernel<float, true> : flat ? flat_kernel(float()) : cov_band_kernel<float, false>);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (measure) cov_stamp_kernel<<<1, 1, 0, st>>>(H.cyc + (size_t)H.nbands * H.groups);
   k<<<H.nbands * H.groups, kCovWarps * 32, smem, st>>>(H);
   int rc = check_launch("cov_band_kernel");
   if (rc) return rc;
@@ -992,7 +1036,7 @@ static int cov_launch_part(const int32_t* idx, const void* val, int val_f64, int
     std::lock_guard<std::mutex> lk(g_plan_mu);
     plan->groups = H.groups;
     plan->n_meas = n;
-    if (cudaMemcpyAsync(plan->h_cyc, H.cyc, (size_t)H.nbands * H.groups * 8, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+    if (cudaMemcpyAsync(plan->h_cyc, H.cyc, ((size_t)H.nbands * H.groups + 1) * 8, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
         cudaEventRecord(plan->ev, st) == cudaSuccess)
       plan->pending = true;
     cudaGetLastError();
