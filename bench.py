@@ -379,20 +379,22 @@ def run_reference(args, cfg):
     nthreads = os.cpu_count() or 1
     sample = min(cfg["n"], 1 << 16 if cfg["p"] >= 1024 else 1 << 17)
     rows = gen_rows_np(args.workload, sample)
-    per_step = []
+    per_step, per_step_s = [], []
     for i in range(args.warmup + args.steps):
         if cfg["kind"] == "cov":
-            rate, _ = cpu_cov_rate(rows, cfg, nthreads, min_seconds=0.0)
+            rate, el = cpu_cov_rate(rows, cfg, nthreads, min_seconds=0.0)
         else:
-            rate, _ = cpu_kmeans_rate(rows, cfg, nthreads, min_seconds=0.0)
+            rate, el = cpu_kmeans_rate(rows, cfg, nthreads, min_seconds=0.0)
         if i >= args.warmup:
             per_step.append(rate)
+            per_step_s.append(el)
     value = statistics.median(per_step)
     unit = "samples/s" if cfg["kind"] == "cov" else "point-iters/s"
     desc = f"{sample} rows of {args.workload}, oracle port (C) with {nthreads} threads"
     out = {
         "impl": "reference", "metric": metric_name(cfg), "value": value, "unit": unit, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": args.scaling,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(per_step_s),
+        "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (numpy, same generative model)",
         "config": {"workload": args.workload, "desc": cfg["desc"], "p": cfg["p"], "m": cfg["m"]},
         "cpu_baseline": {"value": value, "unit": unit, "cores": nthreads, "kind": "port", "sample": desc},
